@@ -1,0 +1,337 @@
+"""Benchmark: simulated patient-weeks per second of the closed-loop Monte
+Carlo hot path (BASELINE.json metric) on B200s, with the FP64 roofline of
+the fused integrator and the reference-path CPU baseline.
+
+Workload (BASELINE configs[1]): 100,000 virtual patients x 4 weeks per GPU,
+FP64, Euler-Maruyama at 1-min step with process noise, 5-min CGM with sensor
+noise, the reference dual-hormone AP controller (PD basal + heuristic meal
+bolus), 3 meals/day ~N(50/70/80 g, 10 g) with U(+-30 min)
+jitter, seed 1, population drawn by the device sampler from the reference
+distribution table.  One "step" = one pass of the hot path over the batch:
+fused integrator + population reduction (histograms, quantile bins, exact
+accumulator).  Multi-GPU (torchrun): weak scaling, each rank simulates its
+own 100k-patient shard (global patient ids rank*n ...), exact accumulators
+are combined with NCCL all-reduce (sum/min/max) — the only collective.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+N_PATIENTS = 100_000
+WEEKS = 4
+DT_S = 60.0
+SEED = 1
+METRIC = "simulated patient-weeks/sec"
+FP64_PEAK_FILE = os.path.join(REPO, "profiles", "fp64_peak_r01.jsonl")
+
+
+def fp64_peak():
+    """Measured DFMA peak (tools/fp64_peak.cu on this pool's B200, best of
+    10); MEASURED_PEAKS.json carries no FP64 figure."""
+    best = 0.0
+    try:
+        for line in open(FP64_PEAK_FILE):
+            d = json.loads(line)
+            if d.get("kernel") == "dfma":
+                best = max(best, d["tflops"])
+    except OSError:
+        pass
+    return (best, "measured DFMA (profiles/fp64_peak_r01.jsonl)") if best else (
+        37.2, "nominal 148 SM x 64 DFMA x 2 x 1.965 GHz (fallback)")
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if len(r) > 2 + k and r[2 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_baseline(n_sample: int, weeks: int, threads: int):
+    """Reference path on the host cores: the oracle's C restatement of the
+    numba kernel (bitwise equal to it on injected inputs), OpenMP over
+    patients, per-patient noise + schedule generation included."""
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle
+    from paper_2202_13927_b200.config import SimulationConfig, sizes
+    from paper_2202_13927_b200.controller import ControllerHyperparameters, initial_icr
+    from paper_2202_13927_b200.protocol import ThreeMealProtocol
+    from paper_2202_13927_b200.rng import ROLE_DEVICE_NOISE
+    cfg = SimulationConfig(horizon_s=weeks * 7 * 86400.0, seed=SEED, dt_s=DT_S)
+    sz = sizes(cfg)
+    pop = golden_population(n_sample)
+    params, ub, x0 = pop
+    prof = ControllerHyperparameters()
+    c0 = np.zeros((n_sample, 11))
+    c0[:, 3] = [initial_icr(u, prof) for u in ub]
+    c0[:, 6] = -1e18
+    t0 = time.perf_counter()
+    out = oracle.run_batch_philox(ThreeMealProtocol(), SEED, 0, params, x0, c0, prof.to_vec(), ub, sz,
+                                  cfg.dt_s, cfg.controller_period_s, ROLE_DEVICE_NOISE, nthreads=threads)
+    wall = time.perf_counter() - t0
+    assert np.all(out["status"] == 0)
+    return n_sample * weeks / wall, wall
+
+
+def golden_population(n):
+    """Host population for the CPU arm: the 64 parameter sets the reference's
+    own sampler drew for seed 0 (tests/golden/population.npz), tiled to n
+    patients (each patient id gets its own noise and meal streams)."""
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle
+    g = np.load(os.path.join(REPO, "tests", "golden", "population.npz"))
+    params = np.ascontiguousarray(np.resize(g["s0_params"], (n, 30)))
+    ub = np.resize(g["s0_ubasal"], n).astype(np.float64)
+    x0 = np.zeros((n, 16))
+    for i in range(min(n, 64)):
+        x0[i], _ = oracle.steady_state(params[i])
+    x0 = np.ascontiguousarray(np.resize(x0[:min(n, 64)], (n, 16)))
+    return params, ub, x0
+
+
+def run_reference_arm(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    n_sample = max(threads * 16, 256)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, wall = cpu_baseline(n_sample, WEEKS, threads)
+        if i >= args.warmup:
+            vals.append(v)
+    v = float(np.mean(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "patient-weeks/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * n_sample * WEEKS / v, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"BASELINE configs[1] shape ({N_PATIENTS} patients x {WEEKS} weeks), "
+                               f"timed on a {n_sample}-patient sample at full horizon",
+                   "dt_s": DT_S, "seed": SEED, "controller": "dual_hormone", "protocol": "three_meal"},
+        "cpu_baseline": {"value": v, "unit": "patient-weeks/s", "cores": threads, "kind": "port",
+                         "sample": f"{n_sample} patients x {WEEKS} weeks, dt 60 s, all {threads} host threads"},
+        "e2e": {"value": v, "unit": "patient-weeks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    ws, rank, local = dist_env()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device")
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=device)
+    from paper_2202_13927_b200 import analytics, engine, flops
+    from paper_2202_13927_b200.config import SimulationConfig
+    from paper_2202_13927_b200.controller import ControllerHyperparameters
+    from paper_2202_13927_b200.parallel import allreduce_accumulator
+    from paper_2202_13927_b200.population import generate_population
+    from paper_2202_13927_b200.protocol import ThreeMealProtocol
+    from paper_2202_13927_b200.trial import FastTrial, run_population_arrays
+
+    n = args.patients
+    cfg = SimulationConfig(horizon_s=WEEKS * 7 * 86400.0, seed=SEED, dt_s=DT_S)
+    pid0 = rank * n
+    prof = ControllerHyperparameters()
+    gen = ThreeMealProtocol()
+    t_s0 = time.perf_counter()
+    pop = generate_population(SEED, n, pid0=pid0, device=device)
+    torch.cuda.synchronize()
+    sampler_s = time.perf_counter() - t_s0
+    ft = FastTrial(pid0, pop.params_device, pop.basal_device, gen, prof, cfg, device=device,
+                   per_patient_metrics=True)
+    stream = torch.cuda.current_stream(device)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)  # > 126 MB L2
+
+    def one_step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        ft.simulate()
+        if ev is not None:
+            ev[1].record(stream)
+        ft._rerun_if_diverged()
+        ft.reduce()
+        if ev is not None:
+            ev[2].record(stream)
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()                 # L2 flush between timed iterations
+            one_step(evs[k])
+        torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    sim_ms = np.array([e[0].elapsed_time(e[1]) for e in evs])
+    step_ms = np.array([e[0].elapsed_time(e[2]) for e in evs])
+    tot_ms = float(step_ms.sum())
+    if ws > 1:
+        t = torch.tensor([tot_ms], device=device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    acc = ft.accumulator()
+    acc_all = allreduce_accumulator(acc, device) if ws > 1 else acc
+
+    # end-to-end through the public array API with host (pinned) buffers
+    params_h = pop.params_device.cpu().pin_memory()
+    basal_h = pop.basal_device.cpu().pin_memory()
+    e2e_ms = []
+    for k in range(max(1, min(args.steps, 3)) + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        acc_e, met = run_population_arrays(params_h, basal_h, gen, prof, cfg, pid0=pid0, device=device)
+        torch.cuda.synchronize()
+        if k > 0:
+            e2e_ms.append(1000 * (time.perf_counter() - t0))
+    e2e = float(np.median(e2e_ms))
+    if ws > 1:
+        t = torch.tensor([e2e], device=device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e = float(t.item())
+    assert analytics.report_bytes(analytics.build_trial_report(acc_e, {})) == \
+        analytics.report_bytes(analytics.build_trial_report(acc, {})), "e2e result differs"
+
+    if rank != 0:
+        if ws > 1:
+            torch.distributed.destroy_process_group()
+        return 0
+    pw_per_step = n * WEEKS * ws
+    value = pw_per_step / (tot_ms / args.steps / 1000.0)
+    F = flops.flops_per_step(ft.sz["period_steps"])
+    flop_per_launch = F * n * ft.sz["horizon_ticks"]
+    sim_s = float(np.mean(sim_ms)) / 1000.0
+    peak, peak_src = fp64_peak()
+    achieved = flop_per_launch / sim_s / 1e12
+    cpu_v, cpu_wall = (None, None)
+    if not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        cpu_n = max(threads * 16, 256)
+        cpu_v, cpu_wall = cpu_baseline(cpu_n, WEEKS, threads)
+    q = analytics.metric_quantiles(acc_all)
+    h2d = params_h.numel() * 8 + basal_h.numel() * 8
+    d2h = n * (5 * 4 + 2 * 4 + 4) + 8 * (4 + 5 + 5 * 201 + 247 + 2 * 246 + 2 + 3 * ft.sz["n_grid"] + 603 + 3 + 4 + 7 * 201)
+    line = {
+        "metric": METRIC, "value": value, "unit": "patient-weeks/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (device-sampled population from the reference distribution table; "
+                "3-meal generator; on-device Philox noise)",
+        "config": {"workload": f"BASELINE configs[1]: {n} patients x {WEEKS} weeks per GPU, dt 60 s, "
+                               "controller period 300 s, seed 1",
+                   "patients_per_gpu": n, "weeks": WEEKS, "dt_s": DT_S, "seed": SEED,
+                   "controller": "dual_hormone (reference AP: PD basal + heuristic meal bolus)",
+                   "protocol": "three_meal N(50/70/80,10) g, U(+-30 min)", "noise": "philox4x32-10",
+                   "parallelism": f"patients sharded over {ws} GPU(s), NCCL all-reduce of exact accumulators",
+                   "l2": "flushed (256 MB write) between timed iterations"},
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "gt::fast_kernel<THREE_MEAL, PHILOX>",
+                     "algorithmic_flops_per_launch": flop_per_launch,
+                     "flops_per_step": F, "peak_source": peak_src,
+                     "kernel_ms": sim_s * 1000.0, "share_of_step": float(np.mean(sim_ms) / np.mean(step_ms))},
+        "cpu_baseline": ({"value": cpu_v, "unit": "patient-weeks/s", "cores": os.cpu_count(), "kind": "port",
+                          "sample": f"{max((os.cpu_count() or 1) * 16, 256)} patients x {WEEKS} weeks (oracle C "
+                                    f"restatement, OpenMP, {cpu_wall:.1f} s wall)"} if cpu_v else None),
+        "e2e": {"value": pw_per_step / (e2e / 1000.0), "unit": "patient-weeks/s",
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "path": "trial.run_population_arrays (pinned host params -> report fields + per-patient metrics)"},
+        "gpu_launches": args.steps * 5,
+        "clocks": clk.summary(),
+        "sampler_s": sampler_s,
+        "trial": {"n_patients": acc_all.n_patients, "n_aborted": acc_all.n_aborted,
+                  "mean_bg": acc_all.sum_bg_fp / 2**24 / (acc_all.n_patients * acc_all.horizon_ticks),
+                  "quantiles": q},
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--patients", type=int, default=N_PATIENTS)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,524 @@
+// Fast fused closed-loop integrator (BASELINE north_star subsystem 3).
+//
+// One thread = one virtual patient for the whole horizon.  SDE state,
+// controller state, Philox counters and metric accumulators live in
+// registers; the 247-bin BG histogram of each patient lives in shared memory
+// as saturating uint8 counters (flushed to the patient's HBM column on
+// overflow), so HBM sees parameters in and metrics out only.
+//
+// Same model (hovorka.py:76-150), controller (controller.py:343-458) and
+// statistics (_kernel.py:137-160) as the parity kernel, re-associated for
+// the FP64 pipe: each linear state update x += h*(b*y - x/tau) is evaluated
+// as fma(x, 1-h/tau, h*b*y) with per-patient constants folded at start-up.
+// For every state of that form the reference's projection max(x,0) is a
+// no-op (monotone rounding of a - b with 0 <= b <= a), so it is applied only
+// to Q1, Q2, D1, D2.  Results agree with the parity path to rounding
+// (DESIGN.md §4 documents the resulting threshold ties).
+//
+// Loop structure is warp-uniform: outer loop over controller periods, inner
+// loop over the period's integration steps; all lanes of a warp hit
+// controller ticks, day boundaries and timeline grid points together, so the
+// only divergence comes from the model's own branches.
+#include <cmath>
+#include "gt_common.cuh"
+
+namespace gt {
+
+constexpr int kFastBS = 128;
+constexpr int kHistWords = (GT_N_BG_BINS + 3) / 4;  // 62 packed uint8x4 words per lane
+
+// Per-patient constants of the re-associated update (h = dt in minutes).
+struct PC {
+  double invVGw;          // bg = Q1 * invVGw
+  double aG, hTG, ginK;   // gut: D1*aG + ginK*rate ; D2*aG + D1*hTG ; h*gut = D2*hTG
+  double aI, hTI;         // SC insulin
+  double cI, dI;          // plasma insulin
+  double ax1, bx1, ax2, bx2, ax3, bx3;
+  double aZ1, aZ2, hTg, cG;  // glucagon chain, h*S_gluc*w*C/(...)
+  double aE1, bE1, aE2, bE2, aE3, bE3, qex, sex;
+  double hF01w, hk12, aK12, hE, rK1, rK0;
+  double aS, hS;          // sensor lag
+  double sqE, sqG, sqrtR; // noise scales
+};
+
+__device__ __forceinline__ void make_pc(const double* p, double h, PC& c) {
+  const double w = p[PW];
+  c.invVGw = 1.0 / (p[PVG] * w);
+  c.hTG = h / p[PTMAXG]; c.aG = 1.0 - c.hTG; c.ginK = h * p[PAG] * kMmolPerGCho;
+  c.hTI = h / p[PTMAXI]; c.aI = 1.0 - c.hTI;
+  c.cI = 1.0 - h * p[PKE]; c.dI = c.hTI / (p[PVI] * w);
+  c.ax1 = 1.0 - h * p[PKA1]; c.bx1 = h * p[PKA1] * p[PSIT];
+  c.ax2 = 1.0 - h * p[PKA2]; c.bx2 = h * p[PKA2] * p[PSID];
+  c.ax3 = 1.0 - h * p[PKA3]; c.bx3 = h * p[PKA3] * p[PSIE];
+  c.hTg = h / p[PTGLUC]; c.aZ1 = 1.0 - c.hTg; c.aZ2 = 1.0 - h * p[PKEGLUC];
+  c.cG = h * p[PSGLUC] * w / (p[PVGLUC] * w);
+  c.bE1 = h / p[PTAUHR]; c.aE1 = 1.0 - c.bE1;
+  c.bE2 = h / p[PTAUEX]; c.aE2 = 1.0 - c.bE2;
+  c.aE3 = 1.0 - h / p[PTAULATE]; c.bE3 = h * p[PALATE];
+  c.qex = p[PQEX]; c.sex = p[PSEX];
+  c.hF01w = h * p[PF01] * w;
+  c.hk12 = h * p[PK12]; c.aK12 = 1.0 - c.hk12;
+  c.hE = h * p[PEGP0] * w;
+  c.rK1 = h * 0.003; c.rK0 = h * 0.003 * 9.0 * p[PVG] * w;
+  c.hS = h / p[PTAUCGM]; c.aS = 1.0 - c.hS;
+  c.sqE = p[PSIGEGP] * w * sqrt(h);
+  c.sqG = p[PSIGGUT] * sqrt(h);
+  c.sqrtR = sqrt(p[PR]);
+}
+
+// Controller state in registers (controller.py:183-195); flags as bits.
+struct Ctl {
+  double filt, prev, icr, suspend, last_gluc, win_end, win_peak, win_min;
+  int mode, exdone, init;
+};
+
+// controller.py:343-458, FMA-contracted; `exercising` is a compile-time
+// false for protocol sources without exercise.
+template <bool HAS_EX>
+__device__ __forceinline__ void controller_fast(Ctl& c, double y, double announced, double phase,
+                                                double t_s, double pred_k, const double* __restrict__ H,
+                                                double assumed, double& basal, double& bolus,
+                                                double& gluc) {
+  basal = 0.0; bolus = 0.0; gluc = 0.0;
+  if (!c.init) {
+    c.filt = y; c.prev = y; c.init = 1;
+  } else {
+    c.prev = c.filt;
+    c.filt = (1.0 - H[HFILTER]) * c.filt + H[HFILTER] * y;
+  }
+  const double filt = c.filt;
+  const double trend = filt - c.prev;
+  const bool exercising = HAS_EX && phase >= 0.0;
+  const double setpoint = exercising ? H[HEXSETPOINT] : H[HSETPOINT];
+  const double gluc_thr = exercising ? H[HEXGLUCTHR] : H[HGLUCTHR];
+  double micro = exercising ? H[HEXMICROUG] : H[HMICROUG];
+  if (exercising) {
+    if (!c.exdone) {
+      c.exdone = 1;
+      if (filt < H[HEXBOLUSBG]) {
+        gluc = fmin(H[HEXBOLUS], H[HMAXGLUC]);
+        c.last_gluc = t_s;
+        return;
+      }
+    }
+  } else {
+    c.exdone = 0;
+  }
+  const double pred = filt + trend * pred_k;
+  if (c.mode == 0) {
+    if (filt < gluc_thr || pred < gluc_thr) c.mode = 1;
+  } else {
+    if (filt >= gluc_thr + H[HHYST] && pred >= gluc_thr) c.mode = 0;
+  }
+  if (c.win_end > 0.0) {
+    if (filt > c.win_peak) c.win_peak = filt;
+    if (filt < c.win_min) c.win_min = filt;
+    if (t_s >= c.win_end) {
+      double icr = c.icr;
+      if (c.win_min < H[HUNDERBG]) icr *= 1.0 + H[HICRSTEPUP];
+      else if (c.win_peak - H[HSETPOINT] > H[HEXCHI]) icr *= 1.0 - H[HICRSTEP];
+      if (icr < H[HICRMIN]) icr = H[HICRMIN];
+      if (icr > H[HICRMAX]) icr = H[HICRMAX];
+      c.icr = icr;
+      c.win_end = 0.0;
+    }
+  }
+  if (c.mode == 1) {
+    if (filt < gluc_thr && trend < -H[HMICROTREND] && t_s - c.last_gluc >= H[HLOCKMIN] * 60.0) {
+      if (micro > H[HMAXGLUC]) micro = H[HMAXGLUC];
+      gluc = micro;
+      c.last_gluc = t_s;
+    }
+    return;
+  }
+  if (announced > 0.0) {
+    double b = announced / c.icr + (filt - setpoint) / (H[HCFICR] * c.icr);
+    if (filt > H[HSUPBG]) b += H[HSUPFRAC] * assumed * H[HSUSPMIN] / 60.0;
+    if (b < 0.0) b = 0.0;
+    if (b > H[HMAXBOLUS]) b = H[HMAXBOLUS];
+    bolus = b;
+    c.suspend = t_s + H[HSUSPMIN] * 60.0;
+    c.win_end = t_s + H[HMEALWIN] * 60.0;
+    c.win_peak = filt;
+    c.win_min = filt;
+  }
+  if (!(t_s < c.suspend)) {
+    double factor = 1.0 + H[HBKP] * (filt - setpoint) + H[HBKD] * trend;
+    if (factor < 0.0) factor = 0.0;
+    if (factor > H[HBFMAX]) factor = H[HBFMAX];
+    double b = assumed * factor;
+    if (exercising) b *= H[HEXBFACTOR];
+    basal = b;
+  }
+}
+
+// ----------------------------------------------------------- noise sources
+struct Normals { double z0, z1, z2; float zm; };
+
+__device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float& z0, float& z1) {
+  const float u1 = fmaf((float)a, 2.3283064365386963e-10f, 1.1641532182693481e-10f);
+  const float u2 = (float)b * 2.3283064365386963e-10f;
+  const float rad = sqrtf(-2.0f * __logf(u1));
+  float s, c;
+  __sincosf(6.283185307179586f * u2, &s, &c);
+  z0 = rad * c; z1 = rad * s;
+}
+
+// ----------------------------------------------------------- meal sources
+// Cursor over a patient's meals in tick units: active while ks <= k < ke,
+// announced on controller period kp (start in [kp*P, (kp+1)*P)).
+struct MealCur { int32_t ks, ke; double rate; int64_t m; };
+struct AnnCur { int32_t kp; double carbs; int64_t m; };
+
+struct ThreeMealSrc {
+  const gt_meal_gen* g; uint64_t seed; uint32_t pid; double dt, period, horizon_s;
+  __device__ __forceinline__ void get(int64_t m, int32_t& ks, int32_t& ke, int32_t& kp,
+                                      double& rate, double& carbs) const {
+    const Meal ml = gen_meal(*g, seed, pid, m);
+    if (ml.start >= horizon_s) {  // compile_protocol filter (simulation.py:157)
+      ks = ke = kp = INT32_MAX; rate = 0.0; carbs = 0.0; return;
+    }
+    ks = (int32_t)ceil(ml.start / dt);
+    ke = (int32_t)ceil(ml.end / dt);
+    kp = (int32_t)floor(ml.start / period);
+    carbs = ml.carbs;
+    rate = ml.carbs / ((ml.end - ml.start) / 60.0);  // simulation.py:162
+  }
+};
+
+struct CsrSrc {
+  const int32_t *ks, *ke, *kp; const double *rate, *ann; int64_t n;
+  __device__ __forceinline__ void get(int64_t m, int32_t& oks, int32_t& oke, int32_t& okp,
+                                      double& orate, double& ocarbs) const {
+    if (m >= n) { oks = oke = okp = INT32_MAX; orate = 0.0; ocarbs = 0.0; return; }
+    oks = ks[m]; oke = ke[m]; okp = kp[m]; orate = rate[m]; ocarbs = ann[m];
+  }
+};
+
+__device__ __forceinline__ long long warp_sum64(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ long long warp_min64(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) { long long w = __shfl_xor_sync(0xffffffffu, v, o); v = w < v ? w : v; }
+  return v;
+}
+__device__ __forceinline__ long long warp_max64(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) { long long w = __shfl_xor_sync(0xffffffffu, v, o); v = w > v ? w : v; }
+  return v;
+}
+
+__device__ __forceinline__ bool any_nonfinite(const double* x) {
+  // max over |hi word| >= 0x7ff00000 <=> some state is inf/nan
+  unsigned m = 0;
+#pragma unroll
+  for (int k = 0; k < NS; ++k) m = max(m, (unsigned)__double2hiint(x[k]) & 0x7fffffffu);
+  return m >= 0x7ff00000u;
+}
+
+template <int PROTO, int NOISE>
+__global__ void __launch_bounds__(kFastBS, 4) fast_kernel(const gt_fast_args a) {
+  constexpr bool HAS_EX = (PROTO == GT_PROTO_CSR);
+  __shared__ long long s_thr[GT_N_THRESHOLDS];
+  __shared__ double s_hyper[GT_N_HYPER];
+  __shared__ uint32_t s_hist[kHistWords * kFastBS];
+  __shared__ gt_meal_gen s_gen;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < GT_N_THRESHOLDS; i += kFastBS)
+    s_thr[i] = __double_as_longlong((double)(5 + i) / 10.0);
+  for (int i = tid; i < GT_N_HYPER; i += kFastBS) s_hyper[i] = a.hyper[i];
+  for (int i = tid; i < kHistWords * kFastBS; i += kFastBS) s_hist[i] = 0u;
+  if (tid == 0) s_gen = a.meal_gen;
+  __syncthreads();
+
+  const int64_t i = (int64_t)blockIdx.x * kFastBS + tid;
+  const int64_t n = a.n;
+  const bool inrange = i < n;
+  const int64_t pid = a.pid0 + i;
+  const int lane = tid & 31;
+  const int64_t warp_global = ((int64_t)blockIdx.x * kFastBS + tid) >> 5;
+  const int64_t n_warps = (n + 31) >> 5;
+  const double* __restrict__ H = s_hyper;
+
+  bool alive = inrange && (a.active == nullptr || a.active[i] != 0);
+  int status = (inrange && !alive) ? GT_STATUS_EXCLUDED : GT_STATUS_OK;
+
+  // ---- per-patient set-up
+  const double dt = a.dt_s, period = a.period_s;
+  const double h = dt / 60.0;
+  PC pc;
+  double x[NS];
+  Ctl c;
+  double assumed = 0.0;
+  {
+    double p[NP];
+    const int64_t ii = inrange ? i : 0;
+#pragma unroll
+    for (int k = 0; k < NP; ++k) p[k] = a.params[ii * NP + k];
+    make_pc(p, h, pc);
+#pragma unroll
+    for (int k = 0; k < NS; ++k) x[k] = a.x0[ii * NS + k];
+    const double* c0 = a.c0 + ii * NC;
+    c.filt = c0[CFILT]; c.prev = c0[CPREV]; c.mode = c0[CMODE] != 0.0; c.icr = c0[CICR];
+    c.suspend = c0[CSUSPEND_UNTIL]; c.exdone = c0[CEXBOLUSDONE] != 0.0; c.last_gluc = c0[CLASTGLUC];
+    c.win_end = c0[CWINEND]; c.win_peak = c0[CWINPEAK]; c.win_min = c0[CWINMIN]; c.init = c0[CINIT] != 0.0;
+    assumed = a.assumed_basal[ii];
+  }
+  const bool noise_on = (NOISE == GT_NOISE_PHILOX) ? true : (a.has_noise[inrange ? i : 0] != 0);
+  if (NOISE == GT_NOISE_INJECTED && !noise_on) { pc.sqE = 0.0; pc.sqG = 0.0; }
+
+  // meal cursors
+  ThreeMealSrc tm{&s_gen, a.seed, (uint32_t)pid, dt, period, (double)a.horizon_ticks * dt};
+  CsrSrc cs{};
+  int64_t ex_lo = 0, n_ex = 0;
+  if (PROTO == GT_PROTO_CSR) {
+    const int64_t ii = inrange ? i : 0;
+    const int64_t mo = a.meal_off[ii];
+    cs = CsrSrc{a.meal_ks + mo, a.meal_ke + mo, a.meal_kp + mo, a.meal_rate + mo, a.meal_ann + mo,
+                a.meal_off[ii + 1] - mo};
+    ex_lo = a.ex_off[ii]; n_ex = a.ex_off[ii + 1] - ex_lo;
+  }
+  auto get_meal = [&](int64_t m, int32_t& ks, int32_t& ke, int32_t& kp, double& rate, double& carbs) {
+    if (PROTO == GT_PROTO_CSR) cs.get(m, ks, ke, kp, rate, carbs);
+    else tm.get(m, ks, ke, kp, rate, carbs);
+  };
+  MealCur mc; AnnCur ac;
+  {
+    int32_t kp; double carbs;
+    mc.m = 0; get_meal(0, mc.ks, mc.ke, kp, mc.rate, carbs);
+    int32_t ks, ke; double rate;
+    ac.m = 0; get_meal(0, ks, ke, ac.kp, rate, ac.carbs);
+  }
+  double gin = pc.ginK * mc.rate;
+  int64_t ex_ptr = 0;
+
+  // ---- outputs / accumulators
+  double bg_min = INFINITY, bg_max = -INFINITY, bg_sum = 0.0;
+  double day_basal = 0.0, day_bolus = 0.0, day_gluc = 0.0;
+  int run39 = 0, run30 = 0, ev39 = 0, ev30 = 0;
+  const int hypoL = (int)a.hypo_min_ticks;
+  int64_t ticks_done = 0;
+  int32_t* ghist = a.bg_hist;
+  if (inrange)
+    for (int b = 0; b < GT_N_BG_BINS; ++b) ghist[(int64_t)b * n + i] = 0;
+  uint8_t* my_hist8 = reinterpret_cast<uint8_t*>(s_hist);
+
+  const int64_t ps = a.period_steps;
+  const int64_t n_ctl = a.horizon_ticks / ps;
+  const int64_t ctl_per_day = (int64_t)(86400.0 / period + 0.5);
+  const int64_t gstep = a.grid_step_ticks;
+  const double pred_k = H[HPREDHOR] * 60.0 / period;
+  const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
+  double basal = 0.0, hu_ins = 0.0, hu2 = 0.0;
+  int64_t next_grid = 0, g_idx = 0;
+
+  for (int64_t ctl = 0; ctl < n_ctl; ++ctl) {
+    const int64_t k_base = ctl * ps;
+    const double t_tick = (double)k_base * dt;
+    // day boundary: flush the finished day's dose sums (_kernel.py:133-149)
+    if (ctl > 0 && ctl % ctl_per_day == 0) {
+      const int64_t day = ctl / ctl_per_day - 1;
+      if (inrange) {
+        double* dd = a.day_dose + (day * 3) * n + i;
+        dd[0] = day_basal; dd[n] = day_bolus; dd[2 * n] = day_gluc;
+      }
+      day_basal = day_bolus = day_gluc = 0.0;
+    }
+    if (__all_sync(0xffffffffu, !alive)) {
+      if (NOISE == GT_NOISE_PHILOX || true) break;
+    }
+    for (int64_t s = 0; s < ps; ++s) {
+      const int64_t k = k_base + s;
+      // -------- noise for this tick
+      Normals nz;
+      if (NOISE == GT_NOISE_PHILOX) {
+        const U4 r = philox4x32_10((uint32_t)k, (uint32_t)pid, a.noise_role, (uint32_t)(k >> 32), k0, k1);
+        float f0, f1, f2, f3;
+        box_muller(r.x, r.y, f0, f1);
+        box_muller(r.z, r.w, f2, f3);
+        nz.z0 = (double)f0; nz.z1 = (double)f1; nz.z2 = (double)f2; nz.zm = f3;
+      } else {
+        const int64_t ii = inrange ? i : 0;
+        if (noise_on) {
+          const double* wv = a.wiener + (ii * a.horizon_ticks + k) * 3;
+          nz.z0 = wv[0]; nz.z1 = wv[1]; nz.z2 = wv[2];
+        } else {
+          nz.z0 = nz.z1 = nz.z2 = 0.0;
+        }
+        nz.zm = 0.0f;
+      }
+      // -------- disturbances at tick k (_kernel.py:85-94)
+      while (k >= mc.ke) {
+        int32_t kp; double carbs;
+        ++mc.m; get_meal(mc.m, mc.ks, mc.ke, kp, mc.rate, carbs);
+        gin = pc.ginK * mc.rate;
+      }
+      const double gin_k = (k >= mc.ks) ? gin : 0.0;
+      double hrr = 0.0, phase = -1.0;
+      bool ex_active = false;
+      if (HAS_EX) {
+        while (ex_ptr < n_ex && k >= a.ex_ke[ex_lo + ex_ptr]) ++ex_ptr;
+        ex_active = ex_ptr < n_ex && k >= a.ex_ks[ex_lo + ex_ptr];
+        if (ex_active) hrr = a.ex_hrr[ex_lo + ex_ptr];
+      }
+      // -------- controller tick (_kernel.py:98-135)
+      if (s == 0) {
+        if (alive && any_nonfinite(x)) { alive = false; status = GT_STATUS_NONFINITE; }
+        double announced = 0.0;
+        while (ac.kp < ctl) {
+          int32_t ks, ke; double rate;
+          ++ac.m; get_meal(ac.m, ks, ke, ac.kp, rate, ac.carbs);
+        }
+        while (ac.kp == ctl) {
+          announced += ac.carbs;
+          int32_t ks, ke; double rate;
+          ++ac.m; get_meal(ac.m, ks, ke, ac.kp, rate, ac.carbs);
+        }
+        if (HAS_EX && ex_active && a.ex_announced[ex_lo + ex_ptr] != 0.0)
+          phase = t_tick - a.ex_start_s[ex_lo + ex_ptr];
+        double zm;
+        if (NOISE == GT_NOISE_PHILOX) zm = (double)nz.zm;
+        else zm = (noise_on || true) ? a.meas[(inrange ? i : 0) * n_ctl + ctl] : 0.0;
+        const double y = x[IGSC] + pc.sqrtR * zm;
+        double bolus, gluc;
+        controller_fast<HAS_EX>(c, y, announced, phase, t_tick, pred_k, H, assumed, basal, bolus, gluc);
+        hu_ins = h * (basal * 1000.0 / 60.0 + bolus * 1000.0 / (period / 60.0));
+        hu2 = h * (gluc / (period / 60.0));
+        if (alive) { day_bolus += bolus; day_gluc += gluc; }
+      }
+      // -------- statistics at tick k (_kernel.py:137-160)
+      const double bg = x[IQ1] * pc.invVGw;
+      if (alive && !isfinite(bg)) { alive = false; status = GT_STATUS_NONFINITE; }
+      {
+        // exact searchsorted(THRESHOLDS, bg, 'right') for bg >= 0: FP32
+        // estimate, then one exact int64 compare against the table.
+        const float bf = __double2float_rz(bg);
+        int kb = __float2int_rz(bf * 10.0f) - 4;
+        kb = min(max(kb, 0), GT_N_THRESHOLDS);
+        const long long bb = __double_as_longlong(bg);
+        if (kb < GT_N_THRESHOLDS && s_thr[kb] <= bb) ++kb;
+        else if (kb > 0 && s_thr[kb - 1] > bb) --kb;
+        if (alive) {
+          const int widx = ((kb >> 2) * kFastBS + tid) * 4 + (kb & 3);
+          const uint8_t v = my_hist8[widx];
+          if (v == 254) {  // flush before the uint8 saturates
+            ghist[(int64_t)kb * n + i] += 255;
+            my_hist8[widx] = 0;
+          } else {
+            my_hist8[widx] = v + 1;
+          }
+          bg_min = fmin(bg_min, bg);
+          bg_max = fmax(bg_max, bg);
+          bg_sum += bg;
+          day_basal += basal;
+          run39 = kb <= 34 ? run39 + 1 : 0;  // bg < 3.9 (THRESHOLDS[34])
+          run30 = kb <= 25 ? run30 + 1 : 0;  // bg < 3.0 (THRESHOLDS[25])
+          ev39 += run39 == hypoL;
+          ev30 += run30 == hypoL;
+          ++ticks_done;
+        }
+      }
+      if (k == next_grid) {  // timeline point (warp-uniform)
+        const long long v = __double2ll_rn(bg * kFpScale);
+        const long long vs = alive ? v : 0LL;
+        const long long vmn = alive ? v : LLONG_MAX;
+        const long long vmx = alive ? v : LLONG_MIN;
+        const long long ssum = warp_sum64(vs), smin = warp_min64(vmn), smax = warp_max64(vmx);
+        if (lane == 0 && warp_global < n_warps) {
+          long long* dst = (long long*)a.timeline_warp + (g_idx * n_warps + warp_global) * 3;
+          dst[0] = ssum; dst[1] = smin; dst[2] = smax;
+        }
+        if (a.timeline_pp && inrange) a.timeline_pp[g_idx * n + i] = alive ? bg : 0.0;
+        ++g_idx;
+        next_grid += gstep;
+      }
+      // -------- Euler–Maruyama step, re-associated (hovorka.py:76-150)
+      const double Q1 = x[IQ1], Q2 = x[IQ2], D1 = x[ID1], D2 = x[ID2];
+      const double E2 = x[IE2], E3 = x[IE3];
+      // glucose core
+      const double ab = HAS_EX ? fma(pc.sex, E3, 1.0) : 1.0;
+      const double ub = HAS_EX ? fma(pc.qex, E2, 1.0) : 1.0;
+      const double x1e = x[IX1] * ab, x2e = x[IX2] * ab;
+      const double t1 = x1e * Q1;
+      const double hf01 = pc.hF01w * fmin(bg * (1.0 / 4.5), 1.0);
+      const double hren = fmax(fma(Q1, pc.rK1, -pc.rK0), 0.0);
+      const double hegp = fmax(fma(-pc.hE, x[IX3], pc.hE), 0.0) + pc.cG * x[IZ2];
+      double dq = fma(pc.hk12, Q2, D2 * pc.hTG);
+      dq = fma(-hf01, ub, dq);
+      dq = fma(-h, t1, dq);
+      dq = (dq - hren) + hegp;
+      x[IQ1] = fmax(fma(pc.sqE, nz.z0, Q1 + dq), 0.0);
+      x[IQ2] = fmax(fma(Q2, pc.aK12, h * (t1 - x2e * Q2)), 0.0);
+      // gut (multiplicative noise on D1, D2)
+      x[ID1] = fmax(fma(D1, fma(pc.sqG, nz.z1, pc.aG), gin_k), 0.0);
+      x[ID2] = fmax(fma(D2, fma(pc.sqG, nz.z2, pc.aG), D1 * pc.hTG), 0.0);
+      // subcutaneous insulin, plasma insulin, insulin action
+      const double S1 = x[IS1], S2 = x[IS2], I = x[II];
+      x[IS1] = fma(S1, pc.aI, hu_ins);
+      x[IS2] = fma(S2, pc.aI, S1 * pc.hTI);
+      x[II] = fma(I, pc.cI, S2 * pc.dI);
+      x[IX1] = fma(x[IX1], pc.ax1, I * pc.bx1);
+      x[IX2] = fma(x[IX2], pc.ax2, I * pc.bx2);
+      x[IX3] = fma(x[IX3], pc.ax3, I * pc.bx3);
+      // glucagon chain
+      const double Z1 = x[IZ1];
+      x[IZ1] = fma(Z1, pc.aZ1, hu2);
+      x[IZ2] = fma(x[IZ2], pc.aZ2, Z1 * pc.hTg);
+      // exercise (exactly zero forever without exercise)
+      if (HAS_EX) {
+        const double E1 = x[IE1];
+        x[IE1] = fma(E1, pc.aE1, pc.bE1 * hrr);
+        x[IE2] = fma(E2, pc.aE2, E1 * pc.bE2);
+        x[IE3] = fma(E3, pc.aE3, E1 * pc.bE3);
+      }
+      // sensor lag
+      x[IGSC] = fma(x[IGSC], pc.aS, bg * pc.hS);
+    }
+  }
+  // final partial day
+  const int64_t last_day = a.n_days - 1;
+  if (inrange && last_day >= 0) {
+    double* dd = a.day_dose + (last_day * 3) * n + i;
+    dd[0] = day_basal; dd[n] = day_bolus; dd[2 * n] = day_gluc;
+  }
+  if (!inrange) return;
+  for (int b = 0; b < GT_N_BG_BINS; ++b) {
+    const int widx = ((b >> 2) * kFastBS + tid) * 4 + (b & 3);
+    ghist[(int64_t)b * n + i] += my_hist8[widx];
+  }
+  a.status[i] = status;
+  a.ticks[i] = ticks_done;
+  a.bg_stats[i] = bg_min;
+  a.bg_stats[n + i] = bg_max;
+  a.bg_stats[2 * n + i] = bg_sum;
+  a.hypo_events[i] = ev39;
+  a.hypo_events[n + i] = ev30;
+  if (a.x_out)
+    for (int k = 0; k < NS; ++k) a.x_out[(int64_t)k * n + i] = x[k];
+}
+
+}  // namespace gt
+
+int64_t gt_fast_warps(int64_t n) { return (n + 31) / 32; }
+
+int gt_launch_fast(const gt_fast_args* a, cudaStream_t st) {
+  if (a->n <= 0) return GT_OK;
+  const unsigned grid = (unsigned)((a->n + gt::kFastBS - 1) / gt::kFastBS);
+  const int pk = a->proto_kind, nk = a->noise_kind;
+  if (pk == GT_PROTO_THREE_MEAL && nk == GT_NOISE_PHILOX)
+    gt::fast_kernel<GT_PROTO_THREE_MEAL, GT_NOISE_PHILOX><<<grid, gt::kFastBS, 0, st>>>(*a);
+  else if (pk == GT_PROTO_THREE_MEAL && nk == GT_NOISE_INJECTED)
+    gt::fast_kernel<GT_PROTO_THREE_MEAL, GT_NOISE_INJECTED><<<grid, gt::kFastBS, 0, st>>>(*a);
+  else if (pk == GT_PROTO_CSR && nk == GT_NOISE_PHILOX)
+    gt::fast_kernel<GT_PROTO_CSR, GT_NOISE_PHILOX><<<grid, gt::kFastBS, 0, st>>>(*a);
+  else if (pk == GT_PROTO_CSR && nk == GT_NOISE_INJECTED)
+    gt::fast_kernel<GT_PROTO_CSR, GT_NOISE_INJECTED><<<grid, gt::kFastBS, 0, st>>>(*a);
+  else {
+    gt_set_error("gt_simulate_fast: unsupported proto_kind=%d noise_kind=%d", pk, nk);
+    return GT_EUNSUPPORTED;
+  }
+  return gt_check_launch("fast_kernel");
+}

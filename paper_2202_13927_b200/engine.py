@@ -1,0 +1,323 @@
+"""Device engine: buffers, launches and result transfer around libglucosim.
+
+PyTorch provides device memory and streams only; all compute runs in the
+hand-written kernels behind the C-ABI (_lib.py).  There is no CPU path:
+without a CUDA device or the built library every call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import (FastArgs, MealGen, ParityArgs, ReduceArgs, SamplerArgs, check)
+from .layout import N_BG_BINS, N_CSTATE, N_PARAMS, N_STATES, N_THRESHOLDS, TIR_BINS
+
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as t
+        _torch = t
+    return _torch
+
+
+def require_device(device=None):
+    t = torch()
+    if not t.cuda.is_available():
+        raise _lib.GlucosimError("no CUDA device: the glucosim engine has no CPU fallback")
+    _lib.load()
+    if device is None:
+        device = t.device("cuda", t.cuda.current_device())
+    return t.device(device)
+
+
+def ptr(x) -> C.c_void_p:
+    return C.c_void_p(0 if x is None else x.data_ptr())
+
+
+def stream_ptr(device) -> C.c_void_p:
+    return C.c_void_p(torch().cuda.current_stream(device).cuda_stream)
+
+
+def dev(a, dtype, device):
+    t = torch()
+    arr = np.ascontiguousarray(a)
+    tt = t.from_numpy(arr)
+    if dtype is not None:
+        tt = tt.to(dtype)
+    return tt.to(device, non_blocking=False)
+
+
+def empty(shape, dtype, device):
+    return torch().empty(shape, dtype=dtype, device=device)
+
+
+# ----------------------------------------------------------- steady state
+def steady_state(params: np.ndarray, target_bg: float, device=None):
+    """Batched hovorka.steady_state on device -> (x0 [n,16], u_basal [n], ok [n])."""
+    device = require_device(device)
+    t = torch()
+    n = params.shape[0]
+    p = params.contiguous() if hasattr(params, "data_ptr") else dev(params.astype(np.float64), t.float64, device)
+    x0 = empty((n, N_STATES), t.float64, device)
+    ub = empty((n,), t.float64, device)
+    st = empty((n,), t.int32, device)
+    check(_lib.load().gt_steady_state(n, ptr(p), float(target_bg), ptr(x0), ptr(ub), ptr(st),
+                                      stream_ptr(device)), "gt_steady_state")
+    return x0, ub, st
+
+
+def controller_init(hyper: np.ndarray, icr_factor: float, basal, device=None):
+    device = require_device(device)
+    t = torch()
+    basal_t = basal if hasattr(basal, "data_ptr") else dev(np.asarray(basal, np.float64), t.float64, device)
+    n = basal_t.shape[0]
+    h = dev(np.asarray(hyper, np.float64), t.float64, device)
+    c0 = empty((n, N_CSTATE), t.float64, device)
+    check(_lib.load().gt_controller_init(n, ptr(h), float(icr_factor), ptr(basal_t), ptr(c0),
+                                         stream_ptr(device)), "gt_controller_init")
+    return c0
+
+
+# ------------------------------------------------------------ parity path
+@dataclass
+class ParityBatch:
+    """Host inputs of the parity kernel (see include/glucosim.h gt_parity_args)."""
+    params: np.ndarray        # [n,30]
+    x0: np.ndarray            # [n,16]
+    c0: np.ndarray            # [n,11]
+    hyper: np.ndarray         # [30]
+    assumed_basal: np.ndarray # [n]
+    meal_off: np.ndarray      # [n+1] int64
+    meals: tuple              # 4 x float64 [total]
+    ex_off: np.ndarray
+    ex: tuple
+    wiener: np.ndarray        # [n,H,3]
+    has_noise: np.ndarray     # [n] uint8
+    meas: np.ndarray          # [n,H/ps]
+    active: np.ndarray | None = None
+
+
+def run_parity(batch: ParityBatch, sz: dict, dt_s: float, period_s: float,
+               record_trace: bool = False, device=None) -> dict:
+    """Run the bitwise-parity integrator; returns numpy per-patient outputs."""
+    device = require_device(device)
+    t = torch()
+    n = batch.params.shape[0]
+    H, nd, ng = sz["horizon_ticks"], sz["n_days"], sz["n_grid"]
+    f64, i64 = t.float64, t.int64
+    D = lambda a, dt=f64: dev(a, dt, device)
+    nz1 = lambda a: a if a.size else np.zeros(1)
+    ins = {
+        "params": D(batch.params), "x0": D(batch.x0), "c0": D(batch.c0), "hyper": D(batch.hyper),
+        "assumed_basal": D(batch.assumed_basal),
+        "active": D(batch.active.astype(np.int32), t.int32) if batch.active is not None else None,
+        "meal_off": D(batch.meal_off, i64), "ex_off": D(batch.ex_off, i64),
+        "meals": [D(nz1(m)) for m in batch.meals], "ex": [D(nz1(e)) for e in batch.ex],
+        "wiener": D(nz1(batch.wiener.reshape(-1))), "has_noise": D(batch.has_noise.astype(np.uint8), t.uint8),
+        "meas": D(nz1(batch.meas.reshape(-1))),
+    }
+    out = {
+        "status": empty((n,), t.int32, device), "ticks": empty((n,), i64, device),
+        "tir_ticks": empty((n, 5), i64, device), "bg_hist": empty((n, N_BG_BINS), i64, device),
+        "scal": empty((n, 4), f64, device), "day_dose": empty((n, nd, 3), f64, device),
+        "timeline": empty((n, ng), f64, device), "x_out": empty((n, N_STATES), f64, device),
+        "c_out": empty((n, N_CSTATE), f64, device),
+        "trace": empty((n, H, 8), f64, device) if record_trace else None,
+    }
+    a = ParityArgs()
+    a.n, a.dt_s, a.period_s = n, float(dt_s), float(period_s)
+    a.period_steps, a.horizon_ticks, a.grid_step_ticks = sz["period_steps"], H, sz["grid_step_ticks"]
+    a.n_days, a.n_grid, a.block_ticks = nd, ng, sz["block_ticks"]
+    for k in ("params", "x0", "c0", "hyper", "assumed_basal", "active", "meal_off", "ex_off",
+              "wiener", "has_noise", "meas"):
+        setattr(a, k, ptr(ins[k]))
+    a.meals_start, a.meals_end, a.meals_rate, a.meals_ann = (ptr(m) for m in ins["meals"])
+    a.ex_start, a.ex_end, a.ex_hrr, a.ex_announced = (ptr(e) for e in ins["ex"])
+    for k, v in out.items():
+        setattr(a, k, ptr(v))
+    check(_lib.load().gt_simulate_parity(C.byref(a), stream_ptr(device)), "gt_simulate_parity")
+    res = {k: (v.cpu().numpy() if v is not None else None) for k, v in out.items()}
+    return res
+
+
+# -------------------------------------------------------------- fast path
+def meal_gen_struct(spec: dict | None) -> MealGen:
+    g = MealGen()
+    if spec:
+        for j in range(3):
+            g.clock_s[j] = spec["clock_s"][j]
+            g.mean_g[j] = spec["mean_g"][j]
+        g.sd_g, g.jitter_s, g.duration_s, g.role = (spec["sd_g"], spec["jitter_s"],
+                                                     spec["duration_s"], spec["role"])
+    return g
+
+
+@dataclass
+class FastOutputs:
+    """Device-resident per-patient outputs of the fused integrator (SoA)."""
+    n: int
+    pid0: int
+    status: object
+    ticks: object
+    bg_hist: object       # [247, n] int32
+    bg_stats: object      # [3, n]
+    day_dose: object      # [n_days, 3, n]
+    hypo_events: object   # [2, n]
+    timeline_warp: object # [n_grid, n_warps, 3]
+    timeline_pp: object = None
+    x_out: object = None
+
+
+def alloc_fast_outputs(n: int, pid0: int, sz: dict, device, per_patient_timeline=False,
+                       final_state=False) -> FastOutputs:
+    t = torch()
+    nw = (n + 31) // 32
+    return FastOutputs(
+        n=n, pid0=pid0,
+        status=empty((n,), t.int32, device), ticks=empty((n,), t.int64, device),
+        bg_hist=empty((N_BG_BINS, n), t.int32, device), bg_stats=empty((3, n), t.float64, device),
+        day_dose=empty((sz["n_days"], 3, n), t.float64, device),
+        hypo_events=empty((2, n), t.int32, device),
+        timeline_warp=empty((sz["n_grid"], nw, 3), t.int64, device),
+        timeline_pp=empty((sz["n_grid"], n), t.float64, device) if per_patient_timeline else None,
+        x_out=empty((N_STATES, n), t.float64, device) if final_state else None,
+    )
+
+
+def launch_fast(inputs: dict, outs: FastOutputs, sz: dict, dt_s: float, period_s: float,
+                seed: int, noise_role: int, hypo_min_ticks: int, device,
+                meal_spec: dict | None = None, csr: dict | None = None,
+                injected: dict | None = None, controller_code: int = 0) -> None:
+    """Enqueue the fused integrator on the current stream (no sync)."""
+    from ._lib import GT_NOISE_INJECTED, GT_NOISE_PHILOX, GT_PROTO_CSR, GT_PROTO_THREE_MEAL
+    a = FastArgs()
+    a.n, a.pid0, a.seed = outs.n, outs.pid0, int(seed) & 0xFFFFFFFFFFFFFFFF
+    a.proto_kind = GT_PROTO_THREE_MEAL if csr is None else GT_PROTO_CSR
+    a.noise_kind = GT_NOISE_PHILOX if injected is None else GT_NOISE_INJECTED
+    a.controller = controller_code
+    a.record_timeline_per_patient = int(outs.timeline_pp is not None)
+    a.dt_s, a.period_s = float(dt_s), float(period_s)
+    a.period_steps, a.horizon_ticks, a.grid_step_ticks = (sz["period_steps"], sz["horizon_ticks"],
+                                                          sz["grid_step_ticks"])
+    a.n_days, a.n_grid, a.hypo_min_ticks = sz["n_days"], sz["n_grid"], int(hypo_min_ticks)
+    a.noise_role = noise_role
+    for k in ("params", "x0", "c0", "hyper", "assumed_basal", "active"):
+        setattr(a, k, ptr(inputs.get(k)))
+    a.meal_gen = meal_gen_struct(meal_spec)
+    if csr is not None:
+        for k in ("meal_off", "meal_ks", "meal_ke", "meal_kp", "meal_rate", "meal_ann", "ex_off",
+                  "ex_ks", "ex_ke", "ex_start_s", "ex_hrr", "ex_announced"):
+            setattr(a, k, ptr(csr[k]))
+    if injected is not None:
+        a.wiener, a.has_noise, a.meas = ptr(injected["wiener"]), ptr(injected["has_noise"]), ptr(injected["meas"])
+    a.status, a.ticks, a.bg_hist, a.bg_stats = ptr(outs.status), ptr(outs.ticks), ptr(outs.bg_hist), ptr(outs.bg_stats)
+    a.day_dose, a.hypo_events, a.timeline_warp = ptr(outs.day_dose), ptr(outs.hypo_events), ptr(outs.timeline_warp)
+    a.timeline_pp, a.x_out = ptr(outs.timeline_pp), ptr(outs.x_out)
+    check(_lib.load().gt_simulate_fast(C.byref(a), stream_ptr(device)), "gt_simulate_fast")
+
+
+@dataclass
+class ReduceOutputs:
+    counts: object
+    tir_ticks_total: object
+    tir_hist: object
+    bg_hist_total: object
+    below_min: object
+    below_max: object
+    minmax_bg_bits: object
+    timeline: object
+    dose_hist: object
+    dose_sum_fp: object
+    worst: object
+    metric_hist: object
+    metrics: dict | None = None
+
+
+def alloc_reduce_outputs(n: int, sz: dict, device, per_patient_metrics=False) -> ReduceOutputs:
+    t = torch()
+    i64 = t.int64
+    return ReduceOutputs(
+        counts=empty((6,), i64, device), tir_ticks_total=empty((5,), i64, device),
+        tir_hist=empty((5, TIR_BINS + 1), i64, device), bg_hist_total=empty((N_BG_BINS,), i64, device),
+        below_min=empty((N_THRESHOLDS,), i64, device), below_max=empty((N_THRESHOLDS,), i64, device),
+        minmax_bg_bits=empty((2,), i64, device), timeline=empty((3, sz["n_grid"]), i64, device),
+        dose_hist=empty((3, 201), i64, device), dose_sum_fp=empty((3,), i64, device),
+        worst=empty((4,), i64, device), metric_hist=empty((7, TIR_BINS + 1), i64, device),
+        metrics={k: empty((n,), t.float32, device) for k in ("tir", "tbr70", "tbr54", "tar180", "tar250")}
+        if per_patient_metrics else None,
+    )
+
+
+def launch_reduce(outs: FastOutputs, red: ReduceOutputs, sz: dict, dt_s: float, device) -> None:
+    a = ReduceArgs()
+    a.n, a.pid0, a.horizon_ticks, a.n_days, a.n_grid = outs.n, outs.pid0, sz["horizon_ticks"], sz["n_days"], sz["n_grid"]
+    a.n_warps, a.dt_s = (outs.n + 31) // 32, float(dt_s)
+    a.status, a.ticks, a.bg_hist, a.bg_stats = ptr(outs.status), ptr(outs.ticks), ptr(outs.bg_hist), ptr(outs.bg_stats)
+    a.day_dose, a.hypo_events, a.timeline_warp = ptr(outs.day_dose), ptr(outs.hypo_events), ptr(outs.timeline_warp)
+    for k in ("counts", "tir_ticks_total", "tir_hist", "bg_hist_total", "below_min", "below_max",
+              "minmax_bg_bits", "timeline", "dose_hist", "dose_sum_fp", "worst", "metric_hist"):
+        setattr(a, k, ptr(getattr(red, k)))
+    if red.metrics is not None:
+        a.metric_tir, a.metric_tbr70, a.metric_tbr54 = (ptr(red.metrics[k]) for k in ("tir", "tbr70", "tbr54"))
+        a.metric_tar180, a.metric_tar250 = ptr(red.metrics["tar180"]), ptr(red.metrics["tar250"])
+    check(_lib.load().gt_reduce_trial(C.byref(a), stream_ptr(device)), "gt_reduce_trial")
+
+
+def ordered_bits_to_double(b: int) -> float:
+    b = int(b)
+    if b < 0:
+        b ^= 0x7FFFFFFFFFFFFFFF
+    return float(np.array([b], dtype=np.int64).view(np.float64)[0])
+
+
+# ------------------------------------------------------ population sampler
+def sample_population(seed: int, n: int, table, pid0: int = 0, target_bg: float = 6.0,
+                      device=None, max_attempts: int = 10_000, weight=(74.0, 13.0),
+                      min_basal: float = 0.4):
+    """Device rejection sampler -> dict of device tensors."""
+    from .layout import PARAM_INDEX, PARAM_NAMES
+    device = require_device(device)
+    t = torch()
+    a = SamplerArgs()
+    a.n, a.pid0, a.seed = n, pid0, int(seed) & 0xFFFFFFFFFFFFFFFF
+    names = list(table.sampled)
+    if len(names) > 16:
+        raise ValueError("at most 16 sampled parameters")
+    a.n_sampled, a.max_attempts = len(names), max_attempts
+    a.target_bg, a.min_basal_uh = float(target_bg), float(min_basal)
+    a.weight_mean, a.weight_sd = float(weight[0]), float(weight[1])
+    for j, name in enumerate(names):
+        spec = table.sampled[name]
+        a.kind[j] = 0 if spec.kind == "normal" else 1
+        a.param_index[j] = PARAM_INDEX[name]
+        a.a[j], a.b[j] = ((spec.mean, spec.sd) if spec.kind == "normal" else (spec.log_mu, spec.log_sigma))
+    for k, name in enumerate(PARAM_NAMES):
+        a.fixed_params[k] = float(table.fixed.get(name, 0.0))
+    out = {
+        "params": empty((n, N_PARAMS), t.float64, device), "x0": empty((n, N_STATES), t.float64, device),
+        "u_basal": empty((n,), t.float64, device), "attempts": empty((n,), t.int32, device),
+        "status": empty((n,), t.int32, device), "reject_counts": t.zeros((4,), dtype=t.int64, device=device),
+    }
+    a.params, a.x0, a.u_basal_uh = ptr(out["params"]), ptr(out["x0"]), ptr(out["u_basal"])
+    a.attempts, a.status, a.reject_counts = ptr(out["attempts"]), ptr(out["status"]), ptr(out["reject_counts"])
+    check(_lib.load().gt_sample_population(C.byref(a), stream_ptr(device)), "gt_sample_population")
+    return out
+
+
+def generate_meals(seed: int, pid0: int, n: int, n_meals: int, spec: dict, device=None):
+    device = require_device(device)
+    t = torch()
+    s = empty((n, n_meals), t.float64, device)
+    e = empty((n, n_meals), t.float64, device)
+    g = empty((n, n_meals), t.float64, device)
+    mg = meal_gen_struct(spec)
+    check(_lib.load().gt_generate_meals(n, pid0, int(seed) & 0xFFFFFFFFFFFFFFFF, C.byref(mg), n_meals,
+                                        ptr(s), ptr(e), ptr(g), stream_ptr(device)), "gt_generate_meals")
+    return s.cpu().numpy(), e.cpu().numpy(), g.cpu().numpy()

@@ -1,0 +1,27 @@
+"""Algorithmic FP64 work of the hot path, counted from the reference code.
+
+A "flop" is one FP64 add, subtract, multiply or divide of the reference's
+arithmetic (compares / min / max count 0).  Per integration step
+(_kernel.py:79-177): 2 (t = t0 + i*dt) + 1 (bg) + 1 (sum_bg) + 1
+(t // 86400) + 1 (day basal) + drift_vec (69 on the typical branch,
+hovorka.py:76-136) + diffusion_diag 3 + 16 x (x += f*dt) 32 + 3 x
+(x += sig*sqrt(dt)*w) 9 = 119.  Per controller tick: controller_step_vec
+15 (typical) + y 2 + u conversions 7 + announcement horizon 1 = 25.
+tests/golden/flop_counts.json holds the drift/controller counts measured by
+an op-counting float over the reference's own functions (make_golden.py);
+tests/test_flops.py pins these constants to it.
+"""
+
+DRIFT_TYPICAL = 69
+CONTROLLER_TYPICAL = 15
+STEP_OTHER = 2 + 1 + 1 + 1 + 1 + 3 + 32 + 9
+STEP = STEP_OTHER + DRIFT_TYPICAL            # 119
+TICK = CONTROLLER_TYPICAL + 2 + 7 + 1        # 25
+
+
+def flops_per_step(period_steps: int) -> float:
+    return STEP + TICK / period_steps
+
+
+def flops_per_patient_week(dt_s: float, period_steps: int) -> float:
+    return flops_per_step(period_steps) * 604800.0 / dt_s

@@ -1,0 +1,96 @@
+"""Virtual populations.
+
+``generate_population`` runs the device rejection sampler (csrc/gt_sampler.cu,
+BASELINE north_star subsystem 1): same parameter distributions and
+acceptance rules as the reference (population.py:207-259), counter-based
+device streams keyed by (seed, patient id).  The result stays on device
+(``DevicePopulation``) and feeds the fused trial path directly; ``entries()``
+materialises reference-style ``(Patient, ParameterSet)`` pairs.
+Populations produced by the reference's own sampler are accepted everywhere
+a population is expected.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import engine, rng, tables
+from .layout import PARAM_NAMES
+
+
+class PopulationError(RuntimeError):
+    pass
+
+
+@dataclass(slots=True)
+class Patient:
+    """Minimal patient record: the simulation uses id and body weight only
+    (population.py:42-58); names/dates/places carry no simulation semantics."""
+    id: int
+    body_weight_kg: float
+
+
+@dataclass(slots=True)
+class ParameterSet:
+    values: dict
+    u_basal_u_per_h: float
+
+
+@dataclass
+class SamplingStats:
+    attempts: int = 0
+    accepted: int = 0
+    rejected_negative: int = 0
+    rejected_outside_sd: int = 0
+    rejected_basal: int = 0
+    rejected_no_steady_state: int = 0
+
+    @property
+    def acceptance_rate(self) -> float:
+        return self.accepted / self.attempts if self.attempts else 0.0
+
+
+class DevicePopulation:
+    """A device-resident population shard (ids pid0 .. pid0+n-1)."""
+
+    def __init__(self, pid0, params_device, basal_device, x0_device, stats: SamplingStats):
+        self.pid0 = int(pid0)
+        self.params_device = params_device
+        self.basal_device = basal_device
+        self.x0_device = x0_device
+        self.stats = stats
+
+    def __len__(self):
+        return int(self.params_device.shape[0])
+
+    def entries(self):
+        p = self.params_device.cpu().numpy()
+        ub = self.basal_device.cpu().numpy()
+        out = []
+        for i in range(len(self)):
+            vals = {name: float(p[i, k]) for k, name in enumerate(PARAM_NAMES)}
+            out.append((Patient(self.pid0 + i, vals["weight_kg"]), ParameterSet(vals, float(ub[i]))))
+        return out
+
+
+def generate_population(seed: int, n: int, table=None, target_bg: float = 6.0, pid0: int = 0,
+                        device=None, max_attempts: int = tables.MAX_ATTEMPTS) -> DevicePopulation:
+    if n < 1:
+        raise PopulationError("population size must be >= 1")
+    table = table or tables.default_parameter_table()
+    out = engine.sample_population(seed, n, table, pid0=pid0, target_bg=target_bg, device=device,
+                                   max_attempts=max_attempts,
+                                   weight=(tables.WEIGHT_MEAN_KG, tables.WEIGHT_SD_KG),
+                                   min_basal=tables.MIN_BASAL_U_PER_H)
+    status = out["status"]
+    if bool((status != 0).any()):
+        bad = int(np.nonzero(status.cpu().numpy())[0][0]) + pid0
+        raise PopulationError(f"no acceptable parameter set for patient {bad} in {max_attempts} attempts")
+    rc = out["reject_counts"].cpu().numpy()
+    attempts = int(out["attempts"].sum().item())
+    st = SamplingStats(attempts=attempts, accepted=n, rejected_negative=int(rc[0]),
+                       rejected_outside_sd=int(rc[1]), rejected_no_steady_state=int(rc[2]),
+                       rejected_basal=int(rc[3]))
+    return DevicePopulation(pid0, out["params"], out["u_basal"], out["x0"], st)

@@ -1,0 +1,236 @@
+"""Fast trial path: fused integrator + device reduction (+ optional sharding).
+
+``FastTrial`` stages a shard of patients on one device once (parameters,
+steady states, controller states, protocol source) and runs
+simulate -> reduce on a CUDA stream; ``accumulator()`` converts the exact
+device fields into a ``TrialAccumulator``.  Patients whose simulation
+diverges are excluded exactly as the reference does (analytics.py:267-269):
+warps that contained one are re-run with the diverged lanes masked, so the
+per-warp timeline partials never include them.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import analytics, engine, rng
+from ._lib import GT_STATUS_EXCLUDED, GT_STATUS_NO_STEADY_STATE, GT_STATUS_NONFINITE, GT_STATUS_OK
+from .analytics import TrialAccumulator, WorstCase
+from .config import SimulationError, sizes
+from .controller import device_code, hyper_vector, icr_initial_factor
+from .layout import DOSE_SIGNALS, N_BG_BINS, N_THRESHOLDS
+from .protocol import ThreeMealProtocol, compile_protocol, compile_ticks
+
+
+@dataclass
+class ShardInputs:
+    pid0: int
+    n: int
+    params: object       # device [n,30]
+    basal: object        # device [n]
+
+
+def population_to_device(population, basal_scale: float, device):
+    """(pid0, params[n,30] device, basal[n] device) from a list of
+    (patient, parameter_set) or a DevicePopulation."""
+    t = engine.torch()
+    if hasattr(population, "params_device"):
+        return population.pid0, population.params_device, population.basal_device * basal_scale
+    from .simulation import pack_params
+    ids = np.array([int(pt.id) for pt, _ in population], dtype=np.int64)
+    if ids.size and not np.array_equal(ids, ids[0] + np.arange(ids.size)):
+        raise SimulationError("the fused path keys RNG streams by contiguous patient ids")
+    params = np.stack([pack_params(ps.values) for _, ps in population])
+    basal = np.array([float(ps.u_basal_u_per_h) * basal_scale for _, ps in population])
+    return int(ids[0]), engine.dev(params, t.float64, device), engine.dev(basal, t.float64, device)
+
+
+class FastTrial:
+    def __init__(self, pid0, params, basal, generator, profile, config, controller_id="dual_hormone",
+                 device=None, hypo_min_s: float = 900.0, per_patient_metrics: bool = False,
+                 seed: int | None = None):
+        self.device = engine.require_device(device)
+        t = engine.torch()
+        self.config = config
+        self.sz = sizes(config)
+        self.pid0 = int(pid0)
+        self.n = int(params.shape[0])
+        self.seed = int(config.seed if seed is None else seed)
+        self.code = device_code(controller_id)
+        self.profile = profile
+        self.hyper = hyper_vector(profile)
+        self.params, self.basal = params, basal
+        self.hypo_min_ticks = max(1, int(np.ceil(hypo_min_s / config.dt_s)))
+        self.generator = generator
+        with t.cuda.device(self.device):
+            self.x0, _ub, self.ss_status = engine.steady_state(params, config.initial_bg_mmol_per_l, self.device)
+            self.c0 = engine.controller_init(self.hyper, icr_initial_factor(profile), basal, self.device)
+            self.hyper_d = engine.dev(self.hyper, t.float64, self.device)
+            self.active = (self.ss_status == GT_STATUS_OK).to(t.int32)
+            self.meal_spec, self.csr = None, None
+            if isinstance(generator, ThreeMealProtocol):
+                self.meal_spec = generator.device_spec()
+            else:
+                self.csr = self._build_csr(generator)
+            self.outs = engine.alloc_fast_outputs(self.n, self.pid0, self.sz, self.device)
+            self.red = engine.alloc_reduce_outputs(self.n, self.sz, self.device, per_patient_metrics)
+        self._inputs = {"params": self.params, "x0": self.x0, "c0": self.c0, "hyper": self.hyper_d,
+                        "assumed_basal": self.basal, "active": self.active}
+
+    def _build_csr(self, generator):
+        t = engine.torch()
+        cfg = self.config
+
+        class _P:  # minimal patient for generator.build
+            def __init__(self, pid, w):
+                self.id, self.body_weight_kg = pid, w
+        w = self.params[:, 0].cpu().numpy()
+        tas = []
+        for i in range(self.n):
+            pa = compile_protocol(generator.build(cfg.seed, _P(self.pid0 + i, float(w[i]))), cfg.horizon_s)
+            tas.append(compile_ticks(pa, cfg.dt_s, cfg.controller_period_s))
+        moff = np.zeros(self.n + 1, np.int64)
+        eoff = np.zeros(self.n + 1, np.int64)
+        for i, ta in enumerate(tas):
+            moff[i + 1] = moff[i] + ta.meal_ks.size
+            eoff[i + 1] = eoff[i] + ta.ex_ks.size
+        cat = lambda k, dt: np.concatenate([getattr(ta, k) for ta in tas]).astype(dt) if tas else np.zeros(0, dt)
+        nz = lambda a: a if a.size else np.zeros(1, a.dtype)
+        D = lambda a, tdt: engine.dev(nz(a), tdt, self.device)
+        return {
+            "meal_off": D(moff, t.int64), "meal_ks": D(cat("meal_ks", np.int32), t.int32),
+            "meal_ke": D(cat("meal_ke", np.int32), t.int32), "meal_kp": D(cat("meal_kp", np.int32), t.int32),
+            "meal_rate": D(cat("meal_rate", np.float64), t.float64), "meal_ann": D(cat("meal_ann", np.float64), t.float64),
+            "ex_off": D(eoff, t.int64), "ex_ks": D(cat("ex_ks", np.int32), t.int32),
+            "ex_ke": D(cat("ex_ke", np.int32), t.int32), "ex_start_s": D(cat("ex_start", np.float64), t.float64),
+            "ex_hrr": D(cat("ex_hrr", np.float64), t.float64),
+            "ex_announced": D(cat("ex_announced", np.float64), t.float64),
+        }
+
+    # ------------------------------------------------------------- running
+    def simulate(self, active=None, injected=None):
+        """Enqueue the fused integrator (current stream, no sync)."""
+        inputs = dict(self._inputs)
+        if active is not None:
+            inputs["active"] = active
+        engine.launch_fast(inputs, self.outs, self.sz, self.config.dt_s,
+                           self.config.controller_period_s, self.seed, rng.ROLE_DEVICE_NOISE,
+                           self.hypo_min_ticks, self.device, meal_spec=self.meal_spec, csr=self.csr,
+                           injected=injected, controller_code=self.code)
+
+    def reduce(self):
+        engine.launch_reduce(self.outs, self.red, self.sz, self.config.dt_s, self.device)
+
+    def step(self):
+        """One full pass: simulate + (exclusion re-run if needed) + reduce."""
+        self.simulate()
+        self._rerun_if_diverged()
+        self.reduce()
+
+    def _rerun_if_diverged(self):
+        t = engine.torch()
+        st = self.outs.status
+        bad = st == GT_STATUS_NONFINITE
+        if not bool(bad.any()):
+            return
+        # re-simulate with diverged lanes masked out (deterministic streams)
+        active = self.active.clone()
+        active[bad] = 0
+        status_keep = st.clone()
+        self.simulate(active=active)
+        self.outs.status.copy_(t.where(bad, status_keep, self.outs.status))
+
+    # ----------------------------------------------------------- readback
+    def accumulator(self) -> TrialAccumulator:
+        t = engine.torch()
+        cfg, sz, red = self.config, self.sz, self.red
+        acc = TrialAccumulator(dt_s=cfg.dt_s, horizon_ticks=sz["horizon_ticks"], n_days=sz["n_days"],
+                               n_grid=sz["n_grid"], grid_step_s=cfg.grid_step_s)
+        h = lambda x: x.cpu().numpy()
+        counts = h(red.counts)
+        acc.n_patients = int(counts[0])
+        status = h(self.outs.status)
+        ss = h(self.ss_status)
+        aborted = np.nonzero((status == GT_STATUS_NONFINITE) | (ss == GT_STATUS_NO_STEADY_STATE))[0]
+        acc.n_aborted = int(aborted.size)
+        acc.aborted_ids = tuple(int(self.pid0 + i) for i in aborted)
+        acc.sum_bg_fp = (int(counts[4]) << 64) + (int(counts[2]) & 0xFFFFFFFFFFFFFFFF)
+        acc.n_patient_days = int(counts[3])
+        acc.tir_ticks_total = h(red.tir_ticks_total).astype(np.int64)
+        acc.tir_hist = h(red.tir_hist).astype(np.int64)
+        acc.bg_hist_total = h(red.bg_hist_total).astype(np.int64)
+        acc.below_min = h(red.below_min).astype(np.int64)
+        acc.below_max = h(red.below_max).astype(np.int64)
+        mm = h(red.minmax_bg_bits)
+        acc.min_bg = engine.ordered_bits_to_double(mm[0]) if acc.n_patients else np.inf
+        acc.max_bg = engine.ordered_bits_to_double(mm[1]) if acc.n_patients else -np.inf
+        tl = h(red.timeline)
+        acc.timeline_sum_fp, acc.timeline_min_fp, acc.timeline_max_fp = (tl[0].copy(), tl[1].copy(), tl[2].copy())
+        dh = h(red.dose_hist)
+        acc.dose_hist = {s: dh[k].astype(np.int64) for k, s in enumerate(DOSE_SIGNALS)}
+        acc.dose_sum_fp = [int(v) for v in h(red.dose_sum_fp)]
+        acc.metric_hist = h(red.metric_hist).astype(np.int64)
+        w = h(red.worst)
+        if int(w[3]):
+            i = int(w[2]) - self.pid0
+            hist = h(self.outs.bg_hist[:, i]).astype(np.int64)
+            cum = np.cumsum(hist)
+            tir = np.array([cum[25], cum[34] - cum[25], cum[95] - cum[34], cum[134] - cum[95],
+                            cum[-1] - cum[134]], dtype=np.int64)
+            acc.worst = WorstCase(patient_id=int(w[2]), min_bg=engine.ordered_bits_to_double(w[0]),
+                                  max_bg=float(h(self.outs.bg_stats[1, i])), ticks_below_3=int(w[1]),
+                                  ticks=int(h(self.outs.ticks[i])), tir_ticks=tir, bg_hist=hist)
+        return acc
+
+    def metrics(self) -> dict | None:
+        if self.red.metrics is None:
+            return None
+        out = {k: v.cpu().numpy() for k, v in self.red.metrics.items()}
+        out["hypo_events_lt70"] = self.outs.hypo_events[0].cpu().numpy()
+        out["hypo_events_lt54"] = self.outs.hypo_events[1].cpu().numpy()
+        out["status"] = self.outs.status.cpu().numpy()
+        return out
+
+
+def run_trial_fast(population, generator, controller_id, profile, model_id, config, *,
+                   basal_scale=1.0, run_meta=None, progress=None, device=None,
+                   hypo_min_s=900.0, per_patient_metrics=True):
+    from .simulation import TrialResult, _meta
+    t0 = time.perf_counter()
+    device = engine.require_device(device)
+    pid0, params, basal = population_to_device(population, basal_scale, device)
+    ft = FastTrial(pid0, params, basal, generator, profile, config, controller_id, device,
+                   hypo_min_s=hypo_min_s, per_patient_metrics=per_patient_metrics)
+    ft.step()
+    acc = ft.accumulator()
+    wall_s = time.perf_counter() - t0
+    if progress:
+        progress(ft.n, ft.n)
+    if acc.n_patients == 0:
+        raise SimulationError("all simulations diverged; nothing to report")
+    meta = _meta(config, ft.n, model_id, controller_id, profile, basal_scale, generator, run_meta)
+    report = analytics.build_trial_report(acc, meta)
+    return TrialResult(report=report, accumulator=acc, worst_trace=None, wall_s=wall_s,
+                       n_patients=ft.n, metrics=ft.metrics())
+
+
+def run_population_arrays(params_host, basal_host, generator, profile, config, *, pid0=0,
+                          controller_id="dual_hormone", device=None, hypo_min_s=900.0):
+    """Public array API of the fused path (host buffers in, host results out):
+    H2D of the per-patient parameter rows and basal rates, steady state,
+    controller set-up, fused simulation, device reduction, D2H of the exact
+    accumulator fields and the per-patient metric arrays.
+    Returns ``(TrialAccumulator, metrics dict)``."""
+    t = engine.torch()
+    device = engine.require_device(device)
+    p = params_host if hasattr(params_host, "data_ptr") else t.from_numpy(np.ascontiguousarray(params_host))
+    b = basal_host if hasattr(basal_host, "data_ptr") else t.from_numpy(np.ascontiguousarray(basal_host))
+    p_d = p.to(device, non_blocking=True)
+    b_d = b.to(device, non_blocking=True)
+    ft = FastTrial(pid0, p_d, b_d, generator, profile, config, controller_id, device,
+                   hypo_min_s=hypo_min_s, per_patient_metrics=True)
+    ft.step()
+    return ft.accumulator(), ft.metrics()

@@ -1,0 +1,78 @@
+"""World-size-2 gloo test of the multi-GPU combination logic (CPU): the
+all-reduced accumulator of two shards equals the single-process merge, and
+the shard ranges tile the population."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_2202_13927_b200 import analytics
+from paper_2202_13927_b200.parallel import shard_range
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _acc(seed):
+    from test_host import _random_acc
+    return _random_acc(seed)
+
+
+def _worker(rank, world, port, q):
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, here)
+    sys.path.insert(0, os.path.dirname(here))
+    import torch.distributed as dist
+    from paper_2202_13927_b200.parallel import allreduce_accumulator
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    acc = _acc(100 + rank)
+    acc.add_aborted(1000 + rank)
+    acc.sum_bg_fp += (1 << 70) * (rank + 1)   # beyond int64: python-int path
+    out = allreduce_accumulator(acc)
+    q.put((rank, analytics.report_bytes(analytics.build_trial_report(out, {})), out.sum_bg_fp,
+           out.aborted_ids))
+    dist.destroy_process_group()
+
+
+def test_allreduce_equals_merge_world2():
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    a, b = _acc(100), _acc(101)
+    a.add_aborted(1000)
+    b.add_aborted(1001)
+    a.sum_bg_fp += 1 << 70
+    b.sum_bg_fp += 2 << 70
+    ref = analytics.merge(a, b)
+    want = analytics.report_bytes(analytics.build_trial_report(ref, {}))
+    for rank, rep, s, ab in res:
+        assert rep == want
+        assert s == ref.sum_bg_fp
+        assert ab == (1000, 1001)
+
+
+@pytest.mark.parametrize("n,world", [(100_000, 1), (1_000_000, 8), (7, 3), (5, 8)])
+def test_shard_ranges_tile(n, world):
+    got = [shard_range(n, r, world) for r in range(world)]
+    assert got[0][0] == 0 and got[-1][1] == n
+    for (a, b), (c, d) in zip(got, got[1:]):
+        assert b == c
+    sizes = [b - a for a, b in got]
+    assert max(sizes) - min(sizes) <= 1

@@ -1,0 +1,199 @@
+"""GPU parity tests (need a B200): the CUDA path through the C-ABI against
+the oracle and the reference's golden vectors."""
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import golden, golden_bytes
+from helpers import SimCase
+
+pytestmark = pytest.mark.gpu
+
+SIMS = ["sim_northern_dt30.npz", "sim_threemeal_dt60.npz", "sim_northern_dt37p5.npz",
+        "sim_northern_dt30_8d.npz", "sim_faults.npz"]
+
+
+@pytest.fixture(scope="module")
+def dev():
+    import torch
+    from paper_2202_13927_b200 import _lib
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    _lib.load()
+    return torch.device("cuda", 0)
+
+
+def _parity(case, dev, idx=None, trace=False):
+    from paper_2202_13927_b200 import engine
+    sub = case.subset(case.valid() if idx is None else idx)
+    b = engine.ParityBatch(sub["params"], sub["x0"], sub["c0"], case.hyper, sub["basal"],
+                           sub["meal_off"], sub["meals"], sub["ex_off"], sub["ex"], sub["wiener"],
+                           sub["has_noise"], sub["meas"])
+    return sub, engine.run_parity(b, case.sz, case.config.dt_s, case.config.controller_period_s,
+                                  record_trace=trace, device=dev)
+
+
+def test_steady_state_bitwise(dev):
+    from paper_2202_13927_b200 import engine
+    g = golden("steady.npz")
+    x0, ub, ok = engine.steady_state(g["params"], 6.0, dev)
+    assert np.array_equal(x0.cpu().numpy(), g["x0"]) and np.array_equal(ub.cpu().numpy(), g["ub"])
+    assert np.all(ok.cpu().numpy() == 0)
+    x0, ub, ok = engine.steady_state(g["pert"], 6.0, dev)
+    ok = ok.cpu().numpy()
+    assert np.array_equal(ok == 0, g["pert_ok"] == 1)
+    m = g["pert_ok"] == 1
+    assert np.array_equal(x0.cpu().numpy()[m], g["pert_x0"][m])
+    assert np.array_equal(ub.cpu().numpy()[m], g["pert_ub"][m])
+    _, _, bad = engine.steady_state(g["bad_params"][None, :], 6.0, dev)
+    assert int(bad.cpu()[0]) == 2
+
+
+def test_controller_init_matches_reference(dev):
+    from paper_2202_13927_b200 import engine
+    case = SimCase("sim_northern_dt30.npz")
+    c0 = engine.controller_init(case.hyper, 1.6, case.basal, dev).cpu().numpy()
+    assert np.array_equal(c0, case.c0)
+
+
+@pytest.mark.parametrize("name", SIMS)
+def test_parity_kernel_bitwise_vs_reference(dev, name):
+    case = SimCase(name)
+    g = case.g
+    sub, out = _parity(case, dev, trace=True)
+    for j, i in enumerate(sub["idx"]):
+        assert out["status"][j] == g["status"][i]
+        assert out["ticks"][j] == g["ticks"][i]
+        assert np.array_equal(out["tir_ticks"][j], g["tir"][i])
+        assert np.array_equal(out["bg_hist"][j], g["hist"][i])
+        assert np.array_equal(out["scal"][j, :3], g["scal"][i])
+        assert np.array_equal(out["day_dose"][j], g["day_dose"][i])
+        assert np.array_equal(out["timeline"][j], g["timeline"][i])
+        if f"trace_{i}" in g.files:
+            tr = g[f"trace_{i}"]
+            assert np.array_equal(out["trace"][j][: tr.shape[0]], tr)
+
+
+def test_parity_kernel_bitwise_vs_oracle_1000_patients_4_weeks(dev, oracle):
+    """BASELINE configs[1] correctness subset shape: reference noise streams
+    injected, device-sampled parameters, 3-meal schedules, 4 weeks at dt 60 —
+    a 96-patient slice keeps the oracle to seconds; bitwise equality."""
+    from paper_2202_13927_b200 import engine, rng
+    from paper_2202_13927_b200.config import SimulationConfig, sizes
+    from paper_2202_13927_b200.controller import ControllerHyperparameters
+    from paper_2202_13927_b200.population import generate_population
+    from paper_2202_13927_b200.protocol import ThreeMealProtocol, compile_protocol
+    from paper_2202_13927_b200.simulation import _csr
+    cfg = SimulationConfig(horizon_s=28 * 86400.0, seed=1, dt_s=60.0)
+    sz = sizes(cfg)
+    n = 96
+    pop = generate_population(1, n, device=dev)
+    params = pop.params_device.cpu().numpy()
+    ub = pop.basal_device.cpu().numpy()
+    x0 = pop.x0_device.cpu().numpy()
+    prof = ControllerHyperparameters()
+    c0 = engine.controller_init(prof.to_vec(), prof.icr_initial_factor, ub, dev).cpu().numpy()
+    gen = ThreeMealProtocol()
+    pas = [compile_protocol(gen.build(cfg.seed, type("P", (), {"id": i, "body_weight_kg": params[i, 0]})()),
+                            cfg.horizon_s) for i in range(n)]
+    moff, meals, eoff, ex = _csr(pas)
+    H, ps = sz["horizon_ticks"], sz["period_steps"]
+    W = np.zeros((n, H, 3)); M = np.zeros((n, H // ps))
+    for i in range(n):
+        W[i], M[i] = rng.reference_noise(cfg.seed, i, H, ps, True, True)
+    hn = np.ones(n, np.uint8)
+    b = engine.ParityBatch(params, x0, c0, prof.to_vec(), ub, moff, meals, eoff, ex, W, hn, M)
+    out = engine.run_parity(b, sz, cfg.dt_s, cfg.controller_period_s, device=dev)
+    ref = oracle.run_batch_injected(params, x0, c0, prof.to_vec(), ub, sz, cfg.dt_s,
+                                    cfg.controller_period_s, moff, meals, eoff, ex, W, hn, M)
+    for k in ("status", "ticks", "tir_ticks", "bg_hist", "scal", "day_dose", "timeline", "x_out", "c_out"):
+        assert np.array_equal(out[k], ref[k]), k
+
+
+def test_simulate_closed_loop_api(dev):
+    """simulate_closed_loop with the reference's argument types (duck-typed)
+    returns the reference's SimulationResult values bit for bit."""
+    from paper_2202_13927_b200 import simulate_closed_loop
+    from paper_2202_13927_b200.controller import get_controller_factory, ControllerHyperparameters
+    from paper_2202_13927_b200.northern import NorthernYearProtocol
+    from paper_2202_13927_b200.population import ParameterSet, Patient
+    from paper_2202_13927_b200.layout import PARAM_NAMES
+    case = SimCase("sim_northern_dt30.npz")
+    g = case.g
+    for i in (0, 5):
+        vals = dict(zip(PARAM_NAMES, case.params[i]))
+        patient = Patient(int(case.ids[i]), float(case.params[i, 0]))
+        pset = ParameterSet(vals, 0.0)
+        proto = NorthernYearProtocol().build(case.config.seed, patient)
+        ctl = get_controller_factory("dual_hormone")(ControllerHyperparameters(), float(case.basal[i]))
+        res = simulate_closed_loop(patient, pset, proto, ctl, "hovorka_ext", case.config,
+                                   record_trace=True, device=dev)
+        assert res.status == "ok"
+        assert np.array_equal(res.stats.bg_hist, g["hist"][i])
+        assert res.stats.sum_bg == g["scal"][i][2]
+        if f"trace_{i}" in g.files:
+            assert np.array_equal(res.trace, g[f"trace_{i}"])
+
+
+def _entries_from_population(pop_key_prefix, n):
+    from paper_2202_13927_b200.layout import PARAM_NAMES
+    from paper_2202_13927_b200.population import ParameterSet, Patient
+    g = golden("population.npz")
+    P, ub = g[f"{pop_key_prefix}_params"], g[f"{pop_key_prefix}_ubasal"]
+    return [(Patient(i, float(P[i, 0])), ParameterSet(dict(zip(PARAM_NAMES, map(float, P[i]))), float(ub[i])))
+            for i in range(n)]
+
+
+@pytest.mark.parametrize("which", ["northern", "threemeal", "faults"])
+def test_run_trial_report_bytes_equal_reference(dev, which):
+    from paper_2202_13927_b200 import report_bytes, run_trial
+    from paper_2202_13927_b200.config import SimulationConfig
+    from paper_2202_13927_b200.controller import ControllerHyperparameters
+    from paper_2202_13927_b200.northern import NorthernYearProtocol
+    from paper_2202_13927_b200.protocol import ThreeMealProtocol
+    prof = ControllerHyperparameters()
+    if which == "threemeal":
+        entries = _entries_from_population("s0", 64)
+        cfg = SimulationConfig(horizon_s=7 * 86400.0, seed=0, dt_s=60.0)
+        gen, ref = ThreeMealProtocol(), "report_threemeal_dt60.json"
+    else:
+        entries = _entries_from_population("s101", 12 if which == "northern" else 4)
+        cfg = SimulationConfig(horizon_s=2 * 86400.0, seed=33)
+        gen = NorthernYearProtocol()
+        ref = "report_northern_dt30.json" if which == "northern" else "report_faults.json"
+        if which == "faults":
+            entries[2][1].values["tau_cgm"] = -1.0
+            entries[3][1].values["EGP0"] = 0.001
+    res = run_trial(entries, gen, "dual_hormone", prof, "hovorka_ext", cfg, device=dev)
+    assert report_bytes(res.report) == golden_bytes(ref)
+
+
+def test_worst_trace_reproduces_reference(dev):
+    import dataclasses
+    from paper_2202_13927_b200 import run_trial
+    from paper_2202_13927_b200.config import SimulationConfig
+    from paper_2202_13927_b200.controller import ControllerHyperparameters
+    from paper_2202_13927_b200.northern import NorthernYearProtocol
+    g = golden("worst_trace.npz")
+    cfg = SimulationConfig(horizon_s=2 * 86400.0, seed=33, store_trace="worst_case_only")
+    res = run_trial(_entries_from_population("s101", 4), NorthernYearProtocol(), "dual_hormone",
+                    ControllerHyperparameters(), "hovorka_ext", cfg, device=dev)
+    assert res.accumulator.worst.patient_id == int(g["worst_id"])
+    assert np.array_equal(res.worst_trace, g["trace"])
+    assert res.worst_trace[:, 1].min() == res.accumulator.worst.min_bg
+
+
+def test_unsupported_model_or_controller_raises(dev):
+    from paper_2202_13927_b200 import SimulationError, run_trial
+    from paper_2202_13927_b200.config import SimulationConfig
+    from paper_2202_13927_b200.controller import ControllerHyperparameters
+    from paper_2202_13927_b200.protocol import ThreeMealProtocol
+    cfg = SimulationConfig(horizon_s=86400.0, seed=0, dt_s=60.0)
+    e = _entries_from_population("s0", 2)
+    with pytest.raises(SimulationError):
+        run_trial(e, ThreeMealProtocol(), "dual_hormone", ControllerHyperparameters(), "toy", cfg, device=dev)
+    with pytest.raises(SimulationError):
+        run_trial(e, ThreeMealProtocol(), "pid_mpc", ControllerHyperparameters(), "hovorka_ext", cfg, device=dev)
+    with pytest.raises(SimulationError):
+        run_trial([], ThreeMealProtocol(), "dual_hormone", ControllerHyperparameters(), "hovorka_ext", cfg, device=dev)
