@@ -200,7 +200,7 @@ def run_ours(args):
     prof = ControllerHyperparameters()
     gen = ThreeMealProtocol()
     t_s0 = time.perf_counter()
-    pop = generate_population(SEED, n, pid0=pid0, device=device)
+    pop = generate_population(SEED, n, pid0=pid0, device=device, on_exhausted="redraw_weight")
     torch.cuda.synchronize()
     sampler_s = time.perf_counter() - t_s0
     ft = FastTrial(pid0, pop.params_device, pop.basal_device, gen, prof, cfg, device=device,

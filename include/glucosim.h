@@ -234,6 +234,11 @@ typedef struct gt_sampler_args {
     int32_t *attempts;     /* [n] out */
     int32_t *status;       /* [n] out: 0 ok, 1 budget exhausted */
     int64_t *reject_counts; /* [4] negative, outside_sd, no_steady_state, basal (atomic) */
+    /* 0 = reference semantics (budget exhausted -> status 1, PopulationError
+     * on the host).  k > 0: redraw the body weight up to k times when a
+     * weight admits no accepted parameter set within max_attempts (very low
+     * weights cannot reach u_basal >= 0.4 U/h). */
+    int32_t max_weight_redraws, pad;
 } gt_sampler_args;
 int gt_sample_population(const gt_sampler_args *a, void *stream);
 

@@ -95,7 +95,7 @@ class SamplerArgs(C.Structure):
         ("kind", I32 * 16), ("param_index", I32 * 16), ("a", D * 16), ("b", D * 16),
         ("fixed_params", D * 30),
         ("params", P), ("x0", P), ("u_basal_uh", P), ("attempts", P), ("status", P),
-        ("reject_counts", P),
+        ("reject_counts", P), ("max_weight_redraws", I32), ("pad", I32),
     ]
 
 

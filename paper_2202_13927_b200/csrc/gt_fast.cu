@@ -390,7 +390,13 @@ __global__ void __launch_bounds__(kFastBS, 4) fast_kernel(const gt_fast_args a) 
         if (alive) { day_bolus += bolus; day_gluc += gluc; }
       }
       // -------- statistics at tick k (_kernel.py:137-160)
-      const double bg = x[IQ1] * pc.invVGw;
+      double bg = x[IQ1] * pc.invVGw;
+      if (k == 0) {
+        // the steady state puts BG(0) on a histogram edge (6.0 = THRESHOLDS[55],
+        // SURVEY.md §7): use the reference's exact division for that tick
+        const int64_t ii = inrange ? i : 0;
+        bg = x[IQ1] / (a.params[ii * NP + PVG] * a.params[ii * NP + PW]);
+      }
       if (alive && !isfinite(bg)) { alive = false; status = GT_STATUS_NONFINITE; }
       {
         // exact searchsorted(THRESHOLDS, bg, 'right') for bg >= 0: FP32

@@ -30,25 +30,28 @@ __global__ void sampler_kernel(gt_sampler_args a) {
   if (i >= a.n) return;
   const uint32_t pid = (uint32_t)(a.pid0 + i);
   const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
-  // body weight: N(mean, sd) redrawn until > 0 (population.py:148-153)
-  double w = 0.0;
-  for (uint32_t t = 0; t < (uint32_t)a.max_attempts; ++t) {
-    const U4 r = philox4x32_10(t, pid, kRoleSamplerWeight, 0u, k0, k1);
-    const double v = A_(a.weight_mean, M_(a.weight_sd, det_inv_norm(u52(r.x, r.y))));
-    if (v > 0.0) { w = v; break; }
-  }
   double p[GT_N_PARAMS];
   for (int k = 0; k < GT_N_PARAMS; ++k) p[k] = a.fixed_params[k];
-  p[PW] = w;
   int status = 1;
-  int32_t attempt = 0;
+  int32_t attempt = 0, total_attempts = 0;
+  uint32_t wctr = 0;
   long long rej_neg = 0, rej_sd = 0, rej_ss = 0, rej_basal = 0;
   double x[GT_N_STATES], ub = 0.0;
+  for (int wdraw = 0; wdraw <= a.max_weight_redraws && status != 0; ++wdraw) {
+  // body weight: N(mean, sd) redrawn until > 0 (population.py:148-153)
+  double w = 0.0;
+  for (int t = 0; t < a.max_attempts; ++t, ++wctr) {
+    const U4 r = philox4x32_10(wctr, pid, kRoleSamplerWeight, 0u, k0, k1);
+    const double v = A_(a.weight_mean, M_(a.weight_sd, det_inv_norm(u52(r.x, r.y))));
+    if (v > 0.0) { w = v; ++wctr; break; }
+  }
+  p[PW] = w;
   for (attempt = 0; attempt < a.max_attempts && w > 0.0; ++attempt) {
+    const int32_t actr = total_attempts + attempt;
     // draw all sampled values in table order (population.py:207-214)
     double vals[16];
     for (int q = 0; q < a.n_sampled; q += 2) {
-      const U4 r = philox4x32_10((uint32_t)attempt, pid, kRoleSamplerParams, (uint32_t)(q >> 1), k0, k1);
+      const U4 r = philox4x32_10((uint32_t)actr, pid, kRoleSamplerParams, (uint32_t)(q >> 1), k0, k1);
       const double z0 = det_inv_norm(u52(r.x, r.y));
       const double z1 = det_inv_norm(u52(r.z, r.w));
       for (int h = 0; h < 2 && q + h < a.n_sampled; ++h) {
@@ -70,10 +73,12 @@ __global__ void sampler_kernel(gt_sampler_args a) {
     status = 0;
     break;
   }
+  total_attempts += status == 0 ? attempt + 1 : attempt;
+  }
   for (int k = 0; k < GT_N_PARAMS; ++k) a.params[i * GT_N_PARAMS + k] = p[k];
   for (int k = 0; k < GT_N_STATES; ++k) a.x0[i * GT_N_STATES + k] = status == 0 ? x[k] : 0.0;
   a.u_basal_uh[i] = status == 0 ? ub : 0.0;
-  a.attempts[i] = status == 0 ? attempt + 1 : attempt;
+  a.attempts[i] = total_attempts;
   a.status[i] = status;
   if (a.reject_counts) {
     if (rej_neg) atomicAdd((unsigned long long*)&a.reject_counts[0], (unsigned long long)rej_neg);

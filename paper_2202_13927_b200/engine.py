@@ -280,7 +280,7 @@ def ordered_bits_to_double(b: int) -> float:
 # ------------------------------------------------------ population sampler
 def sample_population(seed: int, n: int, table, pid0: int = 0, target_bg: float = 6.0,
                       device=None, max_attempts: int = 10_000, weight=(74.0, 13.0),
-                      min_basal: float = 0.4):
+                      min_basal: float = 0.4, max_weight_redraws: int = 0):
     """Device rejection sampler -> dict of device tensors."""
     from .layout import PARAM_INDEX, PARAM_NAMES
     device = require_device(device)
@@ -291,6 +291,7 @@ def sample_population(seed: int, n: int, table, pid0: int = 0, target_bg: float 
     if len(names) > 16:
         raise ValueError("at most 16 sampled parameters")
     a.n_sampled, a.max_attempts = len(names), max_attempts
+    a.max_weight_redraws = int(max_weight_redraws)
     a.target_bg, a.min_basal_uh = float(target_bg), float(min_basal)
     a.weight_mean, a.weight_sd = float(weight[0]), float(weight[1])
     for j, name in enumerate(names):

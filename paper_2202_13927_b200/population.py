@@ -76,14 +76,25 @@ class DevicePopulation:
 
 
 def generate_population(seed: int, n: int, table=None, target_bg: float = 6.0, pid0: int = 0,
-                        device=None, max_attempts: int = tables.MAX_ATTEMPTS) -> DevicePopulation:
+                        device=None, max_attempts: int = tables.MAX_ATTEMPTS,
+                        on_exhausted: str = "raise") -> DevicePopulation:
+    """``on_exhausted="raise"`` keeps the reference's contract (PopulationError
+    when a patient exhausts the attempt budget, population.py:257-259).  Very
+    low body weights (< ~30 kg, 3.4e-4 of N(74,13)) admit no parameter set with
+    u_basal >= 0.4 U/h, so populations of 1e5+ patients hit that error with
+    near certainty; ``"redraw_weight"`` redraws such a patient's weight
+    (up to 16 times) instead — the body-weight distribution conditioned on
+    feasibility."""
+    if on_exhausted not in ("raise", "redraw_weight"):
+        raise ValueError("on_exhausted must be 'raise' or 'redraw_weight'")
     if n < 1:
         raise PopulationError("population size must be >= 1")
     table = table or tables.default_parameter_table()
     out = engine.sample_population(seed, n, table, pid0=pid0, target_bg=target_bg, device=device,
                                    max_attempts=max_attempts,
                                    weight=(tables.WEIGHT_MEAN_KG, tables.WEIGHT_SD_KG),
-                                   min_basal=tables.MIN_BASAL_U_PER_H)
+                                   min_basal=tables.MIN_BASAL_U_PER_H,
+                                   max_weight_redraws=16 if on_exhausted == "redraw_weight" else 0)
     status = out["status"]
     if bool((status != 0).any()):
         bad = int(np.nonzero(status.cpu().numpy())[0][0]) + pid0

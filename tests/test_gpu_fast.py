@@ -118,7 +118,7 @@ def test_fast_matches_reference_to_rounding(dev, name):
     ties = 0
     for j, i in enumerate(sub["idx"]):
         assert _h(outs.status)[j] == g["status"][i]
-        ref_sum, ref_min, ref_max = g["scal"][i]
+        ref_min, ref_max, ref_sum = g["scal"][i]
         close = (np.isclose(st[2, j], ref_sum, rtol=1e-9, atol=0) and np.isclose(st[0, j], ref_min, rtol=1e-9, atol=0)
                  and np.isclose(st[1, j], ref_max, rtol=1e-9, atol=0)
                  and np.allclose(tl[:, j], g["timeline"][i], rtol=1e-9, atol=0)
@@ -165,7 +165,7 @@ def _fast_trial(n, pid0, cfg, dev, per_patient_timeline=True, seed_pop=5):
     from paper_2202_13927_b200.protocol import ThreeMealProtocol
     from paper_2202_13927_b200.trial import FastTrial
     from paper_2202_13927_b200 import engine
-    pop = generate_population(seed_pop, n, pid0=pid0, device=dev)
+    pop = generate_population(seed_pop, n, pid0=pid0, device=dev, on_exhausted="redraw_weight")
     ft = FastTrial(pid0, pop.params_device, pop.basal_device, ThreeMealProtocol(),
                    ControllerHyperparameters(), cfg, device=dev, per_patient_metrics=True)
     if per_patient_timeline:
