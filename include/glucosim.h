@@ -145,6 +145,12 @@ typedef struct gt_fast_args {
     double dt_s, period_s;
     int64_t period_steps, horizon_ticks, grid_step_ticks, n_days, n_grid, hypo_min_ticks;
     uint32_t noise_role, pad0;
+    /* Values of the non-sampled ("fixed", hovorka_distributions.yaml:46-81)
+     * parameters shared by every patient of the launch, in p[30] order; the
+     * fused kernel folds them into launch constants (kernel-parameter bank)
+     * and ignores those columns of `params`.  Entries of sampled parameters
+     * (and weight) are ignored. */
+    double fixed[30];
     const double *params;        /* [n][30] */
     const double *x0;            /* [n][16] */
     const double *c0;            /* [n][11] */

@@ -194,10 +194,17 @@ def alloc_fast_outputs(n: int, pid0: int, sz: dict, device, per_patient_timeline
 def launch_fast(inputs: dict, outs: FastOutputs, sz: dict, dt_s: float, period_s: float,
                 seed: int, noise_role: int, hypo_min_ticks: int, device,
                 meal_spec: dict | None = None, csr: dict | None = None,
-                injected: dict | None = None, controller_code: int = 0) -> None:
-    """Enqueue the fused integrator on the current stream (no sync)."""
+                injected: dict | None = None, controller_code: int = 0, fixed=None) -> None:
+    """Enqueue the fused integrator on the current stream (no sync).
+    ``fixed``: the launch-uniform values of the non-sampled parameters
+    (p[30] order); defaults to row 0 of ``inputs['params']`` after checking
+    every row agrees (see :func:`uniform_fixed`)."""
     from ._lib import GT_NOISE_INJECTED, GT_NOISE_PHILOX, GT_PROTO_CSR, GT_PROTO_THREE_MEAL
+    if fixed is None:
+        fixed = uniform_fixed(inputs["params"])
     a = FastArgs()
+    for k in range(N_PARAMS):
+        a.fixed[k] = float(fixed[k])
     a.n, a.pid0, a.seed = outs.n, outs.pid0, int(seed) & 0xFFFFFFFFFFFFFFFF
     a.proto_kind = GT_PROTO_THREE_MEAL if csr is None else GT_PROTO_CSR
     a.noise_kind = GT_NOISE_PHILOX if injected is None else GT_NOISE_INJECTED
@@ -221,6 +228,22 @@ def launch_fast(inputs: dict, outs: FastOutputs, sz: dict, dt_s: float, period_s
     a.day_dose, a.hypo_events, a.timeline_warp = ptr(outs.day_dose), ptr(outs.hypo_events), ptr(outs.timeline_warp)
     a.timeline_pp, a.x_out = ptr(outs.timeline_pp), ptr(outs.x_out)
     check(_lib.load().gt_simulate_fast(C.byref(a), stream_ptr(device)), "gt_simulate_fast")
+
+
+FIXED_PARAM_INDEX = tuple(range(15, 30))   # AG .. R: the table's fixed block (hovorka.py:53-55)
+
+
+def uniform_fixed(params) -> np.ndarray:
+    """Row 0 of the parameter matrix after verifying that every patient shares
+    the fixed parameters (hovorka_distributions.yaml: 'identical for every
+    generated patient'); the fused kernel folds them into launch constants."""
+    t = torch()
+    idx = list(FIXED_PARAM_INDEX)
+    cols = params[:, idx]
+    if not bool((cols == cols[0:1]).all()):
+        raise _lib.GlucosimError("the fused path needs fixed parameters shared by all patients; "
+                                 "use the parity path (noise='reference') for per-patient overrides")
+    return params[0].detach().cpu().numpy().astype(np.float64)
 
 
 @dataclass

@@ -212,7 +212,7 @@ def test_diverged_patients_excluded_exactly(dev):
     cfg = SimulationConfig(horizon_s=2 * 86400.0, seed=2, dt_s=60.0)
     pop = generate_population(3, 64, device=dev)
     params = pop.params_device.clone()
-    params[5, 16] = -1.0            # tau_cgm = -1: sensor state diverges (test_simulation.py:277)
+    params[5, 4] = -5.0             # ka1 < 0: insulin action grows without bound -> non-finite
     ft = FastTrial(0, params, pop.basal_device, ThreeMealProtocol(), ControllerHyperparameters(), cfg, device=dev)
     ft.outs = engine.alloc_fast_outputs(64, 0, ft.sz, dev, per_patient_timeline=True)
     ft.step()

@@ -1,0 +1,34 @@
+"""Profiling driver: stage a FastTrial and run simulate+reduce a few times.
+
+    python tools/prof_fast.py [n_patients] [weeks] [reps]
+"""
+import os
+import sys
+import time
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+
+import torch  # noqa: E402
+
+from paper_2202_13927_b200.config import SimulationConfig  # noqa: E402
+from paper_2202_13927_b200.controller import ControllerHyperparameters  # noqa: E402
+from paper_2202_13927_b200.population import generate_population  # noqa: E402
+from paper_2202_13927_b200.protocol import ThreeMealProtocol  # noqa: E402
+from paper_2202_13927_b200.trial import FastTrial  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 20000
+weeks = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+dev = torch.device("cuda", 0)
+cfg = SimulationConfig(horizon_s=weeks * 7 * 86400.0, seed=1, dt_s=60.0)
+pop = generate_population(1, n, device=dev, on_exhausted="redraw_weight")
+ft = FastTrial(0, pop.params_device, pop.basal_device, ThreeMealProtocol(), ControllerHyperparameters(),
+               cfg, device=dev)
+for r in range(reps):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ft.step()
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    print(f"rep {r}: {dt * 1000:.2f} ms  {n * weeks / dt:.4g} patient-weeks/s", flush=True)
