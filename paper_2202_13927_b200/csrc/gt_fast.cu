@@ -43,6 +43,7 @@ struct Uni {
   double sqG, sigEh, sqrtR, rK1, pred_k, u_basal_k, u_bolus_k, u_gluc_k;
   double dt, period, horizon_s;
   int32_t ps, n_ctl, ctl_per_day, grid_ctl, hypoL, pad;
+  uint32_t rk[20];  // Philox round keys (k0 + r*W0, k1 + r*W1): constant-bank operands
 };
 
 // Per-patient constants (registers).
@@ -68,16 +69,24 @@ __device__ __forceinline__ void make_pc(const double* __restrict__ p, const Uni&
 }
 
 // ------------------------------------------------------------ noise
+__device__ __forceinline__ void mulwide(uint32_t a, uint32_t b, uint32_t& lo, uint32_t& hi) {
+  uint64_t p;
+  asm("mul.wide.u32 %0, %1, %2;" : "=l"(p) : "r"(a), "r"(b));  // one IMAD.WIDE.U32
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(p));
+}
+
+// Philox4x32-10 with the round keys precomputed in the kernel-parameter
+// bank: per round 2 IMAD.WIDE.U32 + 2 LOP3 (3-input XOR with a c[] key).
 __device__ __forceinline__ U4 philox_fast(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
-                                          uint32_t k0, uint32_t k1) {
+                                          const uint32_t* __restrict__ rk) {
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
-    if (r > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
-    const uint64_t p0 = (uint64_t)0xD2511F53u * c0;   // IMAD.WIDE.U32: hi and lo at once
-    const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
-    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0;
-    const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
-    c1 = (uint32_t)p1; c3 = (uint32_t)p0; c0 = n0; c2 = n2;
+    uint32_t lo0, hi0, lo1, hi1;
+    mulwide(c0, 0xD2511F53u, lo0, hi0);
+    mulwide(c2, 0xCD9E8D57u, lo1, hi1);
+    const uint32_t n0 = hi1 ^ c1 ^ rk[2 * r];
+    const uint32_t n2 = hi0 ^ c3 ^ rk[2 * r + 1];
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
   }
   return U4{c0, c1, c2, c3};
 }
@@ -250,7 +259,6 @@ __global__ void __launch_bounds__(kFastBS, 4) fast_kernel(const gt_fast_args a, 
   uint8_t* my_hist8 = reinterpret_cast<uint8_t*>(s_hist);
 
   const int ps = PS_T > 0 ? PS_T : u.ps;
-  const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
   double hu_ins = 0.0, hu2 = 0.0, basal = 0.0;
   int32_t g_idx = 0, next_grid_ctl = 0;
   double hrr = 0.0;
@@ -260,7 +268,7 @@ __global__ void __launch_bounds__(kFastBS, 4) fast_kernel(const gt_fast_args a, 
     // noise for tick k (counter = (k, pid, role, 0))
     double z0, z1, z2, zm = 0.0;
     if (NOISE == GT_NOISE_PHILOX) {
-      const U4 r = philox_fast((uint32_t)k, pid, a.noise_role, 0u, k0, k1);
+      const U4 r = philox_fast((uint32_t)k, pid, a.noise_role, 0u, u.rk);
       float f0, f1, f2, f3;
       box_muller(r.x, r.y, f0, f1);
       box_muller(r.z, r.w, f2, f3);
@@ -579,6 +587,11 @@ static Uni make_uni(const gt_fast_args& a) {
   u.ctl_per_day = (int32_t)std::llround(86400.0 / a.period_s);
   u.grid_ctl = (int32_t)(a.grid_step_ticks / a.period_steps);
   u.hypoL = (int32_t)a.hypo_min_ticks;
+  uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
+  for (int r = 0; r < 10; ++r) {
+    u.rk[2 * r] = k0; u.rk[2 * r + 1] = k1;
+    k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+  }
   return u;
 }
 
