@@ -41,7 +41,7 @@ struct Uni {
   double h, ginK, aS, hS, aZ1, hTg, aZ2, cG;
   double aE1, bE1, aE2, bE2, aE3, bE3, qex, sex;
   double sqG, sigEh, sqrtR, rK1, pred_k, u_basal_k, u_bolus_k, u_gluc_k;
-  double dt, period, horizon_s;
+  double dt, period, horizon_s, meal_dur_min;
   int32_t ps, n_ctl, ctl_per_day, grid_ctl, hypoL, pad;
   uint32_t rk[20];  // Philox round keys (k0 + r*W0, k1 + r*W1): constant-bank operands
 };
@@ -165,10 +165,13 @@ __global__ void __launch_bounds__(kFastBS, 4) fast_kernel(const gt_fast_args a, 
   // s_thr[k+1] = bits of THRESHOLDS[k]; s_thr[0] = -inf, s_thr[247] = +inf
   __shared__ long long s_thr[GT_N_THRESHOLDS + 2];
   __shared__ double s_hyper[GT_N_HYPER];
+  __shared__ double s_hc[5];  // hyper-derived controller constants (same IEEE values)
   extern __shared__ uint32_t s_hist[];  // [kHistWords * kFastBS], dynamic (> 48 KB total)
   __shared__ double s_d[N_SC][kFastBS];
   __shared__ int32_t s_i[N_SI][kFastBS];
   __shared__ gt_meal_gen s_gen;
+  __shared__ uint16_t s_mk[3][3][kFastBS];  // THREE_MEAL day window: ks, ke, kp offsets
+  __shared__ double s_mc[3][kFastBS];       // THREE_MEAL day window: carbs (g)
   const int tid = threadIdx.x;
   for (int q = tid; q < GT_N_THRESHOLDS + 2; q += kFastBS)
     s_thr[q] = q == 0 ? LLONG_MIN : (q == GT_N_THRESHOLDS + 1 ? LLONG_MAX
@@ -176,6 +179,14 @@ __global__ void __launch_bounds__(kFastBS, 4) fast_kernel(const gt_fast_args a, 
   for (int q = tid; q < GT_N_HYPER; q += kFastBS) s_hyper[q] = a.hyper[q];
   for (int q = tid; q < kHistWords * kFastBS; q += kFastBS) s_hist[q] = 0u;
   if (tid == 0) s_gen = a.meal_gen;
+  __syncthreads();
+  if (tid == 0) {
+    s_hc[0] = D_(M_(s_hyper[HPREDHOR], 60.0), u.period);  // prediction factor (controller.py:393)
+    s_hc[1] = S_(1.0, s_hyper[HFILTER]);
+    s_hc[2] = M_(s_hyper[HLOCKMIN], 60.0);
+    s_hc[3] = A_(s_hyper[HGLUCTHR], s_hyper[HHYST]);
+    s_hc[4] = A_(s_hyper[HEXGLUCTHR], s_hyper[HHYST]);
+  }
   __syncthreads();
 
   const int64_t i = (int64_t)blockIdx.x * kFastBS + tid;
@@ -237,9 +248,11 @@ __global__ void __launch_bounds__(kFastBS, 4) fast_kernel(const gt_fast_args a, 
     }
     return three_meal_at(&s_gen, a.seed, pid, m, u.dt, u.period, u.horizon_s);
   };
-  int32_t m_ks, m_ke;
-  double gin;
-  {
+  int32_t m_ks = INT_MAX, m_ke = INT_MAX;
+  double gin = 0.0;
+  int m_slot = 3;                      // THREE_MEAL: cursor within the current day (3 = done)
+  int32_t day_k0 = 0, day_ctl0 = 0;    // first tick / controller period of the current day
+  if (PROTO == GT_PROTO_CSR) {
     const MealT m0 = meal_at(0);
     m_ks = m0.ks; m_ke = m0.ke; gin = u.ginK * m0.rate;
     s_i[SI_MEALM][tid] = 0;
@@ -248,6 +261,27 @@ __global__ void __launch_bounds__(kFastBS, 4) fast_kernel(const gt_fast_args a, 
     s_d[SC_ANNCARBS][tid] = m0.carbs;
     s_i[SI_EXPTR][tid] = 0;
   }
+  // THREE_MEAL day window: the day's 3 meals, generated warp-uniformly at the
+  // day's first tick (no divergence), tick offsets relative to the day start
+  // (uint16, 0xFFFF = no meal) and carbs.
+  auto load_slot = [&](int j) {
+    const int ks = s_mk[0][j][tid];
+    if (ks == 0xFFFF) { m_ks = m_ke = INT_MAX; gin = 0.0; return; }
+    m_ks = day_k0 + ks; m_ke = day_k0 + s_mk[1][j][tid];
+    gin = u.ginK * (s_mc[j][tid] / u.meal_dur_min);  // rate = g / duration (simulation.py:162)
+  };
+  auto gen_day = [&](int32_t d) {
+    for (int j = 0; j < 3; ++j) {
+      const MealT mt = three_meal_at(&s_gen, a.seed, pid, 3 * d + j, u.dt, u.period, u.horizon_s);
+      const bool ok = mt.ks != INT_MAX;
+      s_mk[0][j][tid] = ok ? (uint16_t)(mt.ks - day_k0) : (uint16_t)0xFFFF;
+      s_mk[1][j][tid] = ok ? (uint16_t)(mt.ke - day_k0) : (uint16_t)0xFFFF;
+      s_mk[2][j][tid] = ok ? (uint16_t)(mt.kp - day_ctl0) : (uint16_t)0xFFFF;
+      s_mc[j][tid] = mt.carbs;
+    }
+    m_slot = 0;
+    load_slot(0);
+  };
 
   // ---- accumulators
   double bg_sum = 0.0, day_basal = 0.0;
@@ -281,11 +315,17 @@ __global__ void __launch_bounds__(kFastBS, 4) fast_kernel(const gt_fast_args a, 
     }
     // disturbances at tick k (_kernel.py:85-94); meals never overlap and
     // last >= 1 tick, so at most one advance per step
-    while (k >= m_ke) {  // single pass for generated meals (duration >= dt)
-      const int32_t m = s_i[SI_MEALM][tid] + 1;
-      s_i[SI_MEALM][tid] = m;
-      const MealT mt = meal_at(m);
-      m_ks = mt.ks; m_ke = mt.ke; gin = u.ginK * mt.rate;
+    if (PROTO == GT_PROTO_CSR) {
+      while (k >= m_ke) {
+        const int32_t m = s_i[SI_MEALM][tid] + 1;
+        s_i[SI_MEALM][tid] = m;
+        const MealT mt = meal_at(m);
+        m_ks = mt.ks; m_ke = mt.ke; gin = u.ginK * mt.rate;
+      }
+    } else if (k >= m_ke) {  // generated meals last >= 1 tick and never overlap
+      ++m_slot;
+      if (m_slot < 3) load_slot(m_slot);
+      else { m_ks = m_ke = INT_MAX; gin = 0.0; }
     }
     const double gin_k = (k >= m_ks) ? gin : 0.0;
     bool ex_active = false;
@@ -313,7 +353,15 @@ __global__ void __launch_bounds__(kFastBS, 4) fast_kernel(const gt_fast_args a, 
       }
       // announced carbs starting within [t, t+P)
       double announced = 0.0;
-      int32_t akp = s_i[SI_ANNKP][tid];
+      if (PROTO == GT_PROTO_THREE_MEAL) {
+        // meals are >= 1 h apart: at most one starts in a period; adding the
+        // others' 0.0 keeps the reference's sum exact
+        const int rel = ctl - day_ctl0;
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          announced = A_(announced, s_mk[2][j][tid] == rel ? s_mc[j][tid] : 0.0);
+      }
+      int32_t akp = PROTO == GT_PROTO_CSR ? s_i[SI_ANNKP][tid] : INT_MAX;
       if (akp <= ctl) {
         int32_t am = s_i[SI_ANNM][tid];
         double carbs = s_d[SC_ANNCARBS][tid];
@@ -335,7 +383,7 @@ __global__ void __launch_bounds__(kFastBS, 4) fast_kernel(const gt_fast_args a, 
       int flags = s_i[SI_FLAGS][tid];
       double filt = s_d[SC_FILT][tid], prev;
       if (!(flags & 4)) { filt = y; prev = y; flags |= 4; }
-      else { prev = filt; filt = A_(M_(S_(1.0, H[HFILTER]), filt), M_(H[HFILTER], y)); }
+      else { prev = filt; filt = A_(M_(s_hc[1], filt), M_(H[HFILTER], y)); }
       s_d[SC_FILT][tid] = filt; s_d[SC_PREV][tid] = prev;
       const double trend = S_(filt, prev);
       const bool exercising = HAS_EX && phase >= 0.0;
@@ -357,11 +405,11 @@ __global__ void __launch_bounds__(kFastBS, 4) fast_kernel(const gt_fast_args a, 
         flags &= ~2;
       }
       if (!done) {
-        const double pred = A_(filt, M_(trend, D_(M_(H[HPREDHOR], 60.0), u.period)));
+        const double pred = A_(filt, M_(trend, s_hc[0]));
         if (!(flags & 1)) {
           if (filt < gluc_thr || pred < gluc_thr) flags |= 1;
         } else {
-          if (filt >= A_(gluc_thr, H[HHYST]) && pred >= gluc_thr) flags &= ~1;
+          if (filt >= (exercising ? s_hc[4] : s_hc[3]) && pred >= gluc_thr) flags &= ~1;
         }
         double wend = s_d[SC_WEND][tid];
         if (wend > 0.0) {
@@ -379,7 +427,7 @@ __global__ void __launch_bounds__(kFastBS, 4) fast_kernel(const gt_fast_args a, 
           }
         }
         if (flags & 1) {
-          if (filt < gluc_thr && trend < -H[HMICROTREND] && S_(t_s, s_d[SC_LASTG][tid]) >= M_(H[HLOCKMIN], 60.0)) {
+          if (filt < gluc_thr && trend < -H[HMICROTREND] && S_(t_s, s_d[SC_LASTG][tid]) >= s_hc[2]) {
             if (micro > H[HMAXGLUC]) micro = H[HMAXGLUC];
             b_gluc = micro;
             s_d[SC_LASTG][tid] = t_s;
@@ -517,6 +565,10 @@ __global__ void __launch_bounds__(kFastBS, 4) fast_kernel(const gt_fast_args a, 
       }
       day_basal = 0.0; s_d[SC_DBOLUS][tid] = 0.0; s_d[SC_DGLUC][tid] = 0.0;
     }
+    if (PROTO == GT_PROTO_THREE_MEAL && ctl == day_ctl0 + (ctl == 0 ? 0 : u.ctl_per_day)) {
+      if (ctl > 0) { day_ctl0 = ctl; day_k0 = ctl * ps; }
+      gen_day(ctl / u.ctl_per_day);
+    }
     if (__all_sync(0xffffffffu, !alive)) break;
     const int32_t kb0 = ctl * ps;
     step(kb0, true, ctl);
@@ -579,6 +631,7 @@ static Uni make_uni(const gt_fast_args& a) {
   u.rK1 = h * 0.003;
   u.dt = a.dt_s; u.period = a.period_s;
   u.horizon_s = (double)a.horizon_ticks * a.dt_s;
+  u.meal_dur_min = (double)a.meal_gen.duration_s / 60.0;
   u.u_basal_k = h * (1000.0 / 60.0);
   u.u_bolus_k = h * (1000.0 / (a.period_s / 60.0));
   u.u_gluc_k = h * (1.0 / (a.period_s / 60.0));
@@ -622,9 +675,18 @@ int gt_launch_fast(const gt_fast_args* a, cudaStream_t st) {
     gt_set_error("gt_simulate_fast: grid step must be a multiple of the controller period");
     return GT_EUNSUPPORTED;
   }
-  if (a->proto_kind == GT_PROTO_THREE_MEAL && (double)a->meal_gen.duration_s < a->dt_s) {
-    gt_set_error("gt_simulate_fast: meals shorter than one step are not supported");
-    return GT_EUNSUPPORTED;
+  if (a->proto_kind == GT_PROTO_THREE_MEAL) {
+    const gt_meal_gen& g = a->meal_gen;
+    const bool in_day = g.clock_s[0] - g.jitter_s >= 0.0 &&
+                        g.clock_s[2] + g.jitter_s + g.duration_s <= 86400.0;
+    const double span = 2.0 * g.jitter_s + g.duration_s;
+    const bool apart = g.clock_s[1] - g.clock_s[0] >= span + a->period_s &&
+                       g.clock_s[2] - g.clock_s[1] >= span + a->period_s;
+    if ((double)g.duration_s < a->dt_s || a->dt_s < 2.0 || !in_day || !apart) {
+      gt_set_error("gt_simulate_fast: 3-meal generator needs meals within the day, >= one "
+                   "controller period apart, lasting >= one step, and dt >= 2 s");
+      return GT_EUNSUPPORTED;
+    }
   }
   const gt::Uni u = gt::make_uni(*a);
   const unsigned grid = (unsigned)((a->n + gt::kFastBS - 1) / gt::kFastBS);
