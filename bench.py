@@ -153,7 +153,7 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    n_sample = max(threads * 16, 256)
+    n_sample = max(threads * 64, 512)
     vals = []
     for i in range(args.warmup + args.steps):
         v, wall = cpu_baseline(n_sample, WEEKS, threads)
@@ -276,7 +276,7 @@ def run_ours(args):
     cpu_v, cpu_wall = (None, None)
     if not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        cpu_n = max(threads * 16, 256)
+        cpu_n = max(threads * 64, 512)
         cpu_v, cpu_wall = cpu_baseline(cpu_n, WEEKS, threads)
     q = analytics.metric_quantiles(acc_all)
     h2d = params_h.numel() * 8 + basal_h.numel() * 8
@@ -301,7 +301,7 @@ def run_ours(args):
                      "flops_per_step": F, "peak_source": peak_src,
                      "kernel_ms": sim_s * 1000.0, "share_of_step": float(np.mean(sim_ms) / np.mean(step_ms))},
         "cpu_baseline": ({"value": cpu_v, "unit": "patient-weeks/s", "cores": os.cpu_count(), "kind": "port",
-                          "sample": f"{max((os.cpu_count() or 1) * 16, 256)} patients x {WEEKS} weeks (oracle C "
+                          "sample": f"{max((os.cpu_count() or 1) * 64, 512)} patients x {WEEKS} weeks (oracle C "
                                     f"restatement, OpenMP, {cpu_wall:.1f} s wall)"} if cpu_v else None),
         "e2e": {"value": pw_per_step / (e2e / 1000.0), "unit": "patient-weeks/s",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
