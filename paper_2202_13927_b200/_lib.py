@@ -127,7 +127,7 @@ def load(path: str | None = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = path or LIB_PATH
+    p = path or os.environ.get("GLUCOSIM_LIB") or LIB_PATH
     if not os.path.exists(p):
         raise GlucosimError(
             f"libglucosim.so not built ({p}); run __graft_entry__.build() or "

@@ -32,6 +32,9 @@
 
 namespace gt {
 
+#ifndef GT_FAST_MINB
+#define GT_FAST_MINB 4  // resident 128-thread blocks per SM (register budget 128)
+#endif
 constexpr int kFastBS = 128;
 constexpr int kHistWords = (GT_N_BG_BINS + 3) / 4;  // 62 packed uint8x4 words per lane
 
@@ -159,7 +162,7 @@ enum { SC_FILT, SC_PREV, SC_ICR, SC_SUSP, SC_LASTG, SC_WEND, SC_WPEAK, SC_WMIN,
 enum { SI_FLAGS, SI_ANNKP, SI_ANNM, SI_MEALM, SI_EXPTR, N_SI };  // flags: mode | exdone<<1 | init<<2
 
 template <int PROTO, int NOISE, int PS_T>
-__global__ void __launch_bounds__(kFastBS, 4) fast_kernel(const gt_fast_args a, const Uni u) {
+__global__ void __launch_bounds__(kFastBS, GT_FAST_MINB) fast_kernel(const gt_fast_args a, const Uni u) {
   constexpr bool HAS_EX = (PROTO == GT_PROTO_CSR);
   constexpr bool CLAMP_GUT = (NOISE == GT_NOISE_INJECTED);
   // s_thr[k+1] = bits of THRESHOLDS[k]; s_thr[0] = -inf, s_thr[247] = +inf
@@ -250,7 +253,7 @@ __global__ void __launch_bounds__(kFastBS, 4) fast_kernel(const gt_fast_args a, 
   };
   int32_t m_ks = INT_MAX, m_ke = INT_MAX;
   double gin = 0.0;
-  int m_slot = 3;                      // THREE_MEAL: cursor within the current day (3 = done)
+  int32_t act_lo = INT_MAX, act_hi = INT_MAX;  // THREE_MEAL: active steps of this period
   int32_t day_k0 = 0, day_ctl0 = 0;    // first tick / controller period of the current day
   if (PROTO == GT_PROTO_CSR) {
     const MealT m0 = meal_at(0);
@@ -279,18 +282,35 @@ __global__ void __launch_bounds__(kFastBS, 4) fast_kernel(const gt_fast_args a, 
       s_mk[2][j][tid] = ok ? (uint16_t)(mt.kp - day_ctl0) : (uint16_t)0xFFFF;
       s_mc[j][tid] = mt.carbs;
     }
-    m_slot = 0;
+    s_i[SI_MEALM][tid] = 0;
     load_slot(0);
   };
 
   // ---- accumulators
   double bg_sum = 0.0, day_basal = 0.0;
+  // flush the lane's uint8 histogram into its HBM column (bins 0..246; bin
+  // 247 is the dead-lane sink) and clear it
+  auto flush_hist = [&]() {
+    for (int w = 0; w < kHistWords; ++w) {
+      const uint32_t word = s_hist[w * kFastBS + tid];
+      if (word == 0u) continue;
+      s_hist[w * kFastBS + tid] = 0u;
+      if (!inrange) continue;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const uint32_t c = (word >> (8 * b)) & 0xFFu;
+        const int bin = 4 * w + b;
+        if (c && bin < GT_N_BG_BINS) a.bg_hist[(int64_t)bin * n + i] += (int32_t)c;
+      }
+    }
+  };
   int kb_min = INT_MAX, kb_max = -1;
   int run39 = 0, run30 = 0, ev39 = 0, ev30 = 0;
   int32_t* ghist = a.bg_hist;
   if (inrange)
     for (int b = 0; b < GT_N_BG_BINS; ++b) ghist[(int64_t)b * n + i] = 0;
   uint8_t* my_hist8 = reinterpret_cast<uint8_t*>(s_hist);
+  const int tid4 = tid * 4;  // byte index of bin b: ((b >> 2) * kFastBS + tid) * 4 + (b & 3)
 
   const int ps = PS_T > 0 ? PS_T : u.ps;
   double hu_ins = 0.0, hu2 = 0.0, basal = 0.0;
@@ -298,7 +318,7 @@ __global__ void __launch_bounds__(kFastBS, 4) fast_kernel(const gt_fast_args a, 
   double hrr = 0.0;
 
   // ---------------------------------------------------------- one step
-  auto step = [&](const int32_t k, const bool tick, const int32_t ctl) {
+  auto step = [&](const int32_t k, const bool tick, const int32_t ctl, const int32_t k_base) {
     // noise for tick k (counter = (k, pid, role, 0))
     double z0, z1, z2, zm = 0.0;
     if (NOISE == GT_NOISE_PHILOX) {
@@ -322,12 +342,19 @@ __global__ void __launch_bounds__(kFastBS, 4) fast_kernel(const gt_fast_args a, 
         const MealT mt = meal_at(m);
         m_ks = mt.ks; m_ke = mt.ke; gin = u.ginK * mt.rate;
       }
-    } else if (k >= m_ke) {  // generated meals last >= 1 tick and never overlap
-      ++m_slot;
-      if (m_slot < 3) load_slot(m_slot);
-      else { m_ks = m_ke = INT_MAX; gin = 0.0; }
+    } else if (tick) {
+      // generated meals are >= one period apart, so the active window of the
+      // current meal within this period [act_lo, act_hi) is fixed at the tick
+      while (m_ke <= k) {
+        const int j = ++s_i[SI_MEALM][tid];
+        if (j < 3) load_slot(j);
+        else { m_ks = m_ke = INT_MAX; gin = 0.0; }
+      }
+      act_lo = m_ks - k; act_hi = m_ke - k;
     }
-    const double gin_k = (k >= m_ks) ? gin : 0.0;
+    const int32_t sk = k - k_base;
+    const double gin_k = PROTO == GT_PROTO_CSR ? ((k >= m_ks) ? gin : 0.0)
+                                               : ((sk >= act_lo && sk < act_hi) ? gin : 0.0);
     bool ex_active = false;
     int ex_ptr = 0;
     if (HAS_EX) {
@@ -457,6 +484,7 @@ __global__ void __launch_bounds__(kFastBS, 4) fast_kernel(const gt_fast_args a, 
       }
       s_i[SI_FLAGS][tid] = flags;
       basal = b_basal;
+      day_basal = fma(b_basal, (double)ps, day_basal);  // basal held for the whole period
       hu_ins = fma(b_bolus, u.u_bolus_k, b_basal * u.u_basal_k);   // h * (u[0] + u[1])
       hu2 = b_gluc * u.u_gluc_k;                                 // h * u[2]
       if (b_bolus > 0.0 || b_gluc > 0.0) {
@@ -471,30 +499,38 @@ __global__ void __launch_bounds__(kFastBS, 4) fast_kernel(const gt_fast_args a, 
       // SURVEY.md §7): use the reference's exact division for that tick
       bg = Q1 / (a.params[ii * NP + PVG] * a.params[ii * NP + PW]);
     }
-    if (alive && !(fabs(bg) < INFINITY)) { alive = false; status = GT_STATUS_NONFINITE; death_tick = k; }
-    {
-      // exact searchsorted(THRESHOLDS, bg, 'right') for bg >= 0: FP32
-      // estimate (off by at most one), then exact int64 compares against the
-      // sentinel-padded table.  Dead lanes count into the padding bin 247.
-      const float bf = __double2float_rz(bg);
-      int kb = min(max(__float2int_rz(bf * 10.0f) - 4, 0), GT_N_THRESHOLDS);
-      const long long bb = __double_as_longlong(bg);
-      kb += (s_thr[kb + 1] <= bb) - (s_thr[kb] > bb);
-      kb = alive ? kb : GT_N_BG_BINS;
-      const int widx = ((kb >> 2) * kFastBS + tid) * 4 + (kb & 3);
-      const uint8_t v = my_hist8[widx];
-      my_hist8[widx] = v == 254 ? 0 : v + 1;
-      if (v == 254 && kb < GT_N_BG_BINS) ghist[(int64_t)kb * n + i] += 255;  // flush before the uint8 saturates
-      bg_sum += bg;
-      // extremes: only a tick in a new lowest/highest bin can move them
-      if (kb <= kb_min) { const double o = s_d[SC_BGMIN][tid]; s_d[SC_BGMIN][tid] = bg < o ? bg : o; kb_min = kb; }
-      if (kb >= kb_max && alive) { const double o = s_d[SC_BGMAX][tid]; s_d[SC_BGMAX][tid] = bg > o ? bg : o; kb_max = kb; }
-      run39 = kb <= 34 ? run39 + 1 : 0;  // bg < 3.9 (THRESHOLDS[34])
-      run30 = kb <= 25 ? run30 + 1 : 0;  // bg < 3.0 (THRESHOLDS[25])
-      ev39 += run39 == u.hypoL;
-      ev30 += run30 == u.hypoL;
+    if (__builtin_expect(!(fabs(bg) < INFINITY), 0) && alive) {
+      alive = false; status = GT_STATUS_NONFINITE; death_tick = k;
     }
-    day_basal += basal;
+    {
+      // searchsorted(THRESHOLDS, bg, 'right') for bg >= 0.  THRESHOLDS[i] =
+      // RN((5+i)/10), so away from a threshold the bin is floor(10 bg) - 4
+      // (clamped to [0, 246]); the FP32 estimate decides whenever 10 bg is
+      // more than 1e-4 from an integer (its error is < 4e-5 up to bg = 25.6)
+      // and the exact int64 compare against the table settles the rest.
+      const float t10 = __double2float_rz(bg) * 10.0f;
+      const float fl = floorf(t10);
+      int kb = min(max((int)fl - 4, 0), GT_N_THRESHOLDS);
+      const float fr = t10 - fl;
+      if (__builtin_expect(!(fr > 1e-4f && fr < 0.9999f), 0)) {
+        const long long bb = __double_as_longlong(bg);
+        kb = min(max(kb, 0), GT_N_THRESHOLDS);
+        kb += (s_thr[kb + 1] <= bb) - (s_thr[kb] > bb);
+      }
+      kb = alive ? kb : GT_N_BG_BINS;  // dead lanes count into the padding bin 247
+      my_hist8[(kb >> 2) * (4 * kFastBS) + tid4 + (kb & 3)] += 1;  // < 255: flushed every flush_every periods
+      bg_sum += bg;
+      // extremes: only a tick in the lowest/highest bin so far can move them;
+      // hypo runs: only ticks below 3.9 mmol/L (or ending such a run) matter
+      if (__builtin_expect(kb <= kb_min || kb >= kb_max || kb <= 34 || run39 > 0, 0) && alive) {
+        if (kb <= kb_min) { const double o = s_d[SC_BGMIN][tid]; s_d[SC_BGMIN][tid] = bg < o ? bg : o; kb_min = kb; }
+        if (kb >= kb_max) { const double o = s_d[SC_BGMAX][tid]; s_d[SC_BGMAX][tid] = bg > o ? bg : o; kb_max = kb; }
+        run39 = kb <= 34 ? run39 + 1 : 0;  // bg < 3.9 (THRESHOLDS[34])
+        run30 = kb <= 25 ? run30 + 1 : 0;  // bg < 3.0 (THRESHOLDS[25])
+        ev39 += run39 == u.hypoL;
+        ev30 += run30 == u.hypoL;
+      }
+    }
     if (tick && ctl == next_grid_ctl) {  // timeline point (warp-uniform)
       next_grid_ctl += u.grid_ctl;
       const long long v = __double2ll_rn(bg * kFpScale);
@@ -554,7 +590,10 @@ __global__ void __launch_bounds__(kFastBS, 4) fast_kernel(const gt_fast_args a, 
 
   const int n_ctl = u.n_ctl;
   int next_day_ctl = u.ctl_per_day, day_idx = 0;
+  const int flush_every = max(1, 254 / ps);   // periods until a uint8 bin could reach 255
+  int next_flush_ctl = flush_every;
   for (int ctl = 0; ctl < n_ctl; ++ctl) {
+    if (ctl == next_flush_ctl) { next_flush_ctl += flush_every; flush_hist(); }
     // day boundary: flush the finished day's dose sums (_kernel.py:133-149)
     if (ctl == next_day_ctl) {
       next_day_ctl += u.ctl_per_day;
@@ -571,12 +610,12 @@ __global__ void __launch_bounds__(kFastBS, 4) fast_kernel(const gt_fast_args a, 
     }
     if (__all_sync(0xffffffffu, !alive)) break;
     const int32_t kb0 = ctl * ps;
-    step(kb0, true, ctl);
+    step(kb0, true, ctl, kb0);
     if (PS_T > 0) {
 #pragma unroll
-      for (int s = 1; s < PS_T; ++s) step(kb0 + s, false, ctl);
+      for (int s = 1; s < PS_T; ++s) step(kb0 + s, false, ctl, kb0);
     } else {
-      for (int s = 1; s < ps; ++s) step(kb0 + s, false, ctl);
+      for (int s = 1; s < ps; ++s) step(kb0 + s, false, ctl, kb0);
     }
   }
   // an all-dead warp stopped early: its remaining timeline partials are identities
@@ -594,10 +633,7 @@ __global__ void __launch_bounds__(kFastBS, 4) fast_kernel(const gt_fast_args a, 
     double* dd = a.day_dose + (last_day * 3) * n + i;
     dd[0] = day_basal; dd[n] = s_d[SC_DBOLUS][tid]; dd[2 * n] = s_d[SC_DGLUC][tid];
   }
-  for (int b = 0; b < GT_N_BG_BINS; ++b) {
-    const int widx = ((b >> 2) * kFastBS + tid) * 4 + (b & 3);
-    ghist[(int64_t)b * n + i] += my_hist8[widx];
-  }
+  flush_hist();
   a.status[i] = status;
   a.ticks[i] = status == GT_STATUS_OK ? a.horizon_ticks : (death_tick < 0 ? 0 : death_tick);
   a.bg_stats[i] = s_d[SC_BGMIN][tid];
