@@ -144,7 +144,13 @@ typedef struct gt_fast_args {
     int32_t proto_kind, noise_kind, controller, record_timeline_per_patient;
     double dt_s, period_s;
     int64_t period_steps, horizon_ticks, grid_step_ticks, n_days, n_grid, hypo_min_ticks;
-    uint32_t noise_role, pad0;
+    uint32_t noise_role;
+    /* 1 = re-run only the warps that contain a lane whose `status` (an output
+     * of a previous launch over the same arrays) is GT_STATUS_NONFINITE, with
+     * those lanes masked: rewrites the other lanes' outputs and the warps'
+     * timeline partials so no statistic includes a diverged patient
+     * (analytics.py:267-269); warps without one exit at once. */
+    int32_t rerun_diverged;
     /* Values of the non-sampled ("fixed", hovorka_distributions.yaml:46-81)
      * parameters shared by every patient of the launch, in p[30] order; the
      * fused kernel folds them into launch constants (kernel-parameter bank)

@@ -61,7 +61,7 @@ class FastArgs(C.Structure):
         ("dt_s", D), ("period_s", D),
         ("period_steps", I64), ("horizon_ticks", I64), ("grid_step_ticks", I64),
         ("n_days", I64), ("n_grid", I64), ("hypo_min_ticks", I64),
-        ("noise_role", U32), ("pad0", U32), ("fixed", D * 30),
+        ("noise_role", U32), ("rerun_diverged", I32), ("fixed", D * 30),
         ("params", P), ("x0", P), ("c0", P), ("hyper", P), ("assumed_basal", P), ("active", P),
         ("meal_gen", MealGen),
         ("meal_off", P), ("meal_ks", P), ("meal_ke", P), ("meal_kp", P),

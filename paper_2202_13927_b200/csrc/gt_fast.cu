@@ -202,7 +202,10 @@ __global__ void __launch_bounds__(kFastBS, GT_FAST_MINB) fast_kernel(const gt_fa
   const int64_t n_warps = (n + 31) >> 5;
   const double* __restrict__ H = s_hyper;
 
-  bool alive = inrange && (a.active == nullptr || a.active[i] != 0);
+  // rerun mode: only warps holding a diverged lane re-simulate (lanes masked)
+  const bool was_bad = a.rerun_diverged && inrange && a.status[i] == GT_STATUS_NONFINITE;
+  if (a.rerun_diverged && !__any_sync(0xffffffffu, was_bad)) return;
+  bool alive = inrange && !was_bad && (a.active == nullptr || a.active[i] != 0);
   int status = (inrange && !alive) ? GT_STATUS_EXCLUDED : GT_STATUS_OK;
   int32_t death_tick = -1;
 
@@ -627,7 +630,7 @@ __global__ void __launch_bounds__(kFastBS, GT_FAST_MINB) fast_kernel(const gt_fa
         dst[0] = 0; dst[1] = LLONG_MAX; dst[2] = LLONG_MIN;
       }
   }
-  if (!inrange) return;
+  if (!inrange || was_bad) return;  // a rerun keeps the diverged lanes' status
   const int64_t last_day = a.n_days - 1;
   {
     double* dd = a.day_dose + (last_day * 3) * n + i;

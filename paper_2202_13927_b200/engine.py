@@ -194,7 +194,8 @@ def alloc_fast_outputs(n: int, pid0: int, sz: dict, device, per_patient_timeline
 def launch_fast(inputs: dict, outs: FastOutputs, sz: dict, dt_s: float, period_s: float,
                 seed: int, noise_role: int, hypo_min_ticks: int, device,
                 meal_spec: dict | None = None, csr: dict | None = None,
-                injected: dict | None = None, controller_code: int = 0, fixed=None) -> None:
+                injected: dict | None = None, controller_code: int = 0, fixed=None,
+                rerun_diverged: bool = False) -> None:
     """Enqueue the fused integrator on the current stream (no sync).
     ``fixed``: the launch-uniform values of the non-sampled parameters
     (p[30] order); defaults to row 0 of ``inputs['params']`` after checking
@@ -215,6 +216,7 @@ def launch_fast(inputs: dict, outs: FastOutputs, sz: dict, dt_s: float, period_s
                                                           sz["grid_step_ticks"])
     a.n_days, a.n_grid, a.hypo_min_ticks = sz["n_days"], sz["n_grid"], int(hypo_min_ticks)
     a.noise_role = noise_role
+    a.rerun_diverged = int(bool(rerun_diverged))
     for k in ("params", "x0", "c0", "hyper", "assumed_basal", "active"):
         setattr(a, k, ptr(inputs.get(k)))
     a.meal_gen = meal_gen_struct(meal_spec)

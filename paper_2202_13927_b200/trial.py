@@ -69,6 +69,7 @@ class FastTrial:
             self.x0, _ub, self.ss_status = engine.steady_state(params, config.initial_bg_mmol_per_l, self.device)
             self.c0 = engine.controller_init(self.hyper, icr_initial_factor(profile), basal, self.device)
             self.hyper_d = engine.dev(self.hyper, t.float64, self.device)
+            self.fixed = engine.uniform_fixed(params)   # verified once, at staging
             self.active = (self.ss_status == GT_STATUS_OK).to(t.int32)
             self.meal_spec, self.csr = None, None
             if isinstance(generator, ThreeMealProtocol):
@@ -111,7 +112,7 @@ class FastTrial:
         }
 
     # ------------------------------------------------------------- running
-    def simulate(self, active=None, injected=None):
+    def simulate(self, active=None, injected=None, rerun_diverged=False):
         """Enqueue the fused integrator (current stream, no sync)."""
         inputs = dict(self._inputs)
         if active is not None:
@@ -119,7 +120,8 @@ class FastTrial:
         engine.launch_fast(inputs, self.outs, self.sz, self.config.dt_s,
                            self.config.controller_period_s, self.seed, rng.ROLE_DEVICE_NOISE,
                            self.hypo_min_ticks, self.device, meal_spec=self.meal_spec, csr=self.csr,
-                           injected=injected, controller_code=self.code)
+                           injected=injected, controller_code=self.code, fixed=self.fixed,
+                           rerun_diverged=rerun_diverged)
 
     def reduce(self):
         engine.launch_reduce(self.outs, self.red, self.sz, self.config.dt_s, self.device)
@@ -131,17 +133,10 @@ class FastTrial:
         self.reduce()
 
     def _rerun_if_diverged(self):
-        t = engine.torch()
-        st = self.outs.status
-        bad = st == GT_STATUS_NONFINITE
-        if not bool(bad.any()):
-            return
-        # re-simulate with diverged lanes masked out (deterministic streams)
-        active = self.active.clone()
-        active[bad] = 0
-        status_keep = st.clone()
-        self.simulate(active=active)
-        self.outs.status.copy_(t.where(bad, status_keep, self.outs.status))
+        """Device-side: warps that hold a diverged patient re-simulate with it
+        masked (deterministic streams); all other warps exit at once.  No host
+        synchronisation."""
+        self.simulate(rerun_diverged=True)
 
     # ----------------------------------------------------------- readback
     def accumulator(self) -> TrialAccumulator:
