@@ -141,7 +141,10 @@ typedef struct gt_meal_gen {
 typedef struct gt_fast_args {
     int64_t n, pid0;
     uint64_t seed;
-    int32_t proto_kind, noise_kind, controller, record_timeline_per_patient;
+    int32_t proto_kind, noise_kind, controller;
+    /* horizon slices of the persistent schedule (0 = chosen from the SM count;
+     * results are identical for any value) */
+    int32_t n_slices;
     double dt_s, period_s;
     int64_t period_steps, horizon_ticks, grid_step_ticks, n_days, n_grid, hypo_min_ticks;
     uint32_t noise_role;

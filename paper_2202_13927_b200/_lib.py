@@ -57,7 +57,7 @@ class FastArgs(C.Structure):
     _fields_ = [
         ("n", I64), ("pid0", I64), ("seed", U64),
         ("proto_kind", I32), ("noise_kind", I32), ("controller", I32),
-        ("record_timeline_per_patient", I32),
+        ("n_slices", I32),
         ("dt_s", D), ("period_s", D),
         ("period_steps", I64), ("horizon_ticks", I64), ("grid_step_ticks", I64),
         ("n_days", I64), ("n_grid", I64), ("hypo_min_ticks", I64),

@@ -1,30 +1,35 @@
 // Fast fused closed-loop integrator (BASELINE north_star subsystem 3).
 //
-// One thread = one virtual patient for the whole horizon.  SDE state,
-// Philox counters and per-step accumulators live in registers; the 247-bin
-// BG histogram of each patient lives in shared memory as saturating uint8
-// counters (flushed to the patient's HBM column before they overflow), and
-// the state that changes only on controller ticks (controller memory,
-// announcement cursor, dose sums, BG extremes) lives in shared memory, so
-// HBM sees parameters in and metrics out only.
+// One thread = one virtual patient.  SDE state, Philox counters and per-step
+// accumulators live in registers; the 247-bin BG histogram of each patient
+// lives in shared memory as uint8 counters (flushed into the patient's HBM
+// column every 254/period_steps periods), and the state that changes only on
+// controller ticks (controller memory, meal window, dose sums, BG extremes)
+// lives in shared memory, so HBM sees parameters in and metrics out only.
 //
 // Same model (hovorka.py:76-150), controller (controller.py:343-458) and
 // statistics (_kernel.py:137-160) as the parity kernel, re-associated for
 // the FP64 pipe: each linear update x += h*(b*y - x/tau) is evaluated as
 // fma(x, 1-h/tau, h*b*y) with per-patient constants folded at start-up and
-// launch-uniform constants (fixed parameters) in the kernel-parameter bank.
-// For every state of that form the reference's projection max(x,0) is a
-// no-op (monotone rounding of a - b with 0 <= b <= a), so it is applied only
-// to Q1 and Q2 (and D1/D2 when arbitrary noise is injected: device Philox
-// normals are bounded by 6.7 sigma, far inside the gut states' positivity
-// margin of ~30 sigma).  Results agree with the parity path to rounding;
-// DESIGN.md §4 documents the resulting threshold ties.
+// launch-uniform constants (fixed parameters, Philox round keys) in the
+// kernel-parameter bank.  For every state of that form the reference's
+// projection max(x,0) is a no-op (monotone rounding of a - b with
+// 0 <= b <= a), so it is applied only to Q1 and Q2 (and D1/D2 when arbitrary
+// noise is injected: device Philox normals are bounded by 6.7 sigma, far
+// inside the gut states' positivity margin of ~30 sigma).  Results agree with
+// the parity path to rounding; DESIGN.md §4 documents the threshold ties.
+//
+// Scheduling: the kernel is persistent.  Each warp repeatedly claims a unit
+// (chunk c, logical warp w) = 32 patients x one slice of the horizon, in
+// chunk-major order, from a global counter; a unit with c > 0 waits until
+// unit (c-1, w) has released its saved state.  Slicing the horizon removes
+// the wave quantisation of one-thread-per-patient launches (100k patients =
+// 3125 warps on 2368 resident warp slots = 1.32 waves): the host picks the
+// slice count that makes the unit count divide the slots best.
 //
 // Loop structure is warp-uniform: outer loop over controller periods, inner
-// loop over the period's integration steps (compile-time unrolled for the
-// common period of 5 steps); all lanes of a warp hit controller ticks, day
-// boundaries and timeline grid points together, so divergence comes only
-// from the model's own branches.
+// loop over the period's integration steps; all lanes of a warp hit
+// controller ticks, day boundaries and timeline grid points together.
 #include <cmath>
 #include <climits>
 #include <cstdlib>
@@ -47,6 +52,15 @@ struct Uni {
   double dt, period, horizon_s, meal_dur_min;
   int32_t ps, n_ctl, ctl_per_day, grid_ctl, hypoL, pad;
   uint32_t rk[20];  // Philox round keys (k0 + r*W0, k1 + r*W1): constant-bank operands
+};
+
+// Persistent work distribution (see the header comment).
+struct Sched {
+  int* counter;      // next unit to claim
+  int* done;         // [n_warps] slices completed per logical warp
+  double* sd;        // [SD_N][n] saved FP64 lane state between slices
+  int* si;           // [SI_N][n] saved integer lane state between slices
+  int n_units, n_warps, chunk_ctl, n_chunks;
 };
 
 // Per-patient constants (registers).
@@ -156,13 +170,30 @@ __device__ __forceinline__ long long warp_max64(long long v) {
   return v;
 }
 
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+
 // Shared-memory per-lane slots (SoA, [slot][tid]).
-enum { SC_FILT, SC_PREV, SC_ICR, SC_SUSP, SC_LASTG, SC_WEND, SC_WPEAK, SC_WMIN,
-       SC_BGMIN, SC_BGMAX, SC_DBOLUS, SC_DGLUC, SC_ANNCARBS, N_SC };
+enum { SC_FILT, SC_ICR, SC_SUSP, SC_LASTG, SC_WEND, SC_WPEAK, SC_WMIN,
+       SC_BGMIN, SC_BGMAX, SC_DBOLUS, SC_DGLUC, SC_ANNCARBS, SC_ASSUMED, N_SC };
 enum { SI_FLAGS, SI_ANNKP, SI_ANNM, SI_MEALM, SI_EXPTR, N_SI };  // flags: mode | exdone<<1 | init<<2
 
-template <int PROTO, int NOISE, int PS_T>
-__global__ void __launch_bounds__(kFastBS, GT_FAST_MINB) fast_kernel(const gt_fast_args a, const Uni u) {
+// Saved lane state between horizon slices ([field][n] in Sched::sd / si).
+enum { SD_Q1, SD_Q2, SD_S1, SD_S2, SD_I, SD_X1, SD_X2, SD_X3, SD_D1, SD_D2, SD_G, SD_Z1, SD_Z2,
+       SD_E1, SD_E2, SD_E3, SD_BGSUM, SD_DAYBASAL, SD_HUINS, SD_HU2, SD_GIN, SD_MC0, SD_MC1,
+       SD_MC2, SD_SC0, SD_N = SD_SC0 + N_SC };
+enum { SV_MKS, SV_MKE, SV_ACTLO, SV_ACTHI, SV_KBMIN, SV_KBMAX, SV_RUN39, SV_RUN30, SV_EV39,
+       SV_EV30, SV_ALIVE, SV_STATUS, SV_DEATH, SV_MK0, SV_SI0 = SV_MK0 + 9, SV_N = SV_SI0 + N_SI };
+
+template <int PROTO, int NOISE>
+__global__ void __launch_bounds__(kFastBS, GT_FAST_MINB)
+fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
   constexpr bool HAS_EX = (PROTO == GT_PROTO_CSR);
   constexpr bool CLAMP_GUT = (NOISE == GT_NOISE_INJECTED);
   // s_thr[k+1] = bits of THRESHOLDS[k]; s_thr[0] = -inf, s_thr[247] = +inf
@@ -190,463 +221,541 @@ __global__ void __launch_bounds__(kFastBS, GT_FAST_MINB) fast_kernel(const gt_fa
     s_hc[3] = A_(s_hyper[HGLUCTHR], s_hyper[HHYST]);
     s_hc[4] = A_(s_hyper[HEXGLUCTHR], s_hyper[HHYST]);
   }
-  __syncthreads();
+  __syncthreads();  // no block-wide barrier after this point: warps run independently
 
-  const int64_t i = (int64_t)blockIdx.x * kFastBS + tid;
-  const int64_t n = a.n;
-  const bool inrange = i < n;
-  const int64_t ii = inrange ? i : 0;
-  const uint32_t pid = (uint32_t)(a.pid0 + i);
   const int lane = tid & 31;
-  const int64_t warp_global = ((int64_t)blockIdx.x * kFastBS + tid) >> 5;
-  const int64_t n_warps = (n + 31) >> 5;
+  const int64_t n = a.n;
+  const int64_t n_warps = sch.n_warps;
   const double* __restrict__ H = s_hyper;
-
-  // rerun mode: only warps holding a diverged lane re-simulate (lanes masked)
-  const bool was_bad = a.rerun_diverged && inrange && a.status[i] == GT_STATUS_NONFINITE;
-  if (a.rerun_diverged && !__any_sync(0xffffffffu, was_bad)) return;
-  bool alive = inrange && !was_bad && (a.active == nullptr || a.active[i] != 0);
-  int status = (inrange && !alive) ? GT_STATUS_EXCLUDED : GT_STATUS_OK;
-  int32_t death_tick = -1;
-
-  // ---- per-patient set-up
-  PC pc;
-  double Q1, Q2, S1, S2, I, X1, X2, X3, D1, D2, G, Z1, Z2, E1 = 0.0, E2 = 0.0, E3 = 0.0;
-  double assumed;
-  {
-    double p[NP];
-#pragma unroll
-    for (int k = 0; k < NP; ++k) p[k] = a.params[ii * NP + k];
-    make_pc(p, u, pc);
-    const double* x0 = a.x0 + ii * NS;
-    Q1 = x0[IQ1]; Q2 = x0[IQ2]; S1 = x0[IS1]; S2 = x0[IS2]; I = x0[II];
-    X1 = x0[IX1]; X2 = x0[IX2]; X3 = x0[IX3]; D1 = x0[ID1]; D2 = x0[ID2];
-    G = x0[IGSC]; Z1 = x0[IZ1]; Z2 = x0[IZ2];
-    if (HAS_EX) { E1 = x0[IE1]; E2 = x0[IE2]; E3 = x0[IE3]; }
-    const double* c0 = a.c0 + ii * NC;
-    s_d[SC_FILT][tid] = c0[CFILT]; s_d[SC_PREV][tid] = c0[CPREV]; s_d[SC_ICR][tid] = c0[CICR];
-    s_d[SC_SUSP][tid] = c0[CSUSPEND_UNTIL]; s_d[SC_LASTG][tid] = c0[CLASTGLUC];
-    s_d[SC_WEND][tid] = c0[CWINEND]; s_d[SC_WPEAK][tid] = c0[CWINPEAK]; s_d[SC_WMIN][tid] = c0[CWINMIN];
-    s_i[SI_FLAGS][tid] = (c0[CMODE] != 0.0) | ((c0[CEXBOLUSDONE] != 0.0) << 1) | ((c0[CINIT] != 0.0) << 2);
-    assumed = a.assumed_basal[ii];
-  }
-  double sqE = pc.sqE, sqG = u.sqG;
-  if (NOISE == GT_NOISE_INJECTED && a.has_noise[ii] == 0) { sqE = 0.0; sqG = 0.0; }
-  s_d[SC_BGMIN][tid] = INFINITY;
-  s_d[SC_BGMAX][tid] = -INFINITY;
-  s_d[SC_DBOLUS][tid] = 0.0;
-  s_d[SC_DGLUC][tid] = 0.0;
-
-  // meal source
-  int64_t moff = 0, n_meals_csr = 0, ex_lo = 0, n_ex = 0;
-  if (PROTO == GT_PROTO_CSR) {
-    moff = a.meal_off[ii]; n_meals_csr = a.meal_off[ii + 1] - moff;
-    ex_lo = a.ex_off[ii]; n_ex = a.ex_off[ii + 1] - ex_lo;
-  }
-  auto meal_at = [&](int32_t m) -> MealT {
-    if (PROTO == GT_PROTO_CSR) {
-      MealT r;
-      if (m >= n_meals_csr) { r.ks = r.ke = r.kp = INT_MAX; r.rate = 0.0; r.carbs = 0.0; return r; }
-      const int64_t q = moff + m;
-      r.ks = a.meal_ks[q]; r.ke = a.meal_ke[q]; r.kp = a.meal_kp[q]; r.rate = a.meal_rate[q];
-      r.carbs = a.meal_ann[q];
-      return r;
-    }
-    return three_meal_at(&s_gen, a.seed, pid, m, u.dt, u.period, u.horizon_s);
-  };
-  int32_t m_ks = INT_MAX, m_ke = INT_MAX;
-  double gin = 0.0;
-  int32_t act_lo = INT_MAX, act_hi = INT_MAX;  // THREE_MEAL: active steps of this period
-  int32_t day_k0 = 0, day_ctl0 = 0;    // first tick / controller period of the current day
-  if (PROTO == GT_PROTO_CSR) {
-    const MealT m0 = meal_at(0);
-    m_ks = m0.ks; m_ke = m0.ke; gin = u.ginK * m0.rate;
-    s_i[SI_MEALM][tid] = 0;
-    s_i[SI_ANNM][tid] = 0;
-    s_i[SI_ANNKP][tid] = m0.kp;
-    s_d[SC_ANNCARBS][tid] = m0.carbs;
-    s_i[SI_EXPTR][tid] = 0;
-  }
-  // THREE_MEAL day window: the day's 3 meals, generated warp-uniformly at the
-  // day's first tick (no divergence), tick offsets relative to the day start
-  // (uint16, 0xFFFF = no meal) and carbs.
-  auto load_slot = [&](int j) {
-    const int ks = s_mk[0][j][tid];
-    if (ks == 0xFFFF) { m_ks = m_ke = INT_MAX; gin = 0.0; return; }
-    m_ks = day_k0 + ks; m_ke = day_k0 + s_mk[1][j][tid];
-    gin = u.ginK * (s_mc[j][tid] / u.meal_dur_min);  // rate = g / duration (simulation.py:162)
-  };
-  auto gen_day = [&](int32_t d) {
-    for (int j = 0; j < 3; ++j) {
-      const MealT mt = three_meal_at(&s_gen, a.seed, pid, 3 * d + j, u.dt, u.period, u.horizon_s);
-      const bool ok = mt.ks != INT_MAX;
-      s_mk[0][j][tid] = ok ? (uint16_t)(mt.ks - day_k0) : (uint16_t)0xFFFF;
-      s_mk[1][j][tid] = ok ? (uint16_t)(mt.ke - day_k0) : (uint16_t)0xFFFF;
-      s_mk[2][j][tid] = ok ? (uint16_t)(mt.kp - day_ctl0) : (uint16_t)0xFFFF;
-      s_mc[j][tid] = mt.carbs;
-    }
-    s_i[SI_MEALM][tid] = 0;
-    load_slot(0);
-  };
-
-  // ---- accumulators
-  double bg_sum = 0.0, day_basal = 0.0;
-  // flush the lane's uint8 histogram into its HBM column (bins 0..246; bin
-  // 247 is the dead-lane sink) and clear it
-  auto flush_hist = [&]() {
-    for (int w = 0; w < kHistWords; ++w) {
-      const uint32_t word = s_hist[w * kFastBS + tid];
-      if (word == 0u) continue;
-      s_hist[w * kFastBS + tid] = 0u;
-      if (!inrange) continue;
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const uint32_t c = (word >> (8 * b)) & 0xFFu;
-        const int bin = 4 * w + b;
-        if (c && bin < GT_N_BG_BINS) a.bg_hist[(int64_t)bin * n + i] += (int32_t)c;
-      }
-    }
-  };
-  int kb_min = INT_MAX, kb_max = -1;
-  int run39 = 0, run30 = 0, ev39 = 0, ev30 = 0;
-  int32_t* ghist = a.bg_hist;
-  if (inrange)
-    for (int b = 0; b < GT_N_BG_BINS; ++b) ghist[(int64_t)b * n + i] = 0;
   uint8_t* my_hist8 = reinterpret_cast<uint8_t*>(s_hist);
   const int tid4 = tid * 4;  // byte index of bin b: ((b >> 2) * kFastBS + tid) * 4 + (b & 3)
+  const int ps = u.ps;
+  const int cpd = u.ctl_per_day;
 
-  const int ps = PS_T > 0 ? PS_T : u.ps;
-  double hu_ins = 0.0, hu2 = 0.0, basal = 0.0;
-  int32_t g_idx = 0, next_grid_ctl = 0;
-  double hrr = 0.0;
+  for (;;) {
+    // ------------------------------------------------------ claim a unit
+    int unit = 0;
+    if (lane == 0) unit = atomicAdd(sch.counter, 1);
+    unit = __shfl_sync(0xffffffffu, unit, 0);
+    if (unit >= sch.n_units) break;
+    const int chunk = unit / sch.n_warps;
+    const int64_t warp_global = unit - (int64_t)chunk * sch.n_warps;
+    const int ctl_lo = chunk * sch.chunk_ctl;
+    const int ctl_hi = min(u.n_ctl, ctl_lo + sch.chunk_ctl);
+    const bool first = chunk == 0, last = chunk == sch.n_chunks - 1;
+    const int64_t i = warp_global * 32 + lane;
+    const bool inrange = i < n;
+    const int64_t ii = inrange ? i : 0;
+    const uint32_t pid = (uint32_t)(a.pid0 + i);
 
-  // ---------------------------------------------------------- one step
-  auto step = [&](const int32_t k, const bool tick, const int32_t ctl, const int32_t k_base) {
-    // noise for tick k (counter = (k, pid, role, 0))
-    double z0, z1, z2, zm = 0.0;
-    if (NOISE == GT_NOISE_PHILOX) {
-      const U4 r = philox_fast((uint32_t)k, pid, a.noise_role, 0u, u.rk);
-      float f0, f1, f2, f3;
-      box_muller(r.x, r.y, f0, f1);
-      box_muller(r.z, r.w, f2, f3);
-      z0 = f0; z1 = f1; z2 = f2;
-      if (tick) zm = f3;
-    } else {
-      const double* wv = a.wiener + (ii * (int64_t)a.horizon_ticks + k) * 3;
-      z0 = wv[0]; z1 = wv[1]; z2 = wv[2];
-      if (tick) zm = a.meas[ii * (int64_t)u.n_ctl + ctl];
+    // rerun mode: only warps holding a diverged lane re-simulate (lanes masked)
+    const bool was_bad = a.rerun_diverged && inrange && a.status[i] == GT_STATUS_NONFINITE;
+    if (a.rerun_diverged && !__any_sync(0xffffffffu, was_bad)) {
+      __syncwarp();
+      if (lane == 0) st_release(sch.done + warp_global, chunk + 1);
+      continue;
     }
-    // disturbances at tick k (_kernel.py:85-94); meals never overlap and
-    // last >= 1 tick, so at most one advance per step
-    if (PROTO == GT_PROTO_CSR) {
-      while (k >= m_ke) {
-        const int32_t m = s_i[SI_MEALM][tid] + 1;
-        s_i[SI_MEALM][tid] = m;
-        const MealT mt = meal_at(m);
-        m_ks = mt.ks; m_ke = mt.ke; gin = u.ginK * mt.rate;
-      }
-    } else if (tick) {
-      // generated meals are >= one period apart, so the active window of the
-      // current meal within this period [act_lo, act_hi) is fixed at the tick
-      while (m_ke <= k) {
-        const int j = ++s_i[SI_MEALM][tid];
-        if (j < 3) load_slot(j);
-        else { m_ks = m_ke = INT_MAX; gin = 0.0; }
-      }
-      act_lo = m_ks - k; act_hi = m_ke - k;
+    if (!first) {  // wait for the previous slice of these 32 patients
+      if (lane == 0)
+        while (ld_acquire(sch.done + warp_global) < chunk) __nanosleep(256);
+      __syncwarp();
+      __threadfence();
     }
-    const int32_t sk = k - k_base;
-    const double gin_k = PROTO == GT_PROTO_CSR ? ((k >= m_ks) ? gin : 0.0)
-                                               : ((sk >= act_lo && sk < act_hi) ? gin : 0.0);
-    bool ex_active = false;
-    int ex_ptr = 0;
-    if (HAS_EX) {
-      ex_ptr = s_i[SI_EXPTR][tid];
-      while (ex_ptr < n_ex && k >= a.ex_ke[ex_lo + ex_ptr]) ++ex_ptr;
-      s_i[SI_EXPTR][tid] = ex_ptr;
-      ex_active = ex_ptr < n_ex && k >= a.ex_ks[ex_lo + ex_ptr];
-      hrr = ex_active ? a.ex_hrr[ex_lo + ex_ptr] : 0.0;
-    }
-    // controller tick (_kernel.py:98-135)
-    if (tick) {
-      const double t_s = (double)k * u.dt;
-      if (alive) {
-        const unsigned m = max(max(max(__double2hiint(Q1) & 0x7fffffff, __double2hiint(Q2) & 0x7fffffff),
-                                   max(__double2hiint(S1) & 0x7fffffff, __double2hiint(S2) & 0x7fffffff)),
-                               max(max(__double2hiint(I) & 0x7fffffff, __double2hiint(X1) & 0x7fffffff),
-                                   max(__double2hiint(X2) & 0x7fffffff, __double2hiint(X3) & 0x7fffffff)));
-        const unsigned m2 = max(max(max(__double2hiint(D1) & 0x7fffffff, __double2hiint(D2) & 0x7fffffff),
-                                    max(__double2hiint(G) & 0x7fffffff, __double2hiint(Z1) & 0x7fffffff)),
-                                max(max(__double2hiint(Z2) & 0x7fffffff, __double2hiint(E1) & 0x7fffffff),
-                                    max(__double2hiint(E2) & 0x7fffffff, __double2hiint(E3) & 0x7fffffff)));
-        if (max(m, m2) >= 0x7ff00000u) { alive = false; status = GT_STATUS_NONFINITE; death_tick = k; }
-      }
-      // announced carbs starting within [t, t+P)
-      double announced = 0.0;
-      if (PROTO == GT_PROTO_THREE_MEAL) {
-        // meals are >= 1 h apart: at most one starts in a period; adding the
-        // others' 0.0 keeps the reference's sum exact
-        const int rel = ctl - day_ctl0;
-#pragma unroll
-        for (int j = 0; j < 3; ++j)
-          announced = A_(announced, s_mk[2][j][tid] == rel ? s_mc[j][tid] : 0.0);
-      }
-      int32_t akp = PROTO == GT_PROTO_CSR ? s_i[SI_ANNKP][tid] : INT_MAX;
-      if (akp <= ctl) {
-        int32_t am = s_i[SI_ANNM][tid];
-        double carbs = s_d[SC_ANNCARBS][tid];
-        while (akp <= ctl) {
-          if (akp == ctl) announced += carbs;
-          ++am;
-          const MealT mt = meal_at(am);
-          akp = mt.kp; carbs = mt.carbs;
-        }
-        s_i[SI_ANNM][tid] = am; s_i[SI_ANNKP][tid] = akp; s_d[SC_ANNCARBS][tid] = carbs;
-      }
-      double phase = -1.0;
-      if (HAS_EX && ex_active && a.ex_announced[ex_lo + ex_ptr] != 0.0)
-        phase = t_s - a.ex_start_s[ex_lo + ex_ptr];
-      const double y = A_(G, M_(u.sqrtR, zm));
-      // ---- controller_step_vec (controller.py:343-458); state in shared memory.
-      // Explicit IEEE operations in the reference's order: the controller is
-      // bit-identical to the reference's for identical sensor readings.
-      int flags = s_i[SI_FLAGS][tid];
-      double filt = s_d[SC_FILT][tid], prev;
-      if (!(flags & 4)) { filt = y; prev = y; flags |= 4; }
-      else { prev = filt; filt = A_(M_(s_hc[1], filt), M_(H[HFILTER], y)); }
-      s_d[SC_FILT][tid] = filt; s_d[SC_PREV][tid] = prev;
-      const double trend = S_(filt, prev);
-      const bool exercising = HAS_EX && phase >= 0.0;
-      const double setpoint = exercising ? H[HEXSETPOINT] : H[HSETPOINT];
-      const double gluc_thr = exercising ? H[HEXGLUCTHR] : H[HGLUCTHR];
-      double micro = exercising ? H[HEXMICROUG] : H[HMICROUG];
-      double b_basal = 0.0, b_bolus = 0.0, b_gluc = 0.0;
-      bool done = false;
-      if (exercising) {
-        if (!(flags & 2)) {
-          flags |= 2;
-          if (filt < H[HEXBOLUSBG]) {
-            b_gluc = fmin(H[HEXBOLUS], H[HMAXGLUC]);
-            s_d[SC_LASTG][tid] = t_s;
-            done = true;
-          }
-        }
-      } else {
-        flags &= ~2;
-      }
-      if (!done) {
-        const double pred = A_(filt, M_(trend, s_hc[0]));
-        if (!(flags & 1)) {
-          if (filt < gluc_thr || pred < gluc_thr) flags |= 1;
-        } else {
-          if (filt >= (exercising ? s_hc[4] : s_hc[3]) && pred >= gluc_thr) flags &= ~1;
-        }
-        double wend = s_d[SC_WEND][tid];
-        if (wend > 0.0) {
-          double wpeak = fmax(s_d[SC_WPEAK][tid], filt);
-          double wmin = fmin(s_d[SC_WMIN][tid], filt);
-          s_d[SC_WPEAK][tid] = wpeak; s_d[SC_WMIN][tid] = wmin;
-          if (t_s >= wend) {
-            double icr = s_d[SC_ICR][tid];
-            if (wmin < H[HUNDERBG]) icr = M_(icr, A_(1.0, H[HICRSTEPUP]));
-            else if (S_(wpeak, H[HSETPOINT]) > H[HEXCHI]) icr = M_(icr, S_(1.0, H[HICRSTEP]));
-            if (icr < H[HICRMIN]) icr = H[HICRMIN];
-            if (icr > H[HICRMAX]) icr = H[HICRMAX];
-            s_d[SC_ICR][tid] = icr;
-            s_d[SC_WEND][tid] = 0.0;
-          }
-        }
-        if (flags & 1) {
-          if (filt < gluc_thr && trend < -H[HMICROTREND] && S_(t_s, s_d[SC_LASTG][tid]) >= s_hc[2]) {
-            if (micro > H[HMAXGLUC]) micro = H[HMAXGLUC];
-            b_gluc = micro;
-            s_d[SC_LASTG][tid] = t_s;
-          }
-        } else {
-          if (announced > 0.0) {
-            const double icr = s_d[SC_ICR][tid];
-            double b = A_(D_(announced, icr), D_(S_(filt, setpoint), M_(H[HCFICR], icr)));
-            if (filt > H[HSUPBG]) b = A_(b, D_(M_(M_(H[HSUPFRAC], assumed), H[HSUSPMIN]), 60.0));
-            if (b < 0.0) b = 0.0;
-            if (b > H[HMAXBOLUS]) b = H[HMAXBOLUS];
-            b_bolus = b;
-            s_d[SC_SUSP][tid] = A_(t_s, M_(H[HSUSPMIN], 60.0));
-            s_d[SC_WEND][tid] = A_(t_s, M_(H[HMEALWIN], 60.0));
-            s_d[SC_WPEAK][tid] = filt;
-            s_d[SC_WMIN][tid] = filt;
-          }
-          if (!(t_s < s_d[SC_SUSP][tid])) {
-            double factor = A_(A_(1.0, M_(H[HBKP], S_(filt, setpoint))), M_(H[HBKD], trend));
-            if (factor < 0.0) factor = 0.0;
-            if (factor > H[HBFMAX]) factor = H[HBFMAX];
-            double b = M_(assumed, factor);
-            if (exercising) b = M_(b, H[HEXBFACTOR]);
-            b_basal = b;
-          }
-        }
-      }
-      s_i[SI_FLAGS][tid] = flags;
-      basal = b_basal;
-      day_basal = fma(b_basal, (double)ps, day_basal);  // basal held for the whole period
-      hu_ins = fma(b_bolus, u.u_bolus_k, b_basal * u.u_basal_k);   // h * (u[0] + u[1])
-      hu2 = b_gluc * u.u_gluc_k;                                 // h * u[2]
-      if (b_bolus > 0.0 || b_gluc > 0.0) {
-        s_d[SC_DBOLUS][tid] += b_bolus;
-        s_d[SC_DGLUC][tid] += b_gluc;
-      }
-    }
-    // statistics at tick k (_kernel.py:137-160)
-    double bg = M_(Q1, pc.invVGw);  // explicit: never fused into the sums below
-    if (tick && ctl == 0) {
-      // the steady state puts BG(0) on a histogram edge (6.0 = THRESHOLDS[55],
-      // SURVEY.md §7): use the reference's exact division for that tick
-      bg = Q1 / (a.params[ii * NP + PVG] * a.params[ii * NP + PW]);
-    }
-    if (__builtin_expect(!(fabs(bg) < INFINITY), 0) && alive) {
-      alive = false; status = GT_STATUS_NONFINITE; death_tick = k;
-    }
+
+    // ---- per-patient constants (recomputed per slice: cheap, register-free)
+    PC pc;
     {
-      // searchsorted(THRESHOLDS, bg, 'right') for bg >= 0.  THRESHOLDS[i] =
-      // RN((5+i)/10), so away from a threshold the bin is floor(10 bg) - 4
-      // (clamped to [0, 246]); the FP32 estimate decides whenever 10 bg is
-      // more than 1e-4 from an integer (its error is < 4e-5 up to bg = 25.6)
-      // and the exact int64 compare against the table settles the rest.
-      const float t10 = __double2float_rz(bg) * 10.0f;
-      const float fl = floorf(t10);
-      int kb = min(max((int)fl - 4, 0), GT_N_THRESHOLDS);
-      const float fr = t10 - fl;
-      if (__builtin_expect(!(fr > 1e-4f && fr < 0.9999f), 0)) {
-        const long long bb = __double_as_longlong(bg);
-        kb = min(max(kb, 0), GT_N_THRESHOLDS);
-        kb += (s_thr[kb + 1] <= bb) - (s_thr[kb] > bb);
-      }
-      kb = alive ? kb : GT_N_BG_BINS;  // dead lanes count into the padding bin 247
-      my_hist8[(kb >> 2) * (4 * kFastBS) + tid4 + (kb & 3)] += 1;  // < 255: flushed every flush_every periods
-      bg_sum += bg;
-      // extremes: only a tick in the lowest/highest bin so far can move them;
-      // hypo runs: only ticks below 3.9 mmol/L (or ending such a run) matter
-      if (__builtin_expect(kb <= kb_min || kb >= kb_max || kb <= 34 || run39 > 0, 0) && alive) {
-        if (kb <= kb_min) { const double o = s_d[SC_BGMIN][tid]; s_d[SC_BGMIN][tid] = bg < o ? bg : o; kb_min = kb; }
-        if (kb >= kb_max) { const double o = s_d[SC_BGMAX][tid]; s_d[SC_BGMAX][tid] = bg > o ? bg : o; kb_max = kb; }
-        run39 = kb <= 34 ? run39 + 1 : 0;  // bg < 3.9 (THRESHOLDS[34])
-        run30 = kb <= 25 ? run30 + 1 : 0;  // bg < 3.0 (THRESHOLDS[25])
-        ev39 += run39 == u.hypoL;
-        ev30 += run30 == u.hypoL;
-      }
-    }
-    if (tick && ctl == next_grid_ctl) {  // timeline point (warp-uniform)
-      next_grid_ctl += u.grid_ctl;
-      const long long v = __double2ll_rn(bg * kFpScale);
-      const long long ssum = warp_sum64(alive ? v : 0LL);
-      const long long smin = warp_min64(alive ? v : LLONG_MAX);
-      const long long smax = warp_max64(alive ? v : LLONG_MIN);
-      if (lane == 0 && warp_global < n_warps) {
-        long long* dst = (long long*)a.timeline_warp + ((int64_t)g_idx * n_warps + warp_global) * 3;
-        dst[0] = ssum; dst[1] = smin; dst[2] = smax;
-      }
-      if (a.timeline_pp && inrange) a.timeline_pp[(int64_t)g_idx * n + i] = alive ? bg : 0.0;
-      ++g_idx;
-    }
-    // Euler–Maruyama step, re-associated (hovorka.py:76-150)
-    const double ab = HAS_EX ? fma(u.sex, E3, 1.0) : 1.0;
-    const double ub = HAS_EX ? fma(u.qex, E2, 1.0) : 1.0;
-    const double x1e = X1 * ab, x2e = X2 * ab;
-    const double t1 = x1e * Q1;
-    const double bg45 = bg * (1.0 / 4.5);
-    const double hf01 = M_(pc.hF01w, bg45 < 1.0 ? bg45 : 1.0);  // explicit: fixed rounding
-    const double ren = fma(Q1, u.rK1, -pc.rK0);
-    const double hren = ren > 0.0 ? ren : 0.0;
-    const double egp = fma(-pc.hE, X3, pc.hE);
-    const double hegp = fma(u.cG, Z2, egp > 0.0 ? egp : 0.0);
-    double dq = fma(pc.hk12, Q2, D2 * pc.hTG);
-    dq = fma(-hf01, ub, dq);
-    dq = fma(-u.h, t1, dq);
-    dq = (dq - hren) + hegp;
-    // projection max(x, 0) (_kernel.py:175-177): keeps NaN like `if x < 0: x = 0`
-    const double q1n = fma(sqE, z0, Q1 + dq);
-    const double q2n = fma(Q2, pc.aK12, u.h * fma(-x2e, Q2, t1));
-    const double nQ1 = q1n < 0.0 ? 0.0 : q1n;
-    const double nQ2 = q2n < 0.0 ? 0.0 : q2n;
-    double nD1 = fma(D1, fma(sqG, z1, pc.aG), gin_k);
-    double nD2 = fma(D2, fma(sqG, z2, pc.aG), D1 * pc.hTG);
-    if (CLAMP_GUT) { nD1 = nD1 < 0.0 ? 0.0 : nD1; nD2 = nD2 < 0.0 ? 0.0 : nD2; }
-    const double nS2 = fma(S2, pc.aI, S1 * pc.hTI);
-    S1 = fma(S1, pc.aI, hu_ins);
-    const double nI = fma(I, pc.cI, S2 * pc.dI);
-    S2 = nS2;
-    X1 = fma(X1, pc.ax1, I * pc.bx1);
-    X2 = fma(X2, pc.ax2, I * pc.bx2);
-    X3 = fma(X3, pc.ax3, I * pc.bx3);
-    I = nI;
-    const double nZ2 = fma(Z2, u.aZ2, Z1 * u.hTg);
-    Z1 = fma(Z1, u.aZ1, hu2);
-    Z2 = nZ2;
-    if (HAS_EX) {
-      const double nE2 = fma(E2, u.aE2, E1 * u.bE2);
-      const double nE3 = fma(E3, u.aE3, E1 * u.bE3);
-      E1 = fma(E1, u.aE1, u.bE1 * hrr);
-      E2 = nE2; E3 = nE3;
-    }
-    G = fma(G, u.aS, bg * u.hS);
-    Q1 = nQ1; Q2 = nQ2; D1 = nD1; D2 = nD2;
-  };
-
-  const int n_ctl = u.n_ctl;
-  int next_day_ctl = u.ctl_per_day, day_idx = 0;
-  const int flush_every = max(1, 254 / ps);   // periods until a uint8 bin could reach 255
-  int next_flush_ctl = flush_every;
-  for (int ctl = 0; ctl < n_ctl; ++ctl) {
-    if (ctl == next_flush_ctl) { next_flush_ctl += flush_every; flush_hist(); }
-    // day boundary: flush the finished day's dose sums (_kernel.py:133-149)
-    if (ctl == next_day_ctl) {
-      next_day_ctl += u.ctl_per_day;
-      const int64_t day = day_idx++;
-      if (inrange) {
-        double* dd = a.day_dose + (day * 3) * n + i;
-        dd[0] = day_basal; dd[n] = s_d[SC_DBOLUS][tid]; dd[2 * n] = s_d[SC_DGLUC][tid];
-      }
-      day_basal = 0.0; s_d[SC_DBOLUS][tid] = 0.0; s_d[SC_DGLUC][tid] = 0.0;
-    }
-    if (PROTO == GT_PROTO_THREE_MEAL && ctl == day_ctl0 + (ctl == 0 ? 0 : u.ctl_per_day)) {
-      if (ctl > 0) { day_ctl0 = ctl; day_k0 = ctl * ps; }
-      gen_day(ctl / u.ctl_per_day);
-    }
-    if (__all_sync(0xffffffffu, !alive)) break;
-    const int32_t kb0 = ctl * ps;
-    step(kb0, true, ctl, kb0);
-    if (PS_T > 0) {
+      double p[NP];
 #pragma unroll
-      for (int s = 1; s < PS_T; ++s) step(kb0 + s, false, ctl, kb0);
+      for (int k = 0; k < NP; ++k) p[k] = a.params[ii * NP + k];
+      make_pc(p, u, pc);
+    }
+    double sqE = pc.sqE, sqG = u.sqG;
+    if (NOISE == GT_NOISE_INJECTED && a.has_noise[ii] == 0) { sqE = 0.0; sqG = 0.0; }
+    int64_t moff = 0, n_meals_csr = 0, ex_lo = 0, n_ex = 0;
+    if (PROTO == GT_PROTO_CSR) {
+      moff = a.meal_off[ii]; n_meals_csr = a.meal_off[ii + 1] - moff;
+      ex_lo = a.ex_off[ii]; n_ex = a.ex_off[ii + 1] - ex_lo;
+    }
+    auto meal_at = [&](int32_t m) -> MealT {
+      if (PROTO == GT_PROTO_CSR) {
+        MealT r;
+        if (m >= n_meals_csr) { r.ks = r.ke = r.kp = INT_MAX; r.rate = 0.0; r.carbs = 0.0; return r; }
+        const int64_t q = moff + m;
+        r.ks = a.meal_ks[q]; r.ke = a.meal_ke[q]; r.kp = a.meal_kp[q]; r.rate = a.meal_rate[q];
+        r.carbs = a.meal_ann[q];
+        return r;
+      }
+      return three_meal_at(&s_gen, a.seed, pid, m, u.dt, u.period, u.horizon_s);
+    };
+
+    // ---- lane state: initialise (first slice) or restore
+    double Q1, Q2, S1, S2, I, X1, X2, X3, D1, D2, G, Z1, Z2, E1 = 0.0, E2 = 0.0, E3 = 0.0;
+    double bg_sum, day_basal, hu_ins, hu2, gin;
+    int32_t m_ks, m_ke, act_lo, act_hi;
+    int kb_min, kb_max, run39, run30, ev39, ev30;
+    bool alive;
+    int status, death_tick;
+    if (first) {
+      alive = inrange && !was_bad && (a.active == nullptr || a.active[i] != 0);
+      status = (inrange && !alive) ? GT_STATUS_EXCLUDED : GT_STATUS_OK;
+      death_tick = -1;
+      const double* x0 = a.x0 + ii * NS;
+      Q1 = x0[IQ1]; Q2 = x0[IQ2]; S1 = x0[IS1]; S2 = x0[IS2]; I = x0[II];
+      X1 = x0[IX1]; X2 = x0[IX2]; X3 = x0[IX3]; D1 = x0[ID1]; D2 = x0[ID2];
+      G = x0[IGSC]; Z1 = x0[IZ1]; Z2 = x0[IZ2];
+      if (HAS_EX) { E1 = x0[IE1]; E2 = x0[IE2]; E3 = x0[IE3]; }
+      const double* c0 = a.c0 + ii * NC;
+      s_d[SC_FILT][tid] = c0[CFILT]; s_d[SC_ICR][tid] = c0[CICR];
+      s_d[SC_SUSP][tid] = c0[CSUSPEND_UNTIL]; s_d[SC_LASTG][tid] = c0[CLASTGLUC];
+      s_d[SC_WEND][tid] = c0[CWINEND]; s_d[SC_WPEAK][tid] = c0[CWINPEAK]; s_d[SC_WMIN][tid] = c0[CWINMIN];
+      s_i[SI_FLAGS][tid] = (c0[CMODE] != 0.0) | ((c0[CEXBOLUSDONE] != 0.0) << 1) | ((c0[CINIT] != 0.0) << 2);
+      s_d[SC_ASSUMED][tid] = a.assumed_basal[ii];
+      s_d[SC_BGMIN][tid] = INFINITY;
+      s_d[SC_BGMAX][tid] = -INFINITY;
+      s_d[SC_DBOLUS][tid] = 0.0;
+      s_d[SC_DGLUC][tid] = 0.0;
+      bg_sum = 0.0; day_basal = 0.0; hu_ins = 0.0; hu2 = 0.0;
+      kb_min = INT_MAX; kb_max = -1; run39 = run30 = ev39 = ev30 = 0;
+      m_ks = m_ke = INT_MAX; gin = 0.0; act_lo = act_hi = INT_MAX;
+      if (PROTO == GT_PROTO_CSR) {
+        const MealT m0 = meal_at(0);
+        m_ks = m0.ks; m_ke = m0.ke; gin = u.ginK * m0.rate;
+        s_i[SI_MEALM][tid] = 0;
+        s_i[SI_ANNM][tid] = 0;
+        s_i[SI_ANNKP][tid] = m0.kp;
+        s_d[SC_ANNCARBS][tid] = m0.carbs;
+        s_i[SI_EXPTR][tid] = 0;
+      }
+      if (inrange)
+        for (int b = 0; b < GT_N_BG_BINS; ++b) a.bg_hist[(int64_t)b * n + i] = 0;
     } else {
+      const double* sd = sch.sd + ii;
+      const int* si = sch.si + ii;
+#define LDD(f) sd[(int64_t)(f) * n]
+#define LDI(f) si[(int64_t)(f) * n]
+      Q1 = LDD(SD_Q1); Q2 = LDD(SD_Q2); S1 = LDD(SD_S1); S2 = LDD(SD_S2); I = LDD(SD_I);
+      X1 = LDD(SD_X1); X2 = LDD(SD_X2); X3 = LDD(SD_X3); D1 = LDD(SD_D1); D2 = LDD(SD_D2);
+      G = LDD(SD_G); Z1 = LDD(SD_Z1); Z2 = LDD(SD_Z2);
+      if (HAS_EX) { E1 = LDD(SD_E1); E2 = LDD(SD_E2); E3 = LDD(SD_E3); }
+      bg_sum = LDD(SD_BGSUM); day_basal = LDD(SD_DAYBASAL); hu_ins = LDD(SD_HUINS); hu2 = LDD(SD_HU2);
+      gin = LDD(SD_GIN);
+      for (int q = 0; q < N_SC; ++q) s_d[q][tid] = LDD(SD_SC0 + q);
+      for (int q = 0; q < N_SI; ++q) s_i[q][tid] = LDI(SV_SI0 + q);
+      if (PROTO == GT_PROTO_THREE_MEAL) {
+        for (int j = 0; j < 3; ++j) {
+          s_mc[j][tid] = LDD(SD_MC0 + j);
+          for (int f = 0; f < 3; ++f) s_mk[f][j][tid] = (uint16_t)LDI(SV_MK0 + 3 * f + j);
+        }
+      }
+      m_ks = LDI(SV_MKS); m_ke = LDI(SV_MKE); act_lo = LDI(SV_ACTLO); act_hi = LDI(SV_ACTHI);
+      kb_min = LDI(SV_KBMIN); kb_max = LDI(SV_KBMAX); run39 = LDI(SV_RUN39); run30 = LDI(SV_RUN30);
+      ev39 = LDI(SV_EV39); ev30 = LDI(SV_EV30); alive = LDI(SV_ALIVE) != 0;
+      status = LDI(SV_STATUS); death_tick = LDI(SV_DEATH);
+#undef LDD
+#undef LDI
+      alive = alive && inrange && !was_bad;  // padding lanes read patient 0's slot
+    }
+
+    // THREE_MEAL day window: the day's 3 meals, generated warp-uniformly at
+    // the day's first tick (no divergence), tick offsets relative to the day
+    // start (uint16, 0xFFFF = no meal) and carbs.
+    int32_t day_ctl0 = (ctl_lo / cpd) * cpd;
+    int32_t day_k0 = day_ctl0 * ps;
+    auto load_slot = [&](int j) {
+      const int ks = s_mk[0][j][tid];
+      if (ks == 0xFFFF) { m_ks = m_ke = INT_MAX; gin = 0.0; return; }
+      m_ks = day_k0 + ks; m_ke = day_k0 + s_mk[1][j][tid];
+      gin = u.ginK * (s_mc[j][tid] / u.meal_dur_min);  // rate = g / duration (simulation.py:162)
+    };
+    auto gen_day = [&](int32_t d) {
+      for (int j = 0; j < 3; ++j) {
+        const MealT mt = three_meal_at(&s_gen, a.seed, pid, 3 * d + j, u.dt, u.period, u.horizon_s);
+        const bool ok = mt.ks != INT_MAX;
+        s_mk[0][j][tid] = ok ? (uint16_t)(mt.ks - day_k0) : (uint16_t)0xFFFF;
+        s_mk[1][j][tid] = ok ? (uint16_t)(mt.ke - day_k0) : (uint16_t)0xFFFF;
+        s_mk[2][j][tid] = ok ? (uint16_t)(mt.kp - day_ctl0) : (uint16_t)0xFFFF;
+        s_mc[j][tid] = mt.carbs;
+      }
+      s_i[SI_MEALM][tid] = 0;
+      load_slot(0);
+    };
+    // flush the lane's uint8 histogram into its HBM column (bins 0..246;
+    // bin 247 is the dead-lane sink) and clear it
+    auto flush_hist = [&]() {
+      for (int w = 0; w < kHistWords; ++w) {
+        const uint32_t word = s_hist[w * kFastBS + tid];
+        if (word == 0u) continue;
+        s_hist[w * kFastBS + tid] = 0u;
+        if (!inrange) continue;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const uint32_t c = (word >> (8 * b)) & 0xFFu;
+          const int bin = 4 * w + b;
+          if (c && bin < GT_N_BG_BINS) a.bg_hist[(int64_t)bin * n + i] += (int32_t)c;
+        }
+      }
+    };
+    double hrr = 0.0;
+    // warp-uniform cursors derived from the slice start
+    int next_grid_ctl = ((ctl_lo + u.grid_ctl - 1) / u.grid_ctl) * u.grid_ctl;
+    int g_idx = next_grid_ctl / u.grid_ctl;
+    int next_day_ctl = max(cpd, ((ctl_lo + cpd - 1) / cpd) * cpd);  // day flush (ctl > 0)
+    int next_gen_ctl = ((ctl_lo + cpd - 1) / cpd) * cpd;             // day window generation
+    const int flush_every = max(1, 254 / ps);   // periods until a uint8 bin could reach 255
+    int next_flush_ctl = ctl_lo + flush_every;
+
+    // ---------------------------------------------------------- one step
+    auto step = [&](const int32_t k, const bool tick, const int32_t ctl, const int32_t k_base) {
+      // noise for tick k (counter = (k, pid, role, 0))
+      double z0, z1, z2, zm = 0.0;
+      if (NOISE == GT_NOISE_PHILOX) {
+        const U4 r = philox_fast((uint32_t)k, pid, a.noise_role, 0u, u.rk);
+        float f0, f1, f2, f3;
+        box_muller(r.x, r.y, f0, f1);
+        box_muller(r.z, r.w, f2, f3);
+        z0 = f0; z1 = f1; z2 = f2;
+        if (tick) zm = f3;
+      } else {
+        const double* wv = a.wiener + (ii * (int64_t)a.horizon_ticks + k) * 3;
+        z0 = wv[0]; z1 = wv[1]; z2 = wv[2];
+        if (tick) zm = a.meas[ii * (int64_t)u.n_ctl + ctl];
+      }
+      // disturbances at tick k (_kernel.py:85-94)
+      if (PROTO == GT_PROTO_CSR) {
+        while (k >= m_ke) {
+          const int32_t m = s_i[SI_MEALM][tid] + 1;
+          s_i[SI_MEALM][tid] = m;
+          const MealT mt = meal_at(m);
+          m_ks = mt.ks; m_ke = mt.ke; gin = u.ginK * mt.rate;
+        }
+      } else if (tick) {
+        // generated meals are >= one period apart, so the active window of
+        // the current meal within this period [act_lo, act_hi) is fixed here
+        while (m_ke <= k) {
+          const int j = ++s_i[SI_MEALM][tid];
+          if (j < 3) load_slot(j);
+          else { m_ks = m_ke = INT_MAX; gin = 0.0; }
+        }
+        act_lo = m_ks - k; act_hi = m_ke - k;
+      }
+      const int32_t sk = k - k_base;
+      const double gin_k = PROTO == GT_PROTO_CSR ? ((k >= m_ks) ? gin : 0.0)
+                                                 : ((sk >= act_lo && sk < act_hi) ? gin : 0.0);
+      bool ex_active = false;
+      int ex_ptr = 0;
+      if (HAS_EX) {
+        ex_ptr = s_i[SI_EXPTR][tid];
+        while (ex_ptr < n_ex && k >= a.ex_ke[ex_lo + ex_ptr]) ++ex_ptr;
+        s_i[SI_EXPTR][tid] = ex_ptr;
+        ex_active = ex_ptr < n_ex && k >= a.ex_ks[ex_lo + ex_ptr];
+        hrr = ex_active ? a.ex_hrr[ex_lo + ex_ptr] : 0.0;
+      }
+      // controller tick (_kernel.py:98-135)
+      if (tick) {
+        const double t_s = (double)k * u.dt;
+        if (alive) {
+          const unsigned m = max(max(max(__double2hiint(Q1) & 0x7fffffff, __double2hiint(Q2) & 0x7fffffff),
+                                     max(__double2hiint(S1) & 0x7fffffff, __double2hiint(S2) & 0x7fffffff)),
+                                 max(max(__double2hiint(I) & 0x7fffffff, __double2hiint(X1) & 0x7fffffff),
+                                     max(__double2hiint(X2) & 0x7fffffff, __double2hiint(X3) & 0x7fffffff)));
+          const unsigned m2 = max(max(max(__double2hiint(D1) & 0x7fffffff, __double2hiint(D2) & 0x7fffffff),
+                                      max(__double2hiint(G) & 0x7fffffff, __double2hiint(Z1) & 0x7fffffff)),
+                                  max(max(__double2hiint(Z2) & 0x7fffffff, __double2hiint(E1) & 0x7fffffff),
+                                      max(__double2hiint(E2) & 0x7fffffff, __double2hiint(E3) & 0x7fffffff)));
+          if (max(m, m2) >= 0x7ff00000u) { alive = false; status = GT_STATUS_NONFINITE; death_tick = k; }
+        }
+        // announced carbs starting within [t, t+P)
+        double announced = 0.0;
+        if (PROTO == GT_PROTO_THREE_MEAL) {
+          // meals are >= 1 h apart: at most one starts in a period; adding
+          // the others' 0.0 keeps the reference's sum exact
+          const int rel = ctl - day_ctl0;
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+            announced = A_(announced, s_mk[2][j][tid] == rel ? s_mc[j][tid] : 0.0);
+        }
+        int32_t akp = PROTO == GT_PROTO_CSR ? s_i[SI_ANNKP][tid] : INT_MAX;
+        if (akp <= ctl) {
+          int32_t am = s_i[SI_ANNM][tid];
+          double carbs = s_d[SC_ANNCARBS][tid];
+          while (akp <= ctl) {
+            if (akp == ctl) announced += carbs;
+            ++am;
+            const MealT mt = meal_at(am);
+            akp = mt.kp; carbs = mt.carbs;
+          }
+          s_i[SI_ANNM][tid] = am; s_i[SI_ANNKP][tid] = akp; s_d[SC_ANNCARBS][tid] = carbs;
+        }
+        double phase = -1.0;
+        if (HAS_EX && ex_active && a.ex_announced[ex_lo + ex_ptr] != 0.0)
+          phase = t_s - a.ex_start_s[ex_lo + ex_ptr];
+        const double y = A_(G, M_(u.sqrtR, zm));
+        // ---- controller_step_vec (controller.py:343-458); state in shared
+        // memory.  Explicit IEEE operations in the reference's order: the
+        // controller is bit-identical to the reference's for identical readings.
+        int flags = s_i[SI_FLAGS][tid];
+        double filt = s_d[SC_FILT][tid], prev;
+        if (!(flags & 4)) { filt = y; prev = y; flags |= 4; }
+        else { prev = filt; filt = A_(M_(s_hc[1], filt), M_(H[HFILTER], y)); }
+        s_d[SC_FILT][tid] = filt;
+        const double trend = S_(filt, prev);
+        const bool exercising = HAS_EX && phase >= 0.0;
+        const double setpoint = exercising ? H[HEXSETPOINT] : H[HSETPOINT];
+        const double gluc_thr = exercising ? H[HEXGLUCTHR] : H[HGLUCTHR];
+        double micro = exercising ? H[HEXMICROUG] : H[HMICROUG];
+        double b_basal = 0.0, b_bolus = 0.0, b_gluc = 0.0;
+        bool done = false;
+        if (exercising) {
+          if (!(flags & 2)) {
+            flags |= 2;
+            if (filt < H[HEXBOLUSBG]) {
+              b_gluc = fmin(H[HEXBOLUS], H[HMAXGLUC]);
+              s_d[SC_LASTG][tid] = t_s;
+              done = true;
+            }
+          }
+        } else {
+          flags &= ~2;
+        }
+        if (!done) {
+          const double pred = A_(filt, M_(trend, s_hc[0]));
+          if (!(flags & 1)) {
+            if (filt < gluc_thr || pred < gluc_thr) flags |= 1;
+          } else {
+            if (filt >= (exercising ? s_hc[4] : s_hc[3]) && pred >= gluc_thr) flags &= ~1;
+          }
+          const double wend = s_d[SC_WEND][tid];
+          if (wend > 0.0) {
+            const double wpeak = fmax(s_d[SC_WPEAK][tid], filt);
+            const double wmin = fmin(s_d[SC_WMIN][tid], filt);
+            s_d[SC_WPEAK][tid] = wpeak; s_d[SC_WMIN][tid] = wmin;
+            if (t_s >= wend) {
+              double icr = s_d[SC_ICR][tid];
+              if (wmin < H[HUNDERBG]) icr = M_(icr, A_(1.0, H[HICRSTEPUP]));
+              else if (S_(wpeak, H[HSETPOINT]) > H[HEXCHI]) icr = M_(icr, S_(1.0, H[HICRSTEP]));
+              if (icr < H[HICRMIN]) icr = H[HICRMIN];
+              if (icr > H[HICRMAX]) icr = H[HICRMAX];
+              s_d[SC_ICR][tid] = icr;
+              s_d[SC_WEND][tid] = 0.0;
+            }
+          }
+          if (flags & 1) {
+            if (filt < gluc_thr && trend < -H[HMICROTREND] && S_(t_s, s_d[SC_LASTG][tid]) >= s_hc[2]) {
+              if (micro > H[HMAXGLUC]) micro = H[HMAXGLUC];
+              b_gluc = micro;
+              s_d[SC_LASTG][tid] = t_s;
+            }
+          } else {
+            const double assumed = s_d[SC_ASSUMED][tid];
+            if (announced > 0.0) {
+              const double icr = s_d[SC_ICR][tid];
+              double b = A_(D_(announced, icr), D_(S_(filt, setpoint), M_(H[HCFICR], icr)));
+              if (filt > H[HSUPBG]) b = A_(b, D_(M_(M_(H[HSUPFRAC], assumed), H[HSUSPMIN]), 60.0));
+              if (b < 0.0) b = 0.0;
+              if (b > H[HMAXBOLUS]) b = H[HMAXBOLUS];
+              b_bolus = b;
+              s_d[SC_SUSP][tid] = A_(t_s, M_(H[HSUSPMIN], 60.0));
+              s_d[SC_WEND][tid] = A_(t_s, M_(H[HMEALWIN], 60.0));
+              s_d[SC_WPEAK][tid] = filt;
+              s_d[SC_WMIN][tid] = filt;
+            }
+            if (!(t_s < s_d[SC_SUSP][tid])) {
+              double factor = A_(A_(1.0, M_(H[HBKP], S_(filt, setpoint))), M_(H[HBKD], trend));
+              if (factor < 0.0) factor = 0.0;
+              if (factor > H[HBFMAX]) factor = H[HBFMAX];
+              double b = M_(assumed, factor);
+              if (exercising) b = M_(b, H[HEXBFACTOR]);
+              b_basal = b;
+            }
+          }
+        }
+        s_i[SI_FLAGS][tid] = flags;
+        day_basal = fma(b_basal, (double)ps, day_basal);  // basal held for the whole period
+        hu_ins = fma(b_bolus, u.u_bolus_k, b_basal * u.u_basal_k);   // h * (u[0] + u[1])
+        hu2 = b_gluc * u.u_gluc_k;                                 // h * u[2]
+        if (b_bolus > 0.0 || b_gluc > 0.0) {
+          s_d[SC_DBOLUS][tid] += b_bolus;
+          s_d[SC_DGLUC][tid] += b_gluc;
+        }
+      }
+      // statistics at tick k (_kernel.py:137-160)
+      double bg = M_(Q1, pc.invVGw);  // explicit: never fused into the sums below
+      if (tick && ctl == 0) {
+        // the steady state puts BG(0) on a histogram edge (6.0 = THRESHOLDS[55],
+        // SURVEY.md §7): use the reference's exact division for that tick
+        bg = Q1 / (a.params[ii * NP + PVG] * a.params[ii * NP + PW]);
+      }
+      if (__builtin_expect(!(fabs(bg) < INFINITY), 0) && alive) {
+        alive = false; status = GT_STATUS_NONFINITE; death_tick = k;
+      }
+      {
+        // searchsorted(THRESHOLDS, bg, 'right') for bg >= 0.  THRESHOLDS[i] =
+        // RN((5+i)/10), so away from a threshold the bin is floor(10 bg) - 4
+        // (clamped to [0, 246]); the FP32 estimate decides whenever 10 bg is
+        // more than 1e-4 from an integer (its error is < 4e-5 up to bg = 25.6)
+        // and the exact int64 compare against the table settles the rest.
+        const float t10 = __double2float_rz(bg) * 10.0f;
+        const float fl = floorf(t10);
+        int kb = min(max((int)fl - 4, 0), GT_N_THRESHOLDS);
+        const float fr = t10 - fl;
+        if (__builtin_expect(!(fr > 1e-4f && fr < 0.9999f), 0)) {
+          const long long bb = __double_as_longlong(bg);
+          kb = min(max(kb, 0), GT_N_THRESHOLDS);
+          kb += (s_thr[kb + 1] <= bb) - (s_thr[kb] > bb);
+        }
+        kb = alive ? kb : GT_N_BG_BINS;  // dead lanes count into the padding bin 247
+        my_hist8[(kb >> 2) * (4 * kFastBS) + tid4 + (kb & 3)] += 1;  // < 255 between flushes
+        bg_sum += bg;
+        // extremes: only a tick in the lowest/highest bin so far can move them;
+        // hypo runs: only ticks below 3.9 mmol/L (or ending such a run) matter
+        if (__builtin_expect(kb <= kb_min || kb >= kb_max || kb <= 34 || run39 > 0, 0) && alive) {
+          if (kb <= kb_min) { const double o = s_d[SC_BGMIN][tid]; s_d[SC_BGMIN][tid] = bg < o ? bg : o; kb_min = kb; }
+          if (kb >= kb_max) { const double o = s_d[SC_BGMAX][tid]; s_d[SC_BGMAX][tid] = bg > o ? bg : o; kb_max = kb; }
+          run39 = kb <= 34 ? run39 + 1 : 0;  // bg < 3.9 (THRESHOLDS[34])
+          run30 = kb <= 25 ? run30 + 1 : 0;  // bg < 3.0 (THRESHOLDS[25])
+          ev39 += run39 == u.hypoL;
+          ev30 += run30 == u.hypoL;
+        }
+      }
+      if (tick && ctl == next_grid_ctl) {  // timeline point (warp-uniform)
+        next_grid_ctl += u.grid_ctl;
+        const long long v = __double2ll_rn(bg * kFpScale);
+        const long long ssum = warp_sum64(alive ? v : 0LL);
+        const long long smin = warp_min64(alive ? v : LLONG_MAX);
+        const long long smax = warp_max64(alive ? v : LLONG_MIN);
+        if (lane == 0) {
+          long long* dst = (long long*)a.timeline_warp + ((int64_t)g_idx * n_warps + warp_global) * 3;
+          dst[0] = ssum; dst[1] = smin; dst[2] = smax;
+        }
+        if (a.timeline_pp && inrange) a.timeline_pp[(int64_t)g_idx * n + i] = alive ? bg : 0.0;
+        ++g_idx;
+      }
+      // Euler–Maruyama step, re-associated (hovorka.py:76-150)
+      const double ab = HAS_EX ? fma(u.sex, E3, 1.0) : 1.0;
+      const double ub = HAS_EX ? fma(u.qex, E2, 1.0) : 1.0;
+      const double x1e = X1 * ab, x2e = X2 * ab;
+      const double t1 = x1e * Q1;
+      const double bg45 = bg * (1.0 / 4.5);
+      const double hf01 = M_(pc.hF01w, bg45 < 1.0 ? bg45 : 1.0);  // explicit: fixed rounding
+      const double ren = fma(Q1, u.rK1, -pc.rK0);
+      const double hren = ren > 0.0 ? ren : 0.0;
+      const double egp = fma(-pc.hE, X3, pc.hE);
+      const double hegp = fma(u.cG, Z2, egp > 0.0 ? egp : 0.0);
+      double dq = fma(pc.hk12, Q2, D2 * pc.hTG);
+      dq = fma(-hf01, ub, dq);
+      dq = fma(-u.h, t1, dq);
+      dq = (dq - hren) + hegp;
+      // projection max(x, 0) (_kernel.py:175-177): keeps NaN like `if x < 0: x = 0`
+      const double q1n = fma(sqE, z0, Q1 + dq);
+      const double q2n = fma(Q2, pc.aK12, u.h * fma(-x2e, Q2, t1));
+      const double nQ1 = q1n < 0.0 ? 0.0 : q1n;
+      const double nQ2 = q2n < 0.0 ? 0.0 : q2n;
+      double nD1 = fma(D1, fma(sqG, z1, pc.aG), gin_k);
+      double nD2 = fma(D2, fma(sqG, z2, pc.aG), D1 * pc.hTG);
+      if (CLAMP_GUT) { nD1 = nD1 < 0.0 ? 0.0 : nD1; nD2 = nD2 < 0.0 ? 0.0 : nD2; }
+      const double nS2 = fma(S2, pc.aI, S1 * pc.hTI);
+      S1 = fma(S1, pc.aI, hu_ins);
+      const double nI = fma(I, pc.cI, S2 * pc.dI);
+      S2 = nS2;
+      X1 = fma(X1, pc.ax1, I * pc.bx1);
+      X2 = fma(X2, pc.ax2, I * pc.bx2);
+      X3 = fma(X3, pc.ax3, I * pc.bx3);
+      I = nI;
+      const double nZ2 = fma(Z2, u.aZ2, Z1 * u.hTg);
+      Z1 = fma(Z1, u.aZ1, hu2);
+      Z2 = nZ2;
+      if (HAS_EX) {
+        const double nE2 = fma(E2, u.aE2, E1 * u.bE2);
+        const double nE3 = fma(E3, u.aE3, E1 * u.bE3);
+        E1 = fma(E1, u.aE1, u.bE1 * hrr);
+        E2 = nE2; E3 = nE3;
+      }
+      G = fma(G, u.aS, bg * u.hS);
+      Q1 = nQ1; Q2 = nQ2; D1 = nD1; D2 = nD2;
+    };
+
+    // ------------------------------------------------- the slice's periods
+    int ctl = ctl_lo;
+    for (; ctl < ctl_hi; ++ctl) {
+      if (ctl == next_flush_ctl) { next_flush_ctl += flush_every; flush_hist(); }
+      // day boundary: flush the finished day's dose sums (_kernel.py:133-149)
+      if (ctl == next_day_ctl) {
+        next_day_ctl += cpd;
+        const int64_t day = ctl / cpd - 1;
+        if (inrange) {
+          double* dd = a.day_dose + (day * 3) * n + i;
+          dd[0] = day_basal; dd[n] = s_d[SC_DBOLUS][tid]; dd[2 * n] = s_d[SC_DGLUC][tid];
+        }
+        day_basal = 0.0; s_d[SC_DBOLUS][tid] = 0.0; s_d[SC_DGLUC][tid] = 0.0;
+      }
+      if (PROTO == GT_PROTO_THREE_MEAL && ctl == next_gen_ctl) {
+        next_gen_ctl += cpd;
+        day_ctl0 = ctl; day_k0 = ctl * ps;
+        gen_day(ctl / cpd);
+      }
+      if (__all_sync(0xffffffffu, !alive)) break;
+      const int32_t kb0 = ctl * ps;
+      step(kb0, true, ctl, kb0);
       for (int s = 1; s < ps; ++s) step(kb0 + s, false, ctl, kb0);
     }
-  }
-  // an all-dead warp stopped early: its remaining timeline partials are identities
-  {
-    const int n_grid = (int)a.n_grid;
-    for (; g_idx < n_grid; ++g_idx)
-      if (lane == 0 && warp_global < n_warps) {
+    // an all-dead warp stops early: its remaining timeline partials are identities
+    for (; next_grid_ctl < ctl_hi; next_grid_ctl += u.grid_ctl, ++g_idx)
+      if (lane == 0) {
         long long* dst = (long long*)a.timeline_warp + ((int64_t)g_idx * n_warps + warp_global) * 3;
         dst[0] = 0; dst[1] = LLONG_MAX; dst[2] = LLONG_MIN;
       }
-  }
-  if (!inrange || was_bad) return;  // a rerun keeps the diverged lanes' status
-  const int64_t last_day = a.n_days - 1;
-  {
-    double* dd = a.day_dose + (last_day * 3) * n + i;
-    dd[0] = day_basal; dd[n] = s_d[SC_DBOLUS][tid]; dd[2 * n] = s_d[SC_DGLUC][tid];
-  }
-  flush_hist();
-  a.status[i] = status;
-  a.ticks[i] = status == GT_STATUS_OK ? a.horizon_ticks : (death_tick < 0 ? 0 : death_tick);
-  a.bg_stats[i] = s_d[SC_BGMIN][tid];
-  a.bg_stats[n + i] = s_d[SC_BGMAX][tid];
-  a.bg_stats[2 * n + i] = bg_sum;
-  a.hypo_events[i] = ev39;
-  a.hypo_events[n + i] = ev30;
-  if (a.x_out) {
-    const double xs[NS] = {Q1, Q2, S1, S2, I, X1, X2, X3, D1, D2, G, Z1, Z2, E1, E2, E3};
-    for (int k = 0; k < NS; ++k) a.x_out[(int64_t)k * n + i] = xs[k];
+    flush_hist();  // empties this thread's shared histogram for its next unit
+
+    if (!last) {
+      // ---- save the lane state for the next slice
+      if (inrange) {
+        double* sd = sch.sd + i;
+        int* si = sch.si + i;
+#define STD(f, v) sd[(int64_t)(f) * n] = (v)
+#define STI(f, v) si[(int64_t)(f) * n] = (v)
+        STD(SD_Q1, Q1); STD(SD_Q2, Q2); STD(SD_S1, S1); STD(SD_S2, S2); STD(SD_I, I);
+        STD(SD_X1, X1); STD(SD_X2, X2); STD(SD_X3, X3); STD(SD_D1, D1); STD(SD_D2, D2);
+        STD(SD_G, G); STD(SD_Z1, Z1); STD(SD_Z2, Z2);
+        if (HAS_EX) { STD(SD_E1, E1); STD(SD_E2, E2); STD(SD_E3, E3); }
+        STD(SD_BGSUM, bg_sum); STD(SD_DAYBASAL, day_basal); STD(SD_HUINS, hu_ins);
+        STD(SD_HU2, hu2); STD(SD_GIN, gin);
+        for (int q = 0; q < N_SC; ++q) STD(SD_SC0 + q, s_d[q][tid]);
+        for (int q = 0; q < N_SI; ++q) STI(SV_SI0 + q, s_i[q][tid]);
+        if (PROTO == GT_PROTO_THREE_MEAL) {
+          for (int j = 0; j < 3; ++j) {
+            STD(SD_MC0 + j, s_mc[j][tid]);
+            for (int f = 0; f < 3; ++f) STI(SV_MK0 + 3 * f + j, s_mk[f][j][tid]);
+          }
+        }
+        STI(SV_MKS, m_ks); STI(SV_MKE, m_ke); STI(SV_ACTLO, act_lo); STI(SV_ACTHI, act_hi);
+        STI(SV_KBMIN, kb_min); STI(SV_KBMAX, kb_max); STI(SV_RUN39, run39); STI(SV_RUN30, run30);
+        STI(SV_EV39, ev39); STI(SV_EV30, ev30); STI(SV_ALIVE, alive ? 1 : 0);
+        STI(SV_STATUS, status); STI(SV_DEATH, death_tick);
+#undef STD
+#undef STI
+      }
+    } else if (inrange && !was_bad) {  // a rerun keeps the diverged lanes' outputs
+      // ---- final outputs
+      const int64_t last_day = a.n_days - 1;
+      double* dd = a.day_dose + (last_day * 3) * n + i;
+      dd[0] = day_basal; dd[n] = s_d[SC_DBOLUS][tid]; dd[2 * n] = s_d[SC_DGLUC][tid];
+      a.status[i] = status;
+      a.ticks[i] = status == GT_STATUS_OK ? a.horizon_ticks : (death_tick < 0 ? 0 : death_tick);
+      a.bg_stats[i] = s_d[SC_BGMIN][tid];
+      a.bg_stats[n + i] = s_d[SC_BGMAX][tid];
+      a.bg_stats[2 * n + i] = bg_sum;
+      a.hypo_events[i] = ev39;
+      a.hypo_events[n + i] = ev30;
+      if (a.x_out) {
+        const double xs[NS] = {Q1, Q2, S1, S2, I, X1, X2, X3, D1, D2, G, Z1, Z2, E1, E2, E3};
+        for (int k = 0; k < NS; ++k) a.x_out[(int64_t)k * n + i] = xs[k];
+      }
+    }
+    // ---- release this slice
+    __syncwarp();
+    __threadfence();
+    if (lane == 0) st_release(sch.done + warp_global, chunk + 1);
   }
 }
 
@@ -689,23 +798,67 @@ static Uni make_uni(const gt_fast_args& a) {
 
 }  // namespace gt
 
-template <int PROTO, int NOISE, int PS>
-static void launch_one(const gt_fast_args* a, const gt::Uni& u, unsigned grid, cudaStream_t st) {
-  constexpr int kDyn = gt::kHistWords * gt::kFastBS * 4;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gt::fast_kernel<PROTO, NOISE, PS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
-    attr = true;
+// Number of horizon slices: the smallest c in 1..8 minimising
+// ceil(c * warps / slots) / c (the makespan in units of one full horizon).
+static int choose_chunks(int64_t warps, int64_t slots, int n_ctl) {
+  int best = 1;
+  double best_t = 1e300;
+  for (int c = 1; c <= 8 && c <= n_ctl; ++c) {
+    const double rounds = (double)((c * warps + slots - 1) / slots);
+    const double t = rounds / c;
+    if (t < best_t - 1e-9) { best_t = t; best = c; }
   }
-  gt::fast_kernel<PROTO, NOISE, PS><<<grid, gt::kFastBS, kDyn, st>>>(*a, u);
+  return best;
 }
 
-// The period loop is NOT unrolled (PS = 0): measured on B200, the 5-step
-// unrolled body (~2x the SASS) spills and misses the instruction cache —
-// 94 ms vs 76 ms for 100k patients x 4 weeks.
 template <int PROTO, int NOISE>
-static void launch_ps(const gt_fast_args* a, const gt::Uni& u, unsigned grid, cudaStream_t st) {
-  launch_one<PROTO, NOISE, 0>(a, u, grid, st);
+static int launch_one(const gt_fast_args* a, const gt::Uni& u, cudaStream_t st) {
+  constexpr int kDyn = gt::kHistWords * gt::kFastBS * 4;
+  auto kern = gt::fast_kernel<PROTO, NOISE>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
+    attr = true;
+  }
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, gt::kFastBS, kDyn);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t warps = (a->n + 31) / 32;
+  const int64_t slots = (int64_t)sms * per_sm * (gt::kFastBS / 32);
+  const int n_ctl = u.n_ctl;
+  const int chunks = a->n_slices > 0 ? std::min(a->n_slices, n_ctl) : choose_chunks(warps, slots, n_ctl);
+  gt::Sched s{};
+  s.n_warps = (int)warps;
+  s.n_chunks = chunks;
+  s.chunk_ctl = (n_ctl + chunks - 1) / chunks;
+  s.n_chunks = (n_ctl + s.chunk_ctl - 1) / s.chunk_ctl;
+  s.n_units = (int)(warps * s.n_chunks);
+  // scratch: counter + done flags (+ saved lane state when slicing)
+  const size_t n_pad = (size_t)warps * 32;
+  const size_t bytes_i = sizeof(int) * (1 + (size_t)warps);
+  const size_t bytes_state = s.n_chunks > 1 ? (size_t)a->n * (gt::SD_N * sizeof(double) + gt::SV_N * sizeof(int)) : 0;
+  char* scratch = nullptr;
+  if (cudaMallocAsync(&scratch, bytes_i + bytes_state + 16, st) != cudaSuccess) {
+    gt_set_error("gt_simulate_fast: scratch allocation failed");
+    return GT_ECUDA;
+  }
+  (void)n_pad;
+  cudaMemsetAsync(scratch, 0, bytes_i, st);
+  s.counter = reinterpret_cast<int*>(scratch);
+  s.done = s.counter + 1;
+  if (bytes_state) {
+    char* base = scratch + ((bytes_i + 15) & ~size_t(15));
+    s.sd = reinterpret_cast<double*>(base);
+    s.si = reinterpret_cast<int*>(base + (size_t)a->n * gt::SD_N * sizeof(double));
+  }
+  const int64_t blocks_needed = (warps + 3) / 4;
+  const unsigned grid = (unsigned)std::min<int64_t>((int64_t)sms * per_sm, blocks_needed);
+  kern<<<grid, gt::kFastBS, kDyn, st>>>(*a, u, s);
+  const int e = gt_check_launch("fast_kernel");
+  cudaFreeAsync(scratch, st);
+  return e;
 }
 
 int gt_launch_fast(const gt_fast_args* a, cudaStream_t st) {
@@ -727,20 +880,20 @@ int gt_launch_fast(const gt_fast_args* a, cudaStream_t st) {
       return GT_EUNSUPPORTED;
     }
   }
+  if ((a->n + 31) / 32 > INT32_MAX / 8) {
+    gt_set_error("gt_simulate_fast: too many patients for one launch; shard the population");
+    return GT_EINVAL;
+  }
   const gt::Uni u = gt::make_uni(*a);
-  const unsigned grid = (unsigned)((a->n + gt::kFastBS - 1) / gt::kFastBS);
   const int pk = a->proto_kind, nk = a->noise_kind;
   if (pk == GT_PROTO_THREE_MEAL && nk == GT_NOISE_PHILOX)
-    launch_ps<GT_PROTO_THREE_MEAL, GT_NOISE_PHILOX>(a, u, grid, st);
-  else if (pk == GT_PROTO_THREE_MEAL && nk == GT_NOISE_INJECTED)
-    launch_ps<GT_PROTO_THREE_MEAL, GT_NOISE_INJECTED>(a, u, grid, st);
-  else if (pk == GT_PROTO_CSR && nk == GT_NOISE_PHILOX)
-    launch_ps<GT_PROTO_CSR, GT_NOISE_PHILOX>(a, u, grid, st);
-  else if (pk == GT_PROTO_CSR && nk == GT_NOISE_INJECTED)
-    launch_ps<GT_PROTO_CSR, GT_NOISE_INJECTED>(a, u, grid, st);
-  else {
-    gt_set_error("gt_simulate_fast: unsupported proto_kind=%d noise_kind=%d", pk, nk);
-    return GT_EUNSUPPORTED;
-  }
-  return gt_check_launch("fast_kernel");
+    return launch_one<GT_PROTO_THREE_MEAL, GT_NOISE_PHILOX>(a, u, st);
+  if (pk == GT_PROTO_THREE_MEAL && nk == GT_NOISE_INJECTED)
+    return launch_one<GT_PROTO_THREE_MEAL, GT_NOISE_INJECTED>(a, u, st);
+  if (pk == GT_PROTO_CSR && nk == GT_NOISE_PHILOX)
+    return launch_one<GT_PROTO_CSR, GT_NOISE_PHILOX>(a, u, st);
+  if (pk == GT_PROTO_CSR && nk == GT_NOISE_INJECTED)
+    return launch_one<GT_PROTO_CSR, GT_NOISE_INJECTED>(a, u, st);
+  gt_set_error("gt_simulate_fast: unsupported proto_kind=%d noise_kind=%d", pk, nk);
+  return GT_EUNSUPPORTED;
 }

@@ -195,7 +195,7 @@ def launch_fast(inputs: dict, outs: FastOutputs, sz: dict, dt_s: float, period_s
                 seed: int, noise_role: int, hypo_min_ticks: int, device,
                 meal_spec: dict | None = None, csr: dict | None = None,
                 injected: dict | None = None, controller_code: int = 0, fixed=None,
-                rerun_diverged: bool = False) -> None:
+                rerun_diverged: bool = False, n_slices: int = 0) -> None:
     """Enqueue the fused integrator on the current stream (no sync).
     ``fixed``: the launch-uniform values of the non-sampled parameters
     (p[30] order); defaults to row 0 of ``inputs['params']`` after checking
@@ -210,7 +210,7 @@ def launch_fast(inputs: dict, outs: FastOutputs, sz: dict, dt_s: float, period_s
     a.proto_kind = GT_PROTO_THREE_MEAL if csr is None else GT_PROTO_CSR
     a.noise_kind = GT_NOISE_PHILOX if injected is None else GT_NOISE_INJECTED
     a.controller = controller_code
-    a.record_timeline_per_patient = int(outs.timeline_pp is not None)
+    a.n_slices = int(n_slices)
     a.dt_s, a.period_s = float(dt_s), float(period_s)
     a.period_steps, a.horizon_ticks, a.grid_step_ticks = (sz["period_steps"], sz["horizon_ticks"],
                                                           sz["grid_step_ticks"])

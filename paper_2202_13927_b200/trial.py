@@ -51,7 +51,8 @@ def population_to_device(population, basal_scale: float, device):
 class FastTrial:
     def __init__(self, pid0, params, basal, generator, profile, config, controller_id="dual_hormone",
                  device=None, hypo_min_s: float = 900.0, per_patient_metrics: bool = False,
-                 seed: int | None = None):
+                 seed: int | None = None, n_slices: int = 0):
+        self.n_slices = int(n_slices)   # 0 = chosen by the launcher
         self.device = engine.require_device(device)
         t = engine.torch()
         self.config = config
@@ -121,7 +122,7 @@ class FastTrial:
                            self.config.controller_period_s, self.seed, rng.ROLE_DEVICE_NOISE,
                            self.hypo_min_ticks, self.device, meal_spec=self.meal_spec, csr=self.csr,
                            injected=injected, controller_code=self.code, fixed=self.fixed,
-                           rerun_diverged=rerun_diverged)
+                           rerun_diverged=rerun_diverged, n_slices=self.n_slices)
 
     def reduce(self):
         engine.launch_reduce(self.outs, self.red, self.sz, self.config.dt_s, self.device)

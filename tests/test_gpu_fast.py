@@ -273,3 +273,35 @@ def test_philox_trial_statistics_match_oracle(dev, oracle):
     assert abs(tir_ref.mean() - tir_dev.mean()) < 5 * se
     for q in (0.05, 0.25, 0.5, 0.75, 0.95):
         assert abs(np.quantile(tir_ref, q) - np.quantile(tir_dev, q)) < 0.05
+
+
+@pytest.mark.parametrize("slices", [2, 3, 7])
+def test_horizon_slicing_is_invisible(dev, slices):
+    """The persistent schedule may cut each patient's horizon into slices
+    (state saved/restored between them); results are bit-identical to the
+    unsliced run, including a diverged patient's exclusion."""
+    from paper_2202_13927_b200 import engine
+    from paper_2202_13927_b200.config import SimulationConfig
+    from paper_2202_13927_b200.controller import ControllerHyperparameters
+    from paper_2202_13927_b200.population import generate_population
+    from paper_2202_13927_b200.protocol import ThreeMealProtocol
+    from paper_2202_13927_b200.trial import FastTrial
+    cfg = SimulationConfig(horizon_s=9 * 86400.0, seed=12, dt_s=60.0)
+    pop = generate_population(8, 200, device=dev, on_exhausted="redraw_weight")
+    params = pop.params_device.clone()
+    params[37, 4] = -5.0   # one diverging patient
+    runs = []
+    for s in (1, slices):
+        ft = FastTrial(0, params, pop.basal_device, ThreeMealProtocol(), ControllerHyperparameters(), cfg,
+                       device=dev, n_slices=s, per_patient_metrics=True)
+        ft.outs = engine.alloc_fast_outputs(ft.n, 0, ft.sz, dev, per_patient_timeline=True, final_state=True)
+        ft.step()
+        runs.append(ft)
+    a, b = runs
+    for k in ("status", "ticks", "bg_hist", "bg_stats", "day_dose", "hypo_events", "timeline_pp",
+              "timeline_warp", "x_out"):
+        # the diverged patient's own (discarded) statistics are NaN in both runs
+        assert np.array_equal(_h(getattr(a.outs, k)), _h(getattr(b.outs, k)),
+                              equal_nan=getattr(a.outs, k).dtype.is_floating_point), k
+    assert _acc_equal(a.accumulator(), b.accumulator())
+    assert a.accumulator().aborted_ids == (37,)
