@@ -392,7 +392,8 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         for (int b = 0; b < 4; ++b) {
           const uint32_t c = (word >> (8 * b)) & 0xFFu;
           const int bin = 4 * w + b;
-          if (c && bin < GT_N_BG_BINS) a.bg_hist[(int64_t)bin * n + i] += (int32_t)c;
+          // fire-and-forget RED (no load-use wait); the column is this lane's own
+          if (c && bin < GT_N_BG_BINS) atomicAdd(&a.bg_hist[(int64_t)bin * n + i], (int32_t)c);
         }
       }
     };
