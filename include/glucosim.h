@@ -186,6 +186,13 @@ typedef struct gt_fast_args {
     double *timeline_pp;    /* [n_grid][n] or NULL */
     int64_t *timeline_warp; /* [n_grid][n_warps][3] per-warp sum/min/max (2^24 fixed point) */
     double *x_out;          /* [16][n] or NULL */
+    /* Brownian aggregation (BASELINE configs[4]): with noise_agg = m > 1 each
+     * step's Wiener normals are sum_{j<m} Z(m*k + j) / sqrt(m) of the fine
+     * Philox stream, so a run at dt sees the same Brownian path as a run at
+     * dt/m with noise_agg = 1 (the CGM normal is the fine tick's, as well).
+     * precision: 0 = FP64 integrator, 1 = FP32 integrator (controller and
+     * statistics stay FP64). */
+    int32_t noise_agg, precision;
 } gt_fast_args;
 int gt_simulate_fast(const gt_fast_args *a, void *stream);
 int64_t gt_fast_num_warps(int64_t n);

@@ -49,8 +49,8 @@ struct Uni {
   double h, ginK, aS, hS, aZ1, hTg, aZ2, cG;
   double aE1, bE1, aE2, bE2, aE3, bE3, qex, sex;
   double sqG, sigEh, sqrtR, rK1, pred_k, u_basal_k, u_bolus_k, u_gluc_k;
-  double dt, period, horizon_s, meal_dur_min;
-  int32_t ps, n_ctl, ctl_per_day, grid_ctl, hypoL, pad;
+  double dt, period, horizon_s, meal_dur_min, rs_agg;
+  int32_t ps, n_ctl, ctl_per_day, grid_ctl, hypoL, agg;
   uint32_t rk[20];  // Philox round keys (k0 + r*W0, k1 + r*W1): constant-bank operands
 };
 
@@ -63,27 +63,44 @@ struct Sched {
   int n_units, n_warps, chunk_ctl, n_chunks;
 };
 
-// Per-patient constants (registers).
+// Per-patient constants (registers), in the integrator's precision R.
+template <typename R>
 struct PC {
-  double invVGw, aG, hTG, aI, hTI, cI, dI, ax1, bx1, ax2, bx2, ax3, bx3;
-  double hF01w, hk12, aK12, hE, rK0, sqE;
+  R invVGw, aG, hTG, aI, hTI, cI, dI, ax1, bx1, ax2, bx2, ax3, bx3;
+  R hF01w, hk12, aK12, hE, rK0, sqE;
 };
 
-__device__ __forceinline__ void make_pc(const double* __restrict__ p, const Uni& u, PC& c) {
+template <typename R>
+__device__ __forceinline__ void make_pc(const double* __restrict__ p, const Uni& u, PC<R>& c) {
   const double h = u.h, w = p[PW];
-  c.invVGw = 1.0 / (p[PVG] * w);
-  c.hTG = h / p[PTMAXG]; c.aG = 1.0 - c.hTG;
-  c.hTI = h / p[PTMAXI]; c.aI = 1.0 - c.hTI;
-  c.cI = 1.0 - h * p[PKE]; c.dI = c.hTI / (p[PVI] * w);
-  c.ax1 = 1.0 - h * p[PKA1]; c.bx1 = h * p[PKA1] * p[PSIT];
-  c.ax2 = 1.0 - h * p[PKA2]; c.bx2 = h * p[PKA2] * p[PSID];
-  c.ax3 = 1.0 - h * p[PKA3]; c.bx3 = h * p[PKA3] * p[PSIE];
-  c.hF01w = h * p[PF01] * w;
-  c.hk12 = h * p[PK12]; c.aK12 = 1.0 - c.hk12;
-  c.hE = h * p[PEGP0] * w;
-  c.rK0 = h * 0.003 * 9.0 * p[PVG] * w;
-  c.sqE = u.sigEh * w;
+  // folded in FP64, then rounded once to R
+  const double hTG = h / p[PTMAXG], hTI = h / p[PTMAXI], hk12 = h * p[PK12];
+  c.invVGw = (R)(1.0 / (p[PVG] * w));
+  c.hTG = (R)hTG; c.aG = (R)(1.0 - hTG);
+  c.hTI = (R)hTI; c.aI = (R)(1.0 - hTI);
+  c.cI = (R)(1.0 - h * p[PKE]); c.dI = (R)(hTI / (p[PVI] * w));
+  c.ax1 = (R)(1.0 - h * p[PKA1]); c.bx1 = (R)(h * p[PKA1] * p[PSIT]);
+  c.ax2 = (R)(1.0 - h * p[PKA2]); c.bx2 = (R)(h * p[PKA2] * p[PSID]);
+  c.ax3 = (R)(1.0 - h * p[PKA3]); c.bx3 = (R)(h * p[PKA3] * p[PSIE]);
+  c.hF01w = (R)(h * p[PF01] * w);
+  c.hk12 = (R)hk12; c.aK12 = (R)(1.0 - hk12);
+  c.hE = (R)(h * p[PEGP0] * w);
+  c.rK0 = (R)(h * 0.003 * 9.0 * p[PVG] * w);
+  c.sqE = (R)(u.sigEh * w);
 }
+
+// explicit-rounding multiply / fma in the integrator precision (no mixed
+// overloads: a double constant reaching the FP32 integrator fails to compile)
+__device__ __forceinline__ double MR_(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float MR_(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double FMR(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float FMR(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+// |x| bit pattern compared against the exponent-all-ones pattern (Inf/NaN)
+__device__ __forceinline__ unsigned absbits(double x) { return (unsigned)__double2hiint(x) & 0x7fffffffu; }
+__device__ __forceinline__ unsigned absbits(float x) { return __float_as_uint(x) & 0x7fffffffu; }
+template <typename R> struct kNonfiniteBits;
+template <> struct kNonfiniteBits<double> { static constexpr unsigned v = 0x7ff00000u; };
+template <> struct kNonfiniteBits<float> { static constexpr unsigned v = 0x7f800000u; };
 
 // ------------------------------------------------------------ noise
 __device__ __forceinline__ void mulwide(uint32_t a, uint32_t b, uint32_t& lo, uint32_t& hi) {
@@ -191,7 +208,7 @@ enum { SD_Q1, SD_Q2, SD_S1, SD_S2, SD_I, SD_X1, SD_X2, SD_X3, SD_D1, SD_D2, SD_G
 enum { SV_MKS, SV_MKE, SV_ACTLO, SV_ACTHI, SV_KBMIN, SV_KBMAX, SV_RUN39, SV_RUN30, SV_EV39,
        SV_EV30, SV_ALIVE, SV_STATUS, SV_DEATH, SV_MK0, SV_SI0 = SV_MK0 + 9, SV_N = SV_SI0 + N_SI };
 
-template <int PROTO, int NOISE>
+template <int PROTO, int NOISE, typename R, bool AGG>
 __global__ void __launch_bounds__(kFastBS, GT_FAST_MINB)
 fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
   constexpr bool HAS_EX = (PROTO == GT_PROTO_CSR);
@@ -263,15 +280,15 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
     }
 
     // ---- per-patient constants (recomputed per slice: cheap, register-free)
-    PC pc;
+    PC<R> pc;
     {
       double p[NP];
 #pragma unroll
       for (int k = 0; k < NP; ++k) p[k] = a.params[ii * NP + k];
       make_pc(p, u, pc);
     }
-    double sqE = pc.sqE, sqG = u.sqG;
-    if (NOISE == GT_NOISE_INJECTED && a.has_noise[ii] == 0) { sqE = 0.0; sqG = 0.0; }
+    R sqE = pc.sqE, sqG = (R)u.sqG;
+    if (NOISE == GT_NOISE_INJECTED && a.has_noise[ii] == 0) { sqE = 0; sqG = 0; }
     int64_t moff = 0, n_meals_csr = 0, ex_lo = 0, n_ex = 0;
     if (PROTO == GT_PROTO_CSR) {
       moff = a.meal_off[ii]; n_meals_csr = a.meal_off[ii + 1] - moff;
@@ -290,8 +307,9 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
     };
 
     // ---- lane state: initialise (first slice) or restore
-    double Q1, Q2, S1, S2, I, X1, X2, X3, D1, D2, G, Z1, Z2, E1 = 0.0, E2 = 0.0, E3 = 0.0;
-    double bg_sum, day_basal, hu_ins, hu2, gin;
+    R Q1, Q2, S1, S2, I, X1, X2, X3, D1, D2, G, Z1, Z2, E1 = 0, E2 = 0, E3 = 0;
+    R hu_ins, hu2, gin;  // per-step inputs, in the integrator precision
+    double bg_sum, day_basal;
     int32_t m_ks, m_ke, act_lo, act_hi;
     int kb_min, kb_max, run39, run30, ev39, ev30;
     bool alive;
@@ -301,10 +319,10 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       status = (inrange && !alive) ? GT_STATUS_EXCLUDED : GT_STATUS_OK;
       death_tick = -1;
       const double* x0 = a.x0 + ii * NS;
-      Q1 = x0[IQ1]; Q2 = x0[IQ2]; S1 = x0[IS1]; S2 = x0[IS2]; I = x0[II];
-      X1 = x0[IX1]; X2 = x0[IX2]; X3 = x0[IX3]; D1 = x0[ID1]; D2 = x0[ID2];
-      G = x0[IGSC]; Z1 = x0[IZ1]; Z2 = x0[IZ2];
-      if (HAS_EX) { E1 = x0[IE1]; E2 = x0[IE2]; E3 = x0[IE3]; }
+      Q1 = (R)x0[IQ1]; Q2 = (R)x0[IQ2]; S1 = (R)x0[IS1]; S2 = (R)x0[IS2]; I = (R)x0[II];
+      X1 = (R)x0[IX1]; X2 = (R)x0[IX2]; X3 = (R)x0[IX3]; D1 = (R)x0[ID1]; D2 = (R)x0[ID2];
+      G = (R)x0[IGSC]; Z1 = (R)x0[IZ1]; Z2 = (R)x0[IZ2];
+      if (HAS_EX) { E1 = (R)x0[IE1]; E2 = (R)x0[IE2]; E3 = (R)x0[IE3]; }
       const double* c0 = a.c0 + ii * NC;
       s_d[SC_FILT][tid] = c0[CFILT]; s_d[SC_ICR][tid] = c0[CICR];
       s_d[SC_SUSP][tid] = c0[CSUSPEND_UNTIL]; s_d[SC_LASTG][tid] = c0[CLASTGLUC];
@@ -315,12 +333,12 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       s_d[SC_BGMAX][tid] = -INFINITY;
       s_d[SC_DBOLUS][tid] = 0.0;
       s_d[SC_DGLUC][tid] = 0.0;
-      bg_sum = 0.0; day_basal = 0.0; hu_ins = 0.0; hu2 = 0.0;
+      bg_sum = 0.0; day_basal = 0.0; hu_ins = 0; hu2 = 0;
       kb_min = INT_MAX; kb_max = -1; run39 = run30 = ev39 = ev30 = 0;
-      m_ks = m_ke = INT_MAX; gin = 0.0; act_lo = act_hi = INT_MAX;
+      m_ks = m_ke = INT_MAX; gin = 0; act_lo = act_hi = INT_MAX;
       if (PROTO == GT_PROTO_CSR) {
         const MealT m0 = meal_at(0);
-        m_ks = m0.ks; m_ke = m0.ke; gin = u.ginK * m0.rate;
+        m_ks = m0.ks; m_ke = m0.ke; gin = (R)(u.ginK * m0.rate);
         s_i[SI_MEALM][tid] = 0;
         s_i[SI_ANNM][tid] = 0;
         s_i[SI_ANNKP][tid] = m0.kp;
@@ -334,12 +352,12 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       const int* si = sch.si + ii;
 #define LDD(f) sd[(int64_t)(f) * n]
 #define LDI(f) si[(int64_t)(f) * n]
-      Q1 = LDD(SD_Q1); Q2 = LDD(SD_Q2); S1 = LDD(SD_S1); S2 = LDD(SD_S2); I = LDD(SD_I);
-      X1 = LDD(SD_X1); X2 = LDD(SD_X2); X3 = LDD(SD_X3); D1 = LDD(SD_D1); D2 = LDD(SD_D2);
-      G = LDD(SD_G); Z1 = LDD(SD_Z1); Z2 = LDD(SD_Z2);
-      if (HAS_EX) { E1 = LDD(SD_E1); E2 = LDD(SD_E2); E3 = LDD(SD_E3); }
-      bg_sum = LDD(SD_BGSUM); day_basal = LDD(SD_DAYBASAL); hu_ins = LDD(SD_HUINS); hu2 = LDD(SD_HU2);
-      gin = LDD(SD_GIN);
+      Q1 = (R)LDD(SD_Q1); Q2 = (R)LDD(SD_Q2); S1 = (R)LDD(SD_S1); S2 = (R)LDD(SD_S2); I = (R)LDD(SD_I);
+      X1 = (R)LDD(SD_X1); X2 = (R)LDD(SD_X2); X3 = (R)LDD(SD_X3); D1 = (R)LDD(SD_D1); D2 = (R)LDD(SD_D2);
+      G = (R)LDD(SD_G); Z1 = (R)LDD(SD_Z1); Z2 = (R)LDD(SD_Z2);
+      if (HAS_EX) { E1 = (R)LDD(SD_E1); E2 = (R)LDD(SD_E2); E3 = (R)LDD(SD_E3); }
+      bg_sum = LDD(SD_BGSUM); day_basal = LDD(SD_DAYBASAL);
+      hu_ins = (R)LDD(SD_HUINS); hu2 = (R)LDD(SD_HU2); gin = (R)LDD(SD_GIN);
       for (int q = 0; q < N_SC; ++q) s_d[q][tid] = LDD(SD_SC0 + q);
       for (int q = 0; q < N_SI; ++q) s_i[q][tid] = LDI(SV_SI0 + q);
       if (PROTO == GT_PROTO_THREE_MEAL) {
@@ -364,9 +382,9 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
     int32_t day_k0 = day_ctl0 * ps;
     auto load_slot = [&](int j) {
       const int ks = s_mk[0][j][tid];
-      if (ks == 0xFFFF) { m_ks = m_ke = INT_MAX; gin = 0.0; return; }
+      if (ks == 0xFFFF) { m_ks = m_ke = INT_MAX; gin = 0; return; }
       m_ks = day_k0 + ks; m_ke = day_k0 + s_mk[1][j][tid];
-      gin = u.ginK * (s_mc[j][tid] / u.meal_dur_min);  // rate = g / duration (simulation.py:162)
+      gin = (R)(u.ginK * (s_mc[j][tid] / u.meal_dur_min));  // rate = g / duration (simulation.py:162)
     };
     auto gen_day = [&](int32_t d) {
       for (int j = 0; j < 3; ++j) {
@@ -409,17 +427,36 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
     // ---------------------------------------------------------- one step
     auto step = [&](const int32_t k, const bool tick, const int32_t ctl, const int32_t k_base) {
       // noise for tick k (counter = (k, pid, role, 0))
-      double z0, z1, z2, zm = 0.0;
+      R z0, z1, z2;
+      double zm = 0.0;
       if (NOISE == GT_NOISE_PHILOX) {
-        const U4 r = philox_fast((uint32_t)k, pid, a.noise_role, 0u, u.rk);
-        float f0, f1, f2, f3;
-        box_muller(r.x, r.y, f0, f1);
-        box_muller(r.z, r.w, f2, f3);
-        z0 = f0; z1 = f1; z2 = f2;
-        if (tick) zm = f3;
+        if (!AGG) {
+          const U4 r = philox_fast((uint32_t)k, pid, a.noise_role, 0u, u.rk);
+          float f0, f1, f2, f3;
+          box_muller(r.x, r.y, f0, f1);
+          box_muller(r.z, r.w, f2, f3);
+          z0 = f0; z1 = f1; z2 = f2;
+          if (tick) zm = f3;
+        } else {
+          // Brownian aggregation: this step's increment is the sum of the agg
+          // fine increments at counters k*agg + j (the path a run at dt/agg
+          // draws), rescaled to unit variance; the reading uses fine tick k*agg
+          R s0 = 0, s1 = 0, s2 = 0;
+          const uint32_t kf = (uint32_t)k * (uint32_t)u.agg;
+          for (int j = 0; j < u.agg; ++j) {
+            const U4 r = philox_fast(kf + (uint32_t)j, pid, a.noise_role, 0u, u.rk);
+            float f0, f1, f2, f3;
+            box_muller(r.x, r.y, f0, f1);
+            box_muller(r.z, r.w, f2, f3);
+            s0 += (R)f0; s1 += (R)f1; s2 += (R)f2;
+            if (j == 0 && tick) zm = f3;
+          }
+          const R sc = (R)u.rs_agg;
+          z0 = s0 * sc; z1 = s1 * sc; z2 = s2 * sc;
+        }
       } else {
         const double* wv = a.wiener + (ii * (int64_t)a.horizon_ticks + k) * 3;
-        z0 = wv[0]; z1 = wv[1]; z2 = wv[2];
+        z0 = (R)wv[0]; z1 = (R)wv[1]; z2 = (R)wv[2];
         if (tick) zm = a.meas[ii * (int64_t)u.n_ctl + ctl];
       }
       // disturbances at tick k (_kernel.py:85-94)
@@ -428,7 +465,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           const int32_t m = s_i[SI_MEALM][tid] + 1;
           s_i[SI_MEALM][tid] = m;
           const MealT mt = meal_at(m);
-          m_ks = mt.ks; m_ke = mt.ke; gin = u.ginK * mt.rate;
+          m_ks = mt.ks; m_ke = mt.ke; gin = (R)(u.ginK * mt.rate);
         }
       } else if (tick) {
         // generated meals are >= one period apart, so the active window of
@@ -436,13 +473,13 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         while (m_ke <= k) {
           const int j = ++s_i[SI_MEALM][tid];
           if (j < 3) load_slot(j);
-          else { m_ks = m_ke = INT_MAX; gin = 0.0; }
+          else { m_ks = m_ke = INT_MAX; gin = 0; }
         }
         act_lo = m_ks - k; act_hi = m_ke - k;
       }
       const int32_t sk = k - k_base;
-      const double gin_k = PROTO == GT_PROTO_CSR ? ((k >= m_ks) ? gin : 0.0)
-                                                 : ((sk >= act_lo && sk < act_hi) ? gin : 0.0);
+      const R gin_k = PROTO == GT_PROTO_CSR ? ((k >= m_ks) ? gin : (R)0)
+                                            : ((sk >= act_lo && sk < act_hi) ? gin : (R)0);
       bool ex_active = false;
       int ex_ptr = 0;
       if (HAS_EX) {
@@ -456,15 +493,11 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       if (tick) {
         const double t_s = (double)k * u.dt;
         if (alive) {
-          const unsigned m = max(max(max(__double2hiint(Q1) & 0x7fffffff, __double2hiint(Q2) & 0x7fffffff),
-                                     max(__double2hiint(S1) & 0x7fffffff, __double2hiint(S2) & 0x7fffffff)),
-                                 max(max(__double2hiint(I) & 0x7fffffff, __double2hiint(X1) & 0x7fffffff),
-                                     max(__double2hiint(X2) & 0x7fffffff, __double2hiint(X3) & 0x7fffffff)));
-          const unsigned m2 = max(max(max(__double2hiint(D1) & 0x7fffffff, __double2hiint(D2) & 0x7fffffff),
-                                      max(__double2hiint(G) & 0x7fffffff, __double2hiint(Z1) & 0x7fffffff)),
-                                  max(max(__double2hiint(Z2) & 0x7fffffff, __double2hiint(E1) & 0x7fffffff),
-                                      max(__double2hiint(E2) & 0x7fffffff, __double2hiint(E3) & 0x7fffffff)));
-          if (max(m, m2) >= 0x7ff00000u) { alive = false; status = GT_STATUS_NONFINITE; death_tick = k; }
+          const unsigned m = max(max(max(absbits(Q1), absbits(Q2)), max(absbits(S1), absbits(S2))),
+                                 max(max(absbits(I), absbits(X1)), max(absbits(X2), absbits(X3))));
+          const unsigned m2 = max(max(max(absbits(D1), absbits(D2)), max(absbits(G), absbits(Z1))),
+                                  max(max(absbits(Z2), absbits(E1)), max(absbits(E2), absbits(E3))));
+          if (max(m, m2) >= kNonfiniteBits<R>::v) { alive = false; status = GT_STATUS_NONFINITE; death_tick = k; }
         }
         // announced carbs starting within [t, t+P)
         double announced = 0.0;
@@ -491,7 +524,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         double phase = -1.0;
         if (HAS_EX && ex_active && a.ex_announced[ex_lo + ex_ptr] != 0.0)
           phase = t_s - a.ex_start_s[ex_lo + ex_ptr];
-        const double y = A_(G, M_(u.sqrtR, zm));
+        const double y = A_((double)G, M_(u.sqrtR, zm));
         // ---- controller_step_vec (controller.py:343-458); state in shared
         // memory.  Explicit IEEE operations in the reference's order: the
         // controller is bit-identical to the reference's for identical readings.
@@ -573,15 +606,15 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         }
         s_i[SI_FLAGS][tid] = flags;
         day_basal = fma(b_basal, (double)ps, day_basal);  // basal held for the whole period
-        hu_ins = fma(b_bolus, u.u_bolus_k, b_basal * u.u_basal_k);   // h * (u[0] + u[1])
-        hu2 = b_gluc * u.u_gluc_k;                                 // h * u[2]
+        hu_ins = (R)fma(b_bolus, u.u_bolus_k, b_basal * u.u_basal_k);   // h * (u[0] + u[1])
+        hu2 = (R)(b_gluc * u.u_gluc_k);                                 // h * u[2]
         if (b_bolus > 0.0 || b_gluc > 0.0) {
           s_d[SC_DBOLUS][tid] += b_bolus;
           s_d[SC_DGLUC][tid] += b_gluc;
         }
       }
       // statistics at tick k (_kernel.py:137-160)
-      double bg = M_(Q1, pc.invVGw);  // explicit: never fused into the sums below
+      double bg = (double)MR_(Q1, pc.invVGw);  // explicit: never fused into the sums below
       if (tick && ctl == 0) {
         // the steady state puts BG(0) on a histogram edge (6.0 = THRESHOLDS[55],
         // SURVEY.md §7): use the reference's exact division for that tick
@@ -633,46 +666,48 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         ++g_idx;
       }
       // Euler–Maruyama step, re-associated (hovorka.py:76-150)
-      const double ab = HAS_EX ? fma(u.sex, E3, 1.0) : 1.0;
-      const double ub = HAS_EX ? fma(u.qex, E2, 1.0) : 1.0;
-      const double x1e = X1 * ab, x2e = X2 * ab;
-      const double t1 = x1e * Q1;
-      const double bg45 = bg * (1.0 / 4.5);
-      const double hf01 = M_(pc.hF01w, bg45 < 1.0 ? bg45 : 1.0);  // explicit: fixed rounding
-      const double ren = fma(Q1, u.rK1, -pc.rK0);
-      const double hren = ren > 0.0 ? ren : 0.0;
-      const double egp = fma(-pc.hE, X3, pc.hE);
-      const double hegp = fma(u.cG, Z2, egp > 0.0 ? egp : 0.0);
-      double dq = fma(pc.hk12, Q2, D2 * pc.hTG);
-      dq = fma(-hf01, ub, dq);
-      dq = fma(-u.h, t1, dq);
+      // (in R: launch-uniform constants are rounded to R at their use)
+      const R bgR = (R)bg, zero = 0, one = 1;
+      const R ab = HAS_EX ? FMR((R)u.sex, E3, one) : one;
+      const R ub = HAS_EX ? FMR((R)u.qex, E2, one) : one;
+      const R x1e = X1 * ab, x2e = X2 * ab;
+      const R t1 = x1e * Q1;
+      const R bg45 = bgR * (R)(1.0 / 4.5);
+      const R hf01 = MR_(pc.hF01w, bg45 < one ? bg45 : one);  // explicit: fixed rounding
+      const R ren = FMR(Q1, (R)u.rK1, -pc.rK0);
+      const R hren = ren > zero ? ren : zero;
+      const R egp = FMR(-pc.hE, X3, pc.hE);
+      const R hegp = FMR((R)u.cG, Z2, egp > zero ? egp : zero);
+      R dq = FMR(pc.hk12, Q2, D2 * pc.hTG);
+      dq = FMR(-hf01, ub, dq);
+      dq = FMR(-(R)u.h, t1, dq);
       dq = (dq - hren) + hegp;
       // projection max(x, 0) (_kernel.py:175-177): keeps NaN like `if x < 0: x = 0`
-      const double q1n = fma(sqE, z0, Q1 + dq);
-      const double q2n = fma(Q2, pc.aK12, u.h * fma(-x2e, Q2, t1));
-      const double nQ1 = q1n < 0.0 ? 0.0 : q1n;
-      const double nQ2 = q2n < 0.0 ? 0.0 : q2n;
-      double nD1 = fma(D1, fma(sqG, z1, pc.aG), gin_k);
-      double nD2 = fma(D2, fma(sqG, z2, pc.aG), D1 * pc.hTG);
-      if (CLAMP_GUT) { nD1 = nD1 < 0.0 ? 0.0 : nD1; nD2 = nD2 < 0.0 ? 0.0 : nD2; }
-      const double nS2 = fma(S2, pc.aI, S1 * pc.hTI);
-      S1 = fma(S1, pc.aI, hu_ins);
-      const double nI = fma(I, pc.cI, S2 * pc.dI);
+      const R q1n = FMR(sqE, z0, Q1 + dq);
+      const R q2n = FMR(Q2, pc.aK12, (R)u.h * FMR(-x2e, Q2, t1));
+      const R nQ1 = q1n < zero ? zero : q1n;
+      const R nQ2 = q2n < zero ? zero : q2n;
+      R nD1 = FMR(D1, FMR(sqG, z1, pc.aG), gin_k);
+      R nD2 = FMR(D2, FMR(sqG, z2, pc.aG), D1 * pc.hTG);
+      if (CLAMP_GUT) { nD1 = nD1 < zero ? zero : nD1; nD2 = nD2 < zero ? zero : nD2; }
+      const R nS2 = FMR(S2, pc.aI, S1 * pc.hTI);
+      S1 = FMR(S1, pc.aI, hu_ins);
+      const R nI = FMR(I, pc.cI, S2 * pc.dI);
       S2 = nS2;
-      X1 = fma(X1, pc.ax1, I * pc.bx1);
-      X2 = fma(X2, pc.ax2, I * pc.bx2);
-      X3 = fma(X3, pc.ax3, I * pc.bx3);
+      X1 = FMR(X1, pc.ax1, I * pc.bx1);
+      X2 = FMR(X2, pc.ax2, I * pc.bx2);
+      X3 = FMR(X3, pc.ax3, I * pc.bx3);
       I = nI;
-      const double nZ2 = fma(Z2, u.aZ2, Z1 * u.hTg);
-      Z1 = fma(Z1, u.aZ1, hu2);
+      const R nZ2 = FMR(Z2, (R)u.aZ2, Z1 * (R)u.hTg);
+      Z1 = FMR(Z1, (R)u.aZ1, hu2);
       Z2 = nZ2;
       if (HAS_EX) {
-        const double nE2 = fma(E2, u.aE2, E1 * u.bE2);
-        const double nE3 = fma(E3, u.aE3, E1 * u.bE3);
-        E1 = fma(E1, u.aE1, u.bE1 * hrr);
+        const R nE2 = FMR(E2, (R)u.aE2, E1 * (R)u.bE2);
+        const R nE3 = FMR(E3, (R)u.aE3, E1 * (R)u.bE3);
+        E1 = FMR(E1, (R)u.aE1, (R)(u.bE1 * hrr));
         E2 = nE2; E3 = nE3;
       }
-      G = fma(G, u.aS, bg * u.hS);
+      G = FMR(G, (R)u.aS, bgR * (R)u.hS);
       Q1 = nQ1; Q2 = nQ2; D1 = nD1; D2 = nD2;
     };
 
@@ -749,7 +784,9 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       a.hypo_events[i] = ev39;
       a.hypo_events[n + i] = ev30;
       if (a.x_out) {
-        const double xs[NS] = {Q1, Q2, S1, S2, I, X1, X2, X3, D1, D2, G, Z1, Z2, E1, E2, E3};
+        const double xs[NS] = {(double)Q1, (double)Q2, (double)S1, (double)S2, (double)I, (double)X1,
+                               (double)X2, (double)X3, (double)D1, (double)D2, (double)G, (double)Z1,
+                               (double)Z2, (double)E1, (double)E2, (double)E3};
         for (int k = 0; k < NS; ++k) a.x_out[(int64_t)k * n + i] = xs[k];
       }
     }
@@ -789,6 +826,8 @@ static Uni make_uni(const gt_fast_args& a) {
   u.ctl_per_day = (int32_t)std::llround(86400.0 / a.period_s);
   u.grid_ctl = (int32_t)(a.grid_step_ticks / a.period_steps);
   u.hypoL = (int32_t)a.hypo_min_ticks;
+  u.agg = a.noise_agg < 1 ? 1 : a.noise_agg;
+  u.rs_agg = 1.0 / std::sqrt((double)u.agg);
   uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
   for (int r = 0; r < 10; ++r) {
     u.rk[2 * r] = k0; u.rk[2 * r + 1] = k1;
@@ -812,10 +851,10 @@ static int choose_chunks(int64_t warps, int64_t slots, int n_ctl) {
   return best;
 }
 
-template <int PROTO, int NOISE>
+template <int PROTO, int NOISE, typename R = double, bool AGG = false>
 static int launch_one(const gt_fast_args* a, const gt::Uni& u, cudaStream_t st) {
   constexpr int kDyn = gt::kHistWords * gt::kFastBS * 4;
-  auto kern = gt::fast_kernel<PROTO, NOISE>;
+  auto kern = gt::fast_kernel<PROTO, NOISE, R, AGG>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
@@ -885,14 +924,34 @@ int gt_launch_fast(const gt_fast_args* a, cudaStream_t st) {
     gt_set_error("gt_simulate_fast: too many patients for one launch; shard the population");
     return GT_EINVAL;
   }
+  if (a->noise_agg < 1 || (a->noise_agg > 1 && a->noise_kind != GT_NOISE_PHILOX) ||
+      (int64_t)a->noise_agg * a->horizon_ticks > (int64_t)UINT32_MAX) {
+    gt_set_error("gt_simulate_fast: noise_agg must be >= 1, > 1 only with Philox noise, and "
+                 "noise_agg * horizon_ticks must fit the 32-bit tick counter");
+    return GT_EINVAL;
+  }
   const gt::Uni u = gt::make_uni(*a);
   const int pk = a->proto_kind, nk = a->noise_kind;
+  if (a->precision == 1) {  // FP32 integrator: the generated-meal / Philox path only
+    if (pk == GT_PROTO_THREE_MEAL && nk == GT_NOISE_PHILOX)
+      return u.agg > 1 ? launch_one<GT_PROTO_THREE_MEAL, GT_NOISE_PHILOX, float, true>(a, u, st)
+                       : launch_one<GT_PROTO_THREE_MEAL, GT_NOISE_PHILOX, float, false>(a, u, st);
+    gt_set_error("gt_simulate_fast: the FP32 integrator supports the 3-meal generator with "
+                 "Philox noise only");
+    return GT_EUNSUPPORTED;
+  }
+  if (a->precision != 0) {
+    gt_set_error("gt_simulate_fast: precision must be 0 (FP64) or 1 (FP32)");
+    return GT_EINVAL;
+  }
   if (pk == GT_PROTO_THREE_MEAL && nk == GT_NOISE_PHILOX)
-    return launch_one<GT_PROTO_THREE_MEAL, GT_NOISE_PHILOX>(a, u, st);
+    return u.agg > 1 ? launch_one<GT_PROTO_THREE_MEAL, GT_NOISE_PHILOX, double, true>(a, u, st)
+                     : launch_one<GT_PROTO_THREE_MEAL, GT_NOISE_PHILOX>(a, u, st);
   if (pk == GT_PROTO_THREE_MEAL && nk == GT_NOISE_INJECTED)
     return launch_one<GT_PROTO_THREE_MEAL, GT_NOISE_INJECTED>(a, u, st);
   if (pk == GT_PROTO_CSR && nk == GT_NOISE_PHILOX)
-    return launch_one<GT_PROTO_CSR, GT_NOISE_PHILOX>(a, u, st);
+    return u.agg > 1 ? launch_one<GT_PROTO_CSR, GT_NOISE_PHILOX, double, true>(a, u, st)
+                     : launch_one<GT_PROTO_CSR, GT_NOISE_PHILOX>(a, u, st);
   if (pk == GT_PROTO_CSR && nk == GT_NOISE_INJECTED)
     return launch_one<GT_PROTO_CSR, GT_NOISE_INJECTED>(a, u, st);
   gt_set_error("gt_simulate_fast: unsupported proto_kind=%d noise_kind=%d", pk, nk);

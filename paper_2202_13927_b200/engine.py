@@ -195,7 +195,8 @@ def launch_fast(inputs: dict, outs: FastOutputs, sz: dict, dt_s: float, period_s
                 seed: int, noise_role: int, hypo_min_ticks: int, device,
                 meal_spec: dict | None = None, csr: dict | None = None,
                 injected: dict | None = None, controller_code: int = 0, fixed=None,
-                rerun_diverged: bool = False, n_slices: int = 0) -> None:
+                rerun_diverged: bool = False, n_slices: int = 0, noise_agg: int = 1,
+                fp32: bool = False) -> None:
     """Enqueue the fused integrator on the current stream (no sync).
     ``fixed``: the launch-uniform values of the non-sampled parameters
     (p[30] order); defaults to row 0 of ``inputs['params']`` after checking
@@ -211,6 +212,8 @@ def launch_fast(inputs: dict, outs: FastOutputs, sz: dict, dt_s: float, period_s
     a.noise_kind = GT_NOISE_PHILOX if injected is None else GT_NOISE_INJECTED
     a.controller = controller_code
     a.n_slices = int(n_slices)
+    a.noise_agg = int(noise_agg)
+    a.precision = 1 if fp32 else 0
     a.dt_s, a.period_s = float(dt_s), float(period_s)
     a.period_steps, a.horizon_ticks, a.grid_step_ticks = (sz["period_steps"], sz["horizon_ticks"],
                                                           sz["grid_step_ticks"])

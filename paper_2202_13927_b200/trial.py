@@ -51,8 +51,13 @@ def population_to_device(population, basal_scale: float, device):
 class FastTrial:
     def __init__(self, pid0, params, basal, generator, profile, config, controller_id="dual_hormone",
                  device=None, hypo_min_s: float = 900.0, per_patient_metrics: bool = False,
-                 seed: int | None = None, n_slices: int = 0):
+                 seed: int | None = None, n_slices: int = 0, noise_agg: int = 1,
+                 fp32: bool = False):
         self.n_slices = int(n_slices)   # 0 = chosen by the launcher
+        # BASELINE configs[4]: each step's Brownian increment aggregated from
+        # noise_agg fine Philox increments (the path a dt/noise_agg run draws),
+        # and the FP32 integrator (controller and statistics stay FP64)
+        self.noise_agg, self.fp32 = int(noise_agg), bool(fp32)
         self.device = engine.require_device(device)
         t = engine.torch()
         self.config = config
@@ -122,7 +127,8 @@ class FastTrial:
                            self.config.controller_period_s, self.seed, rng.ROLE_DEVICE_NOISE,
                            self.hypo_min_ticks, self.device, meal_spec=self.meal_spec, csr=self.csr,
                            injected=injected, controller_code=self.code, fixed=self.fixed,
-                           rerun_diverged=rerun_diverged, n_slices=self.n_slices)
+                           rerun_diverged=rerun_diverged, n_slices=self.n_slices,
+                           noise_agg=self.noise_agg, fp32=self.fp32)
 
     def reduce(self):
         engine.launch_reduce(self.outs, self.red, self.sz, self.config.dt_s, self.device)
