@@ -89,6 +89,30 @@ __device__ __forceinline__ void make_pc(const double* __restrict__ p, const Uni&
   c.sqE = (R)(u.sigEh * w);
 }
 
+// Explicit selects (setp + selp): the ternary forms below otherwise compile
+// to the DSETP.MAX/MIN + NaN-quieting sequence of fmax/fmin (5 instructions).
+__device__ __forceinline__ double zero_if_neg(double x) {   // x < 0 ? 0 : x (NaN kept)
+  double r;
+  asm("{\n\t.reg .pred p;\n\tsetp.lt.f64 p, %1, 0d0000000000000000;\n\t"
+      "selp.f64 %0, 0d0000000000000000, %1, p;\n\t}" : "=d"(r) : "d"(x));
+  return r;
+}
+__device__ __forceinline__ double pos_or_zero(double x) {   // x > 0 ? x : 0 (NaN -> 0)
+  double r;
+  asm("{\n\t.reg .pred p;\n\tsetp.gt.f64 p, %1, 0d0000000000000000;\n\t"
+      "selp.f64 %0, %1, 0d0000000000000000, p;\n\t}" : "=d"(r) : "d"(x));
+  return r;
+}
+__device__ __forceinline__ double lt_or(double x, double c) {  // x < c ? x : c (NaN -> c)
+  double r;
+  asm("{\n\t.reg .pred p;\n\tsetp.lt.f64 p, %1, %2;\n\tselp.f64 %0, %1, %2, p;\n\t}"
+      : "=d"(r) : "d"(x), "d"(c));
+  return r;
+}
+__device__ __forceinline__ float zero_if_neg(float x) { return x < 0.0f ? 0.0f : x; }
+__device__ __forceinline__ float pos_or_zero(float x) { return x > 0.0f ? x : 0.0f; }
+__device__ __forceinline__ float lt_or(float x, float c) { return x < c ? x : c; }
+
 // explicit-rounding multiply / fma in the integrator precision (no mixed
 // overloads: a double constant reaching the FP32 integrator fails to compile)
 __device__ __forceinline__ double MR_(double a, double b) { return __dmul_rn(a, b); }
@@ -205,7 +229,7 @@ enum { SI_FLAGS, SI_ANNKP, SI_ANNM, SI_MEALM, SI_EXPTR, N_SI };  // flags: mode 
 enum { SD_Q1, SD_Q2, SD_S1, SD_S2, SD_I, SD_X1, SD_X2, SD_X3, SD_D1, SD_D2, SD_G, SD_Z1, SD_Z2,
        SD_E1, SD_E2, SD_E3, SD_BGSUM, SD_DAYBASAL, SD_HUINS, SD_HU2, SD_GIN, SD_MC0, SD_MC1,
        SD_MC2, SD_SC0, SD_N = SD_SC0 + N_SC };
-enum { SV_MKS, SV_MKE, SV_ACTLO, SV_ACTHI, SV_KBMIN, SV_KBMAX, SV_RUN39, SV_RUN30, SV_EV39,
+enum { SV_MKS, SV_MKE, SV_KBMIN, SV_KBMAX, SV_RUN39, SV_RUN30, SV_EV39,
        SV_EV30, SV_ALIVE, SV_STATUS, SV_DEATH, SV_MK0, SV_SI0 = SV_MK0 + 9, SV_N = SV_SI0 + N_SI };
 
 template <int PROTO, int NOISE, typename R, bool AGG>
@@ -244,8 +268,10 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
   const int64_t n = a.n;
   const int64_t n_warps = sch.n_warps;
   const double* __restrict__ H = s_hyper;
-  uint8_t* my_hist8 = reinterpret_cast<uint8_t*>(s_hist);
-  const int tid4 = tid * 4;  // byte index of bin b: ((b >> 2) * kFastBS + tid) * 4 + (b & 3)
+  // shared address of this lane's bin-0 byte, opaque to the compiler so it
+  // stays in one register instead of being rebuilt every step
+  uint32_t hist_lane;
+  asm("mov.b32 %0, %1;" : "=r"(hist_lane) : "r"((uint32_t)__cvta_generic_to_shared(s_hist) + 4u * tid));
   const int ps = u.ps;
   const int cpd = u.ctl_per_day;
 
@@ -310,8 +336,9 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
     R Q1, Q2, S1, S2, I, X1, X2, X3, D1, D2, G, Z1, Z2, E1 = 0, E2 = 0, E3 = 0;
     R hu_ins, hu2, gin;  // per-step inputs, in the integrator precision
     double bg_sum, day_basal;
-    int32_t m_ks, m_ke, act_lo, act_hi;
-    int kb_min, kb_max, run39, run30, ev39, ev30;
+    int32_t m_ks, m_ke, act_lo = 0;
+    uint32_t act_len = 0;  // THREE_MEAL: meal input on for steps act_lo <= s < act_lo + act_len of this period
+    int kb_min, kb_max, run39, run30, ev39, ev30, trig_lo;
     bool alive;
     int status, death_tick;
     if (first) {
@@ -335,7 +362,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       s_d[SC_DGLUC][tid] = 0.0;
       bg_sum = 0.0; day_basal = 0.0; hu_ins = 0; hu2 = 0;
       kb_min = INT_MAX; kb_max = -1; run39 = run30 = ev39 = ev30 = 0;
-      m_ks = m_ke = INT_MAX; gin = 0; act_lo = act_hi = INT_MAX;
+      m_ks = m_ke = INT_MAX; gin = 0;
       if (PROTO == GT_PROTO_CSR) {
         const MealT m0 = meal_at(0);
         m_ks = m0.ks; m_ke = m0.ke; gin = (R)(u.ginK * m0.rate);
@@ -366,7 +393,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           for (int f = 0; f < 3; ++f) s_mk[f][j][tid] = (uint16_t)LDI(SV_MK0 + 3 * f + j);
         }
       }
-      m_ks = LDI(SV_MKS); m_ke = LDI(SV_MKE); act_lo = LDI(SV_ACTLO); act_hi = LDI(SV_ACTHI);
+      m_ks = LDI(SV_MKS); m_ke = LDI(SV_MKE);  // act_lo / act_len are set at the slice's first tick
       kb_min = LDI(SV_KBMIN); kb_max = LDI(SV_KBMAX); run39 = LDI(SV_RUN39); run30 = LDI(SV_RUN30);
       ev39 = LDI(SV_EV39); ev30 = LDI(SV_EV30); alive = LDI(SV_ALIVE) != 0;
       status = LDI(SV_STATUS); death_tick = LDI(SV_DEATH);
@@ -374,6 +401,9 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
 #undef LDI
       alive = alive && inrange && !was_bad;  // padding lanes read patient 0's slot
     }
+
+    // extremes / hypo-run bookkeeping is needed only for a bin <= trig_lo or >= kb_max
+    trig_lo = run39 > 0 ? INT_MAX : max(kb_min, 34);  // 34: bg < 3.9 (THRESHOLDS[34])
 
     // THREE_MEAL day window: the day's 3 meals, generated warp-uniformly at
     // the day's first tick (no divergence), tick offsets relative to the day
@@ -401,6 +431,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
     // flush the lane's uint8 histogram into its HBM column (bins 0..246;
     // bin 247 is the dead-lane sink) and clear it
     auto flush_hist = [&]() {
+      asm volatile("" ::: "memory");  // order after the asm increments
       for (int w = 0; w < kHistWords; ++w) {
         const uint32_t word = s_hist[w * kFastBS + tid];
         if (word == 0u) continue;
@@ -425,7 +456,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
     int next_flush_ctl = ctl_lo + flush_every;
 
     // ---------------------------------------------------------- one step
-    auto step = [&](const int32_t k, const bool tick, const int32_t ctl, const int32_t k_base) {
+    auto step = [&](const int32_t k, const bool tick, const int32_t ctl, const int32_t sk) {
       // noise for tick k (counter = (k, pid, role, 0))
       R z0, z1, z2;
       double zm = 0.0;
@@ -475,11 +506,12 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           if (j < 3) load_slot(j);
           else { m_ks = m_ke = INT_MAX; gin = 0; }
         }
-        act_lo = m_ks - k; act_hi = m_ke - k;
+        // opaque moves: kept in two registers rather than rebuilt from m_ks/m_ke every step
+        asm("mov.b32 %0, %1;" : "=r"(act_lo) : "r"(m_ks - k));
+        asm("mov.b32 %0, %1;" : "=r"(act_len) : "r"(m_ke - m_ks));
       }
-      const int32_t sk = k - k_base;
       const R gin_k = PROTO == GT_PROTO_CSR ? ((k >= m_ks) ? gin : (R)0)
-                                            : ((sk >= act_lo && sk < act_hi) ? gin : (R)0);
+                                            : ((uint32_t)(sk - act_lo) < act_len ? gin : (R)0);
       bool ex_active = false;
       int ex_ptr = 0;
       if (HAS_EX) {
@@ -493,11 +525,12 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       if (tick) {
         const double t_s = (double)k * u.dt;
         if (alive) {
-          const unsigned m = max(max(max(absbits(Q1), absbits(Q2)), max(absbits(S1), absbits(S2))),
-                                 max(max(absbits(I), absbits(X1)), max(absbits(X2), absbits(X3))));
-          const unsigned m2 = max(max(max(absbits(D1), absbits(D2)), max(absbits(G), absbits(Z1))),
-                                  max(max(absbits(Z2), absbits(E1)), max(absbits(E2), absbits(E3))));
-          if (max(m, m2) >= kNonfiniteBits<R>::v) { alive = false; status = GT_STATUS_NONFINITE; death_tick = k; }
+          // x * 0 is +-0 for finite x and NaN for Inf/NaN: one FMA per state
+          const R z = 0;
+          R acc = FMR(Q1, z, FMR(Q2, z, FMR(S1, z, FMR(S2, z, FMR(I, z, FMR(X1, z, FMR(X2, z, FMR(X3, z, z))))))));
+          acc = FMR(D1, z, FMR(D2, z, FMR(G, z, FMR(Z1, z, FMR(Z2, z, acc)))));
+          if (HAS_EX) acc = FMR(E1, z, FMR(E2, z, FMR(E3, z, acc)));
+          if (acc != acc) { alive = false; status = GT_STATUS_NONFINITE; death_tick = k; }
         }
         // announced carbs starting within [t, t+P)
         double announced = 0.0;
@@ -620,9 +653,10 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         // SURVEY.md §7): use the reference's exact division for that tick
         bg = Q1 / (a.params[ii * NP + PVG] * a.params[ii * NP + PW]);
       }
-      if (__builtin_expect(!(fabs(bg) < INFINITY), 0) && alive) {
-        alive = false; status = GT_STATUS_NONFINITE; death_tick = k;
-      }
+      // A non-finite bg (_kernel.py:139-141) is caught lazily: bg = Q1 * c, so the
+      // next tick's state check sees it, and bg_sum (which absorbs Inf/NaN)
+      // is checked after the last step.  Until then the lane's statistics
+      // are garbage but in range, and an aborted patient's are discarded.
       {
         // searchsorted(THRESHOLDS, bg, 'right') for bg >= 0.  THRESHOLDS[i] =
         // RN((5+i)/10), so away from a threshold the bin is floor(10 bg) - 4
@@ -639,17 +673,22 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           kb += (s_thr[kb + 1] <= bb) - (s_thr[kb] > bb);
         }
         kb = alive ? kb : GT_N_BG_BINS;  // dead lanes count into the padding bin 247
-        my_hist8[(kb >> 2) * (4 * kFastBS) + tid4 + (kb & 3)] += 1;  // < 255 between flushes
+        {  // byte ((kb >> 2) * kFastBS + tid) * 4 + (kb & 3); < 255 between flushes
+          const uint32_t ha = hist_lane + ((uint32_t)(kb & ~3) << 7) + (uint32_t)(kb & 3);
+          asm volatile("{\n\t.reg .u32 c;\n\tld.shared.u8 c, [%0];\n\tadd.u32 c, c, 1;\n\t"
+                       "st.shared.u8 [%0], c;\n\t}" :: "r"(ha));
+        }
         bg_sum += bg;
         // extremes: only a tick in the lowest/highest bin so far can move them;
         // hypo runs: only ticks below 3.9 mmol/L (or ending such a run) matter
-        if (__builtin_expect(kb <= kb_min || kb >= kb_max || kb <= 34 || run39 > 0, 0) && alive) {
+        if (__builtin_expect(kb <= trig_lo || kb >= kb_max, 0) && alive) {
           if (kb <= kb_min) { const double o = s_d[SC_BGMIN][tid]; s_d[SC_BGMIN][tid] = bg < o ? bg : o; kb_min = kb; }
           if (kb >= kb_max) { const double o = s_d[SC_BGMAX][tid]; s_d[SC_BGMAX][tid] = bg > o ? bg : o; kb_max = kb; }
           run39 = kb <= 34 ? run39 + 1 : 0;  // bg < 3.9 (THRESHOLDS[34])
           run30 = kb <= 25 ? run30 + 1 : 0;  // bg < 3.0 (THRESHOLDS[25])
           ev39 += run39 == u.hypoL;
           ev30 += run30 == u.hypoL;
+          trig_lo = run39 > 0 ? INT_MAX : max(kb_min, 34);
         }
       }
       if (tick && ctl == next_grid_ctl) {  // timeline point (warp-uniform)
@@ -673,11 +712,11 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       const R x1e = X1 * ab, x2e = X2 * ab;
       const R t1 = x1e * Q1;
       const R bg45 = bgR * (R)(1.0 / 4.5);
-      const R hf01 = MR_(pc.hF01w, bg45 < one ? bg45 : one);  // explicit: fixed rounding
+      const R hf01 = MR_(pc.hF01w, lt_or(bg45, one));  // explicit: fixed rounding
       const R ren = FMR(Q1, (R)u.rK1, -pc.rK0);
-      const R hren = ren > zero ? ren : zero;
+      const R hren = pos_or_zero(ren);
       const R egp = FMR(-pc.hE, X3, pc.hE);
-      const R hegp = FMR((R)u.cG, Z2, egp > zero ? egp : zero);
+      const R hegp = FMR((R)u.cG, Z2, pos_or_zero(egp));
       R dq = FMR(pc.hk12, Q2, D2 * pc.hTG);
       dq = FMR(-hf01, ub, dq);
       dq = FMR(-(R)u.h, t1, dq);
@@ -685,11 +724,11 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       // projection max(x, 0) (_kernel.py:175-177): keeps NaN like `if x < 0: x = 0`
       const R q1n = FMR(sqE, z0, Q1 + dq);
       const R q2n = FMR(Q2, pc.aK12, (R)u.h * FMR(-x2e, Q2, t1));
-      const R nQ1 = q1n < zero ? zero : q1n;
-      const R nQ2 = q2n < zero ? zero : q2n;
+      const R nQ1 = zero_if_neg(q1n);
+      const R nQ2 = zero_if_neg(q2n);
       R nD1 = FMR(D1, FMR(sqG, z1, pc.aG), gin_k);
       R nD2 = FMR(D2, FMR(sqG, z2, pc.aG), D1 * pc.hTG);
-      if (CLAMP_GUT) { nD1 = nD1 < zero ? zero : nD1; nD2 = nD2 < zero ? zero : nD2; }
+      if (CLAMP_GUT) { nD1 = zero_if_neg(nD1); nD2 = zero_if_neg(nD2); }
       const R nS2 = FMR(S2, pc.aI, S1 * pc.hTI);
       S1 = FMR(S1, pc.aI, hu_ins);
       const R nI = FMR(I, pc.cI, S2 * pc.dI);
@@ -732,8 +771,8 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       }
       if (__all_sync(0xffffffffu, !alive)) break;
       const int32_t kb0 = ctl * ps;
-      step(kb0, true, ctl, kb0);
-      for (int s = 1; s < ps; ++s) step(kb0 + s, false, ctl, kb0);
+      step(kb0, true, ctl, 0);
+      for (int s = 1; s < ps; ++s) step(kb0 + s, false, ctl, s);
     }
     // an all-dead warp stops early: its remaining timeline partials are identities
     for (; next_grid_ctl < ctl_hi; next_grid_ctl += u.grid_ctl, ++g_idx)
@@ -743,6 +782,9 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       }
     flush_hist();  // empties this thread's shared histogram for its next unit
 
+    if (last && alive && !(fabs(bg_sum) < INFINITY)) {  // the lazy bg check (see the step)
+      alive = false; status = GT_STATUS_NONFINITE; death_tick = (int)a.horizon_ticks;
+    }
     if (!last) {
       // ---- save the lane state for the next slice
       if (inrange) {
@@ -764,7 +806,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
             for (int f = 0; f < 3; ++f) STI(SV_MK0 + 3 * f + j, s_mk[f][j][tid]);
           }
         }
-        STI(SV_MKS, m_ks); STI(SV_MKE, m_ke); STI(SV_ACTLO, act_lo); STI(SV_ACTHI, act_hi);
+        STI(SV_MKS, m_ks); STI(SV_MKE, m_ke);
         STI(SV_KBMIN, kb_min); STI(SV_KBMAX, kb_max); STI(SV_RUN39, run39); STI(SV_RUN30, run30);
         STI(SV_EV39, ev39); STI(SV_EV30, ev30); STI(SV_ALIVE, alive ? 1 : 0);
         STI(SV_STATUS, status); STI(SV_DEATH, death_tick);
