@@ -193,9 +193,17 @@ typedef struct gt_fast_args {
      * precision: 0 = FP64 integrator, 1 = FP32 integrator (controller and
      * statistics stay FP64). */
     int32_t noise_agg, precision;
+    /* caller-owned device scratch for the persistent schedule (claim counter,
+     * per-warp slice flags, lane state saved between horizon slices), at
+     * least gt_fast_scratch_bytes(n) bytes, 16-byte aligned; it is reused
+     * stream-ordered by every launch.  NULL: the library allocates and frees
+     * it stream-ordered per launch (cudaMallocAsync). */
+    void *scratch;
+    int64_t scratch_bytes;
 } gt_fast_args;
 int gt_simulate_fast(const gt_fast_args *a, void *stream);
 int64_t gt_fast_num_warps(int64_t n);
+int64_t gt_fast_scratch_bytes(int64_t n);
 
 /* --------------------------------------------------- population reduction */
 /* Replaces TrialAccumulator.add_patient / merge (analytics.py:234-302) for a
@@ -231,7 +239,12 @@ typedef struct gt_reduce_args {
     float *metric_tbr70, *metric_tbr54, *metric_tar180, *metric_tar250;
     int64_t *metric_hist;     /* [7][201] population histograms of the 5 range
                                  fractions + 2 hypo-event counts (clamped) */
+    /* caller-owned device scratch (per-block worst-case candidates), at least
+     * GT_REDUCE_SCRATCH_BYTES; NULL: allocated stream-ordered per call */
+    void *scratch;
+    int64_t scratch_bytes;
 } gt_reduce_args;
+#define GT_REDUCE_SCRATCH_BYTES 65536
 int gt_reduce_trial(const gt_reduce_args *a, void *stream);
 
 /* ------------------------------------------------------ population sampler */

@@ -13,6 +13,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libglucosim.so")
 
+GT_REDUCE_SCRATCH_BYTES = 65536
 GT_STATUS_OK = 0
 GT_STATUS_NONFINITE = 1
 GT_STATUS_NO_STEADY_STATE = 2
@@ -71,7 +72,7 @@ class FastArgs(C.Structure):
         ("wiener", P), ("has_noise", P), ("meas", P),
         ("status", P), ("ticks", P), ("bg_hist", P), ("bg_stats", P), ("day_dose", P),
         ("hypo_events", P), ("timeline_pp", P), ("timeline_warp", P), ("x_out", P),
-        ("noise_agg", I32), ("precision", I32),
+        ("noise_agg", I32), ("precision", I32), ("scratch", P), ("scratch_bytes", I64),
     ]
 
 
@@ -85,7 +86,7 @@ class ReduceArgs(C.Structure):
         ("below_min", P), ("below_max", P), ("minmax_bg_bits", P), ("timeline", P),
         ("dose_hist", P), ("dose_sum_fp", P), ("worst", P),
         ("metric_tir", P), ("metric_tbr70", P), ("metric_tbr54", P), ("metric_tar180", P),
-        ("metric_tar250", P), ("metric_hist", P),
+        ("metric_tar250", P), ("metric_hist", P), ("scratch", P), ("scratch_bytes", I64),
     ]
 
 
@@ -110,6 +111,7 @@ SIGNATURES = [
     ("gt_simulate_parity", C.c_int, [C.POINTER(ParityArgs), P]),
     ("gt_simulate_fast", C.c_int, [C.POINTER(FastArgs), P]),
     ("gt_fast_num_warps", I64, [I64]),
+    ("gt_fast_scratch_bytes", I64, [I64]),
     ("gt_reduce_trial", C.c_int, [C.POINTER(ReduceArgs), P]),
     ("gt_sample_population", C.c_int, [C.POINTER(SamplerArgs), P]),
     ("gt_generate_meals", C.c_int, [I64, I64, U64, C.POINTER(MealGen), I64, P, P, P, P]),

@@ -24,12 +24,22 @@ int gt_check_launch(const char* what) {
   return GT_OK;
 }
 
+void gt_keep_pool_mapped() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+  uint64_t thr = UINT64_MAX;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+}
+
 int gt_launch_parity(const gt_parity_args* a, cudaStream_t st);
 int gt_launch_steady_state(int64_t n, const double* params, double target_bg, double* x0,
                            double* ub, int32_t* status, cudaStream_t st);
 int gt_launch_controller_init(int64_t n, const double* hyper, double icr_initial_factor,
                               const double* basal, double* c0, cudaStream_t st);
 int gt_launch_fast(const gt_fast_args* a, cudaStream_t st);
+int64_t gt_fast_scratch_need(int64_t n);
 int gt_launch_reduce(const gt_reduce_args* a, void* scratch_worst, int nblk, cudaStream_t st);
 int gt_launch_sampler(const gt_sampler_args* a, cudaStream_t st);
 int gt_launch_meals(int64_t n, int64_t pid0, uint64_t seed, const gt_meal_gen* g, int64_t n_meals,
@@ -110,6 +120,7 @@ int gt_simulate_parity(const gt_parity_args* a, void* stream) {
 }
 
 int64_t gt_fast_num_warps(int64_t n) { return (n + 31) / 32; }
+int64_t gt_fast_scratch_bytes(int64_t n) { return n <= 0 ? 0 : gt_fast_scratch_need(n); }
 
 int gt_simulate_fast(const gt_fast_args* a, void* stream) {
   REQUIRE(a, "gt_simulate_fast: null args");
@@ -166,13 +177,20 @@ int gt_reduce_trial(const gt_reduce_args* a, void* stream) {
   int nblk = sms * 4;
   const int64_t need = (a->n + 255) / 256;
   if (need < nblk) nblk = (int)(need > 0 ? need : 1);
-  void* scratch = nullptr;
-  if (cudaMallocAsync(&scratch, (size_t)nblk * 24, S(stream)) != cudaSuccess) {
-    gt_set_error("gt_reduce_trial: cudaMallocAsync failed");
-    return GT_ECUDA;
+  if (nblk * 24 > GT_REDUCE_SCRATCH_BYTES) nblk = GT_REDUCE_SCRATCH_BYTES / 24;
+  void* scratch = a->scratch;
+  const bool own = scratch == nullptr;
+  if (own) {
+    gt_keep_pool_mapped();
+    if (cudaMallocAsync(&scratch, (size_t)nblk * 24, S(stream)) != cudaSuccess) {
+      gt_set_error("gt_reduce_trial: cudaMallocAsync failed");
+      return GT_ECUDA;
+    }
+  } else {
+    REQUIRE(a->scratch_bytes >= (int64_t)nblk * 24, "gt_reduce_trial: scratch smaller than GT_REDUCE_SCRATCH_BYTES");
   }
   const int e = gt_launch_reduce(a, scratch, nblk, S(stream));
-  cudaFreeAsync(scratch, S(stream));
+  if (own) cudaFreeAsync(scratch, S(stream));
   return e;
 }
 

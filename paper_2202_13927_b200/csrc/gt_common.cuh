@@ -172,3 +172,7 @@ __device__ __forceinline__ long long ordered_bits(double v) {
 // error plumbing (gt_capi.cu)
 void gt_set_error(const char* fmt, ...);
 int gt_check_launch(const char* what);
+// Keep the current device's default stream-ordered pool mapped between
+// calls (release threshold = max), so per-launch cudaMallocAsync fallbacks
+// do not re-map memory after every synchronisation.
+void gt_keep_pool_mapped();

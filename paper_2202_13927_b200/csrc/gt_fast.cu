@@ -457,39 +457,45 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
 
     // ---------------------------------------------------------- one step
     auto step = [&](const int32_t k, const bool tick, const int32_t ctl, const int32_t sk) {
-      // noise for tick k (counter = (k, pid, role, 0))
+      // noise for tick k (counter = (k, pid, role, 0)).  On a controller tick
+      // the reading's normal is needed first; otherwise the draw is placed
+      // next to the Euler update, in one basic block with the FP64 model
+      // arithmetic, so the Philox chain overlaps it.
       R z0, z1, z2;
       double zm = 0.0;
-      if (NOISE == GT_NOISE_PHILOX) {
-        if (!AGG) {
-          const U4 r = philox_fast((uint32_t)k, pid, a.noise_role, 0u, u.rk);
-          float f0, f1, f2, f3;
-          box_muller(r.x, r.y, f0, f1);
-          box_muller(r.z, r.w, f2, f3);
-          z0 = f0; z1 = f1; z2 = f2;
-          if (tick) zm = f3;
-        } else {
-          // Brownian aggregation: this step's increment is the sum of the agg
-          // fine increments at counters k*agg + j (the path a run at dt/agg
-          // draws), rescaled to unit variance; the reading uses fine tick k*agg
-          R s0 = 0, s1 = 0, s2 = 0;
-          const uint32_t kf = (uint32_t)k * (uint32_t)u.agg;
-          for (int j = 0; j < u.agg; ++j) {
-            const U4 r = philox_fast(kf + (uint32_t)j, pid, a.noise_role, 0u, u.rk);
+      auto draw_noise = [&]() {
+        if (NOISE == GT_NOISE_PHILOX) {
+          if (!AGG) {
+            const U4 r = philox_fast((uint32_t)k, pid, a.noise_role, 0u, u.rk);
             float f0, f1, f2, f3;
             box_muller(r.x, r.y, f0, f1);
             box_muller(r.z, r.w, f2, f3);
-            s0 += (R)f0; s1 += (R)f1; s2 += (R)f2;
-            if (j == 0 && tick) zm = f3;
+            z0 = f0; z1 = f1; z2 = f2;
+            if (tick) zm = f3;
+          } else {
+            // Brownian aggregation: this step's increment is the sum of the agg
+            // fine increments at counters k*agg + j (the path a run at dt/agg
+            // draws), rescaled to unit variance; the reading uses fine tick k*agg
+            R s0 = 0, s1 = 0, s2 = 0;
+            const uint32_t kf = (uint32_t)k * (uint32_t)u.agg;
+            for (int j = 0; j < u.agg; ++j) {
+              const U4 r = philox_fast(kf + (uint32_t)j, pid, a.noise_role, 0u, u.rk);
+              float f0, f1, f2, f3;
+              box_muller(r.x, r.y, f0, f1);
+              box_muller(r.z, r.w, f2, f3);
+              s0 += (R)f0; s1 += (R)f1; s2 += (R)f2;
+              if (j == 0 && tick) zm = f3;
+            }
+            const R sc = (R)u.rs_agg;
+            z0 = s0 * sc; z1 = s1 * sc; z2 = s2 * sc;
           }
-          const R sc = (R)u.rs_agg;
-          z0 = s0 * sc; z1 = s1 * sc; z2 = s2 * sc;
+        } else {
+          const double* wv = a.wiener + (ii * (int64_t)a.horizon_ticks + k) * 3;
+          z0 = (R)wv[0]; z1 = (R)wv[1]; z2 = (R)wv[2];
+          if (tick) zm = a.meas[ii * (int64_t)u.n_ctl + ctl];
         }
-      } else {
-        const double* wv = a.wiener + (ii * (int64_t)a.horizon_ticks + k) * 3;
-        z0 = (R)wv[0]; z1 = (R)wv[1]; z2 = (R)wv[2];
-        if (tick) zm = a.meas[ii * (int64_t)u.n_ctl + ctl];
-      }
+      };
+      if (tick) draw_noise();
       // disturbances at tick k (_kernel.py:85-94)
       if (PROTO == GT_PROTO_CSR) {
         while (k >= m_ke) {
@@ -704,6 +710,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         if (a.timeline_pp && inrange) a.timeline_pp[(int64_t)g_idx * n + i] = alive ? bg : 0.0;
         ++g_idx;
       }
+      if (!tick) draw_noise();
       // Euler–Maruyama step, re-associated (hovorka.py:76-150)
       // (in R: launch-uniform constants are rounded to R at their use)
       const R bgR = (R)bg, zero = 0, one = 1;
@@ -918,15 +925,21 @@ static int launch_one(const gt_fast_args* a, const gt::Uni& u, cudaStream_t st) 
   s.n_chunks = (n_ctl + s.chunk_ctl - 1) / s.chunk_ctl;
   s.n_units = (int)(warps * s.n_chunks);
   // scratch: counter + done flags (+ saved lane state when slicing)
-  const size_t n_pad = (size_t)warps * 32;
   const size_t bytes_i = sizeof(int) * (1 + (size_t)warps);
   const size_t bytes_state = s.n_chunks > 1 ? (size_t)a->n * (gt::SD_N * sizeof(double) + gt::SV_N * sizeof(int)) : 0;
-  char* scratch = nullptr;
-  if (cudaMallocAsync(&scratch, bytes_i + bytes_state + 16, st) != cudaSuccess) {
-    gt_set_error("gt_simulate_fast: scratch allocation failed");
-    return GT_ECUDA;
+  const size_t need = ((bytes_i + 15) & ~size_t(15)) + bytes_state;
+  char* scratch = static_cast<char*>(a->scratch);
+  const bool own = scratch == nullptr;
+  if (own) {
+    gt_keep_pool_mapped();
+    if (cudaMallocAsync(&scratch, need, st) != cudaSuccess) {
+      gt_set_error("gt_simulate_fast: scratch allocation failed");
+      return GT_ECUDA;
+    }
+  } else if (a->scratch_bytes < (int64_t)need || (reinterpret_cast<uintptr_t>(scratch) & 15u)) {
+    gt_set_error("gt_simulate_fast: scratch must be 16-byte aligned and >= gt_fast_scratch_bytes(n)");
+    return GT_EINVAL;
   }
-  (void)n_pad;
   cudaMemsetAsync(scratch, 0, bytes_i, st);
   s.counter = reinterpret_cast<int*>(scratch);
   s.done = s.counter + 1;
@@ -939,8 +952,15 @@ static int launch_one(const gt_fast_args* a, const gt::Uni& u, cudaStream_t st) 
   const unsigned grid = (unsigned)std::min<int64_t>((int64_t)sms * per_sm, blocks_needed);
   kern<<<grid, gt::kFastBS, kDyn, st>>>(*a, u, s);
   const int e = gt_check_launch("fast_kernel");
-  cudaFreeAsync(scratch, st);
+  if (own) cudaFreeAsync(scratch, st);
   return e;
+}
+
+// Upper bound of launch_one's scratch (sliced schedule) for n patients.
+int64_t gt_fast_scratch_need(int64_t n) {
+  const int64_t warps = (n + 31) / 32;
+  const int64_t bytes_i = (int64_t)sizeof(int) * (1 + warps);
+  return ((bytes_i + 15) & ~int64_t(15)) + n * (int64_t)(gt::SD_N * sizeof(double) + gt::SV_N * sizeof(int));
 }
 
 int gt_launch_fast(const gt_fast_args* a, cudaStream_t st) {

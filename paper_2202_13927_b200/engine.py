@@ -173,6 +173,7 @@ class FastOutputs:
     timeline_warp: object # [n_grid, n_warps, 3]
     timeline_pp: object = None
     x_out: object = None
+    scratch: object = None  # uint8 [gt_fast_scratch_bytes(n)]: the persistent schedule's workspace
 
 
 def alloc_fast_outputs(n: int, pid0: int, sz: dict, device, per_patient_timeline=False,
@@ -188,6 +189,7 @@ def alloc_fast_outputs(n: int, pid0: int, sz: dict, device, per_patient_timeline
         timeline_warp=empty((sz["n_grid"], nw, 3), t.int64, device),
         timeline_pp=empty((sz["n_grid"], n), t.float64, device) if per_patient_timeline else None,
         x_out=empty((N_STATES, n), t.float64, device) if final_state else None,
+        scratch=empty((int(_lib.load().gt_fast_scratch_bytes(n)),), t.uint8, device),
     )
 
 
@@ -232,6 +234,8 @@ def launch_fast(inputs: dict, outs: FastOutputs, sz: dict, dt_s: float, period_s
     a.status, a.ticks, a.bg_hist, a.bg_stats = ptr(outs.status), ptr(outs.ticks), ptr(outs.bg_hist), ptr(outs.bg_stats)
     a.day_dose, a.hypo_events, a.timeline_warp = ptr(outs.day_dose), ptr(outs.hypo_events), ptr(outs.timeline_warp)
     a.timeline_pp, a.x_out = ptr(outs.timeline_pp), ptr(outs.x_out)
+    if outs.scratch is not None:
+        a.scratch, a.scratch_bytes = ptr(outs.scratch), outs.scratch.numel()
     check(_lib.load().gt_simulate_fast(C.byref(a), stream_ptr(device)), "gt_simulate_fast")
 
 
@@ -266,6 +270,7 @@ class ReduceOutputs:
     worst: object
     metric_hist: object
     metrics: dict | None = None
+    scratch: object = None  # uint8 [GT_REDUCE_SCRATCH_BYTES]
 
 
 def alloc_reduce_outputs(n: int, sz: dict, device, per_patient_metrics=False) -> ReduceOutputs:
@@ -280,6 +285,7 @@ def alloc_reduce_outputs(n: int, sz: dict, device, per_patient_metrics=False) ->
         worst=empty((4,), i64, device), metric_hist=empty((7, TIR_BINS + 1), i64, device),
         metrics={k: empty((n,), t.float32, device) for k in ("tir", "tbr70", "tbr54", "tar180", "tar250")}
         if per_patient_metrics else None,
+        scratch=empty((_lib.GT_REDUCE_SCRATCH_BYTES,), t.uint8, device),
     )
 
 
@@ -295,6 +301,8 @@ def launch_reduce(outs: FastOutputs, red: ReduceOutputs, sz: dict, dt_s: float, 
     if red.metrics is not None:
         a.metric_tir, a.metric_tbr70, a.metric_tbr54 = (ptr(red.metrics[k]) for k in ("tir", "tbr70", "tbr54"))
         a.metric_tar180, a.metric_tar250 = ptr(red.metrics["tar180"]), ptr(red.metrics["tar250"])
+    if red.scratch is not None:
+        a.scratch, a.scratch_bytes = ptr(red.scratch), red.scratch.numel()
     check(_lib.load().gt_reduce_trial(C.byref(a), stream_ptr(device)), "gt_reduce_trial")
 
 
