@@ -200,6 +200,10 @@ typedef struct gt_fast_args {
      * it stream-ordered per launch (cudaMallocAsync). */
     void *scratch;
     int64_t scratch_bytes;
+    /* optional per-step trace, [n][horizon_ticks][8] = the parity kernel's
+     * columns (t, bg, last CGM reading, meal g/min, exercise HRR, basal U/h,
+     * bolus U, glucagon ug); NULL = off.  A traced launch runs unsliced. */
+    double *trace;
 } gt_fast_args;
 int gt_simulate_fast(const gt_fast_args *a, void *stream);
 int64_t gt_fast_num_warps(int64_t n);

@@ -73,6 +73,7 @@ class FastArgs(C.Structure):
         ("status", P), ("ticks", P), ("bg_hist", P), ("bg_stats", P), ("day_dose", P),
         ("hypo_events", P), ("timeline_pp", P), ("timeline_warp", P), ("x_out", P),
         ("noise_agg", I32), ("precision", I32), ("scratch", P), ("scratch_bytes", I64),
+        ("trace", P),
     ]
 
 

@@ -232,7 +232,7 @@ enum { SD_Q1, SD_Q2, SD_S1, SD_S2, SD_I, SD_X1, SD_X2, SD_X3, SD_D1, SD_D2, SD_G
 enum { SV_MKS, SV_MKE, SV_KBMIN, SV_KBMAX, SV_RUN39, SV_RUN30, SV_EV39,
        SV_EV30, SV_ALIVE, SV_STATUS, SV_DEATH, SV_MK0, SV_SI0 = SV_MK0 + 9, SV_N = SV_SI0 + N_SI };
 
-template <int PROTO, int NOISE, typename R, bool AGG>
+template <int PROTO, int NOISE, typename R, bool AGG, bool TRACE>
 __global__ void __launch_bounds__(kFastBS, GT_FAST_MINB)
 fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
   constexpr bool HAS_EX = (PROTO == GT_PROTO_CSR);
@@ -339,6 +339,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
     int32_t m_ks, m_ke, act_lo = 0;
     uint32_t act_len = 0;  // THREE_MEAL: meal input on for steps act_lo <= s < act_lo + act_len of this period
     int kb_min, kb_max, run39, run30, ev39, ev30, trig_lo;
+    double tr_rate = 0.0, tr_y = 0.0, tr_basal = 0.0;  // TRACE only (held trace columns)
     bool alive;
     int status, death_tick;
     if (first) {
@@ -366,6 +367,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       if (PROTO == GT_PROTO_CSR) {
         const MealT m0 = meal_at(0);
         m_ks = m0.ks; m_ke = m0.ke; gin = (R)(u.ginK * m0.rate);
+        if (TRACE) tr_rate = m0.rate;
         s_i[SI_MEALM][tid] = 0;
         s_i[SI_ANNM][tid] = 0;
         s_i[SI_ANNKP][tid] = m0.kp;
@@ -415,6 +417,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       if (ks == 0xFFFF) { m_ks = m_ke = INT_MAX; gin = 0; return; }
       m_ks = day_k0 + ks; m_ke = day_k0 + s_mk[1][j][tid];
       gin = (R)(u.ginK * (s_mc[j][tid] / u.meal_dur_min));  // rate = g / duration (simulation.py:162)
+      if (TRACE) tr_rate = s_mc[j][tid] / u.meal_dur_min;
     };
     auto gen_day = [&](int32_t d) {
       for (int j = 0; j < 3; ++j) {
@@ -463,6 +466,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       // arithmetic, so the Philox chain overlaps it.
       R z0, z1, z2;
       double zm = 0.0;
+      double tr_bolus = 0.0, tr_gluc = 0.0;  // TRACE only
       auto draw_noise = [&]() {
         if (NOISE == GT_NOISE_PHILOX) {
           if (!AGG) {
@@ -503,6 +507,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           s_i[SI_MEALM][tid] = m;
           const MealT mt = meal_at(m);
           m_ks = mt.ks; m_ke = mt.ke; gin = (R)(u.ginK * mt.rate);
+          if (TRACE) tr_rate = mt.rate;
         }
       } else if (tick) {
         // generated meals are >= one period apart, so the active window of
@@ -564,6 +569,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         if (HAS_EX && ex_active && a.ex_announced[ex_lo + ex_ptr] != 0.0)
           phase = t_s - a.ex_start_s[ex_lo + ex_ptr];
         const double y = A_((double)G, M_(u.sqrtR, zm));
+        if (TRACE) tr_y = y;
         // ---- controller_step_vec (controller.py:343-458); state in shared
         // memory.  Explicit IEEE operations in the reference's order: the
         // controller is bit-identical to the reference's for identical readings.
@@ -645,6 +651,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         }
         s_i[SI_FLAGS][tid] = flags;
         day_basal = fma(b_basal, (double)ps, day_basal);  // basal held for the whole period
+        if (TRACE) { tr_basal = b_basal; tr_bolus = b_bolus; tr_gluc = b_gluc; }
         hu_ins = (R)fma(b_bolus, u.u_bolus_k, b_basal * u.u_basal_k);   // h * (u[0] + u[1])
         hu2 = (R)(b_gluc * u.u_gluc_k);                                 // h * u[2]
         if (b_bolus > 0.0 || b_gluc > 0.0) {
@@ -709,6 +716,11 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         }
         if (a.timeline_pp && inrange) a.timeline_pp[(int64_t)g_idx * n + i] = alive ? bg : 0.0;
         ++g_idx;
+      }
+      if (TRACE && inrange) {  // the parity kernel's 8 trace columns (simulation.py:61-64)
+        double* tr = a.trace + ((int64_t)i * a.horizon_ticks + k) * 8;
+        tr[0] = (double)k * u.dt; tr[1] = bg; tr[2] = tr_y; tr[3] = gin_k != (R)0 ? tr_rate : 0.0;
+        tr[4] = hrr; tr[5] = tr_basal; tr[6] = tr_bolus; tr[7] = tr_gluc;
       }
       if (!tick) draw_noise();
       // Euler–Maruyama step, re-associated (hovorka.py:76-150)
@@ -900,10 +912,10 @@ static int choose_chunks(int64_t warps, int64_t slots, int n_ctl) {
   return best;
 }
 
-template <int PROTO, int NOISE, typename R = double, bool AGG = false>
-static int launch_one(const gt_fast_args* a, const gt::Uni& u, cudaStream_t st) {
+template <int PROTO, int NOISE, typename R, bool AGG, bool TRACE>
+static int launch_sched(const gt_fast_args* a, const gt::Uni& u, cudaStream_t st) {
   constexpr int kDyn = gt::kHistWords * gt::kFastBS * 4;
-  auto kern = gt::fast_kernel<PROTO, NOISE, R, AGG>;
+  auto kern = gt::fast_kernel<PROTO, NOISE, R, AGG, TRACE>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
@@ -917,7 +929,8 @@ static int launch_one(const gt_fast_args* a, const gt::Uni& u, cudaStream_t st) 
   const int64_t warps = (a->n + 31) / 32;
   const int64_t slots = (int64_t)sms * per_sm * (gt::kFastBS / 32);
   const int n_ctl = u.n_ctl;
-  const int chunks = a->n_slices > 0 ? std::min(a->n_slices, n_ctl) : choose_chunks(warps, slots, n_ctl);
+  // a traced launch runs unsliced (the held trace columns are not saved between slices)
+  const int chunks = TRACE ? 1 : a->n_slices > 0 ? std::min(a->n_slices, n_ctl) : choose_chunks(warps, slots, n_ctl);
   gt::Sched s{};
   s.n_warps = (int)warps;
   s.n_chunks = chunks;
@@ -954,6 +967,12 @@ static int launch_one(const gt_fast_args* a, const gt::Uni& u, cudaStream_t st) 
   const int e = gt_check_launch("fast_kernel");
   if (own) cudaFreeAsync(scratch, st);
   return e;
+}
+
+template <int PROTO, int NOISE, typename R = double, bool AGG = false>
+static int launch_one(const gt_fast_args* a, const gt::Uni& u, cudaStream_t st) {
+  if (a->trace) return launch_sched<PROTO, NOISE, R, AGG, true>(a, u, st);
+  return launch_sched<PROTO, NOISE, R, AGG, false>(a, u, st);
 }
 
 // Upper bound of launch_one's scratch (sliced schedule) for n patients.

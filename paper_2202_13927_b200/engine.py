@@ -198,7 +198,7 @@ def launch_fast(inputs: dict, outs: FastOutputs, sz: dict, dt_s: float, period_s
                 meal_spec: dict | None = None, csr: dict | None = None,
                 injected: dict | None = None, controller_code: int = 0, fixed=None,
                 rerun_diverged: bool = False, n_slices: int = 0, noise_agg: int = 1,
-                fp32: bool = False) -> None:
+                fp32: bool = False, trace=None) -> None:
     """Enqueue the fused integrator on the current stream (no sync).
     ``fixed``: the launch-uniform values of the non-sampled parameters
     (p[30] order); defaults to row 0 of ``inputs['params']`` after checking
@@ -236,6 +236,7 @@ def launch_fast(inputs: dict, outs: FastOutputs, sz: dict, dt_s: float, period_s
     a.timeline_pp, a.x_out = ptr(outs.timeline_pp), ptr(outs.x_out)
     if outs.scratch is not None:
         a.scratch, a.scratch_bytes = ptr(outs.scratch), outs.scratch.numel()
+    a.trace = ptr(trace)   # [n, horizon_ticks, 8] float64 or None
     check(_lib.load().gt_simulate_fast(C.byref(a), stream_ptr(device)), "gt_simulate_fast")
 
 

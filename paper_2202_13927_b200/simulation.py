@@ -228,7 +228,7 @@ def run_trial(population, protocol_generator, controller_id: str, profile, model
         from .trial import run_trial_fast
         return run_trial_fast(population, protocol_generator, controller_id, profile, model_id,
                               config, basal_scale=basal_scale, run_meta=run_meta, progress=progress,
-                              device=device, hypo_min_s=hypo_min_s)
+                              device=device, hypo_min_s=hypo_min_s, trace_dir=trace_dir)
     raise SimulationError("noise must be 'reference' or 'philox'")
 
 

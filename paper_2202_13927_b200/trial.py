@@ -65,6 +65,7 @@ class FastTrial:
         self.pid0 = int(pid0)
         self.n = int(params.shape[0])
         self.seed = int(config.seed if seed is None else seed)
+        self.controller_id = controller_id
         self.code = device_code(controller_id)
         self.profile = profile
         self.hyper = hyper_vector(profile)
@@ -129,6 +130,33 @@ class FastTrial:
                            injected=injected, controller_code=self.code, fixed=self.fixed,
                            rerun_diverged=rerun_diverged, n_slices=self.n_slices,
                            noise_agg=self.noise_agg, fp32=self.fp32)
+
+    def trace_range(self, lo: int, hi: int):
+        """Re-simulate patients [lo, hi) of this shard with the per-step trace
+        (the 8 columns of simulation.py:61-64).  Same streams and arithmetic as
+        ``simulate``, so every statistic of a traced patient is reproduced
+        exactly.  Returns numpy (status [m], ticks [m], trace [m, H, 8])."""
+        t = engine.torch()
+        sub = FastTrial(self.pid0 + lo, self.params[lo:hi].contiguous(), self.basal[lo:hi].contiguous(),
+                        self.generator, self.profile, self.config, self.controller_id, self.device,
+                        hypo_min_s=self.hypo_min_ticks * self.config.dt_s, seed=self.seed,
+                        noise_agg=self.noise_agg, fp32=self.fp32)
+        tr = engine.empty((sub.n, self.sz["horizon_ticks"], 8), t.float64, self.device)
+        engine.launch_fast(sub._inputs, sub.outs, sub.sz, self.config.dt_s, self.config.controller_period_s,
+                           sub.seed, rng.ROLE_DEVICE_NOISE, sub.hypo_min_ticks, self.device,
+                           meal_spec=sub.meal_spec, csr=sub.csr, controller_code=sub.code, fixed=sub.fixed,
+                           noise_agg=sub.noise_agg, fp32=sub.fp32, trace=tr)
+        return sub.outs.status.cpu().numpy(), sub.outs.ticks.cpu().numpy(), tr.cpu().numpy()
+
+    def worst_trace(self, acc: TrialAccumulator):
+        """Trace of the accumulator's worst case (simulation.py:619-624), or None."""
+        if acc.worst is None:
+            return None
+        i = acc.worst.patient_id - self.pid0
+        if not 0 <= i < self.n:
+            return None
+        _st, ticks, tr = self.trace_range(i, i + 1)
+        return tr[0, : int(ticks[0])]
 
     def reduce(self):
         engine.launch_reduce(self.outs, self.red, self.sz, self.config.dt_s, self.device)
@@ -199,8 +227,12 @@ class FastTrial:
 
 def run_trial_fast(population, generator, controller_id, profile, model_id, config, *,
                    basal_scale=1.0, run_meta=None, progress=None, device=None,
-                   hypo_min_s=900.0, per_patient_metrics=True):
-    from .simulation import TrialResult, _meta
+                   hypo_min_s=900.0, per_patient_metrics=True, trace_dir=None):
+    """Fused-path ``run_trial`` (simulation.py:551-628 semantics): one staged
+    shard, device reduction, report; ``store_trace`` policies by traced
+    re-simulation (same streams, so the worst case's statistics are exact)."""
+    import os
+    from .simulation import TrialResult, _meta, save_trace
     t0 = time.perf_counter()
     device = engine.require_device(device)
     pid0, params, basal = population_to_device(population, basal_scale, device)
@@ -215,7 +247,19 @@ def run_trial_fast(population, generator, controller_id, profile, model_id, conf
         raise SimulationError("all simulations diverged; nothing to report")
     meta = _meta(config, ft.n, model_id, controller_id, profile, basal_scale, generator, run_meta)
     report = analytics.build_trial_report(acc, meta)
-    return TrialResult(report=report, accumulator=acc, worst_trace=None, wall_s=wall_s,
+    worst_trace = None
+    if config.store_trace in ("worst_case_only", "always"):
+        worst_trace = ft.worst_trace(acc)
+    if config.store_trace == "always" and trace_dir is not None:
+        os.makedirs(trace_dir, exist_ok=True)
+        chunk = max(1, int(2**31 // (ft.sz["horizon_ticks"] * 64)))   # <= 2 GiB of trace per launch
+        for lo in range(0, ft.n, chunk):
+            hi = min(ft.n, lo + chunk)
+            st, ticks, tr = ft.trace_range(lo, hi)
+            for j in range(hi - lo):
+                if int(st[j]) == GT_STATUS_OK:
+                    save_trace(os.path.join(trace_dir, f"patient_{pid0 + lo + j:06d}.npz"), tr[j, : int(ticks[j])])
+    return TrialResult(report=report, accumulator=acc, worst_trace=worst_trace, wall_s=wall_s,
                        n_patients=ft.n, metrics=ft.metrics())
 
 

@@ -305,3 +305,35 @@ def test_horizon_slicing_is_invisible(dev, slices):
                               equal_nan=getattr(a.outs, k).dtype.is_floating_point), k
     assert _acc_equal(a.accumulator(), b.accumulator())
     assert a.accumulator().aborted_ids == (37,)
+
+
+def test_fast_worst_trace_reproduces_the_worst_case(dev, tmp_path):
+    """store_trace on the fused path: the worst case is re-simulated with the
+    per-step trace (same Philox streams and arithmetic), so its minimum BG,
+    ticks below 3 mmol/L, histogram and BG sum are reproduced exactly
+    (the reference's contract, test_simulation.py:290-306)."""
+    import os
+    from paper_2202_13927_b200.config import SimulationConfig
+    from paper_2202_13927_b200.controller import ControllerHyperparameters
+    from paper_2202_13927_b200.layout import THRESHOLDS
+    from paper_2202_13927_b200.population import generate_population
+    from paper_2202_13927_b200.protocol import ThreeMealProtocol
+    from paper_2202_13927_b200.simulation import load_trace, run_trial
+    cfg = SimulationConfig(horizon_s=3 * 86400.0, seed=17, dt_s=60.0, store_trace="always")
+    pop = generate_population(17, 300, device=dev, on_exhausted="redraw_weight")
+    res = run_trial(pop, ThreeMealProtocol(), "dual_hormone", ControllerHyperparameters(), "hovorka_ext", cfg,
+                    noise="philox", device=dev, trace_dir=str(tmp_path))
+    w = res.accumulator.worst
+    tr = res.worst_trace
+    H = 3 * 1440
+    assert tr.shape == (H, 8)
+    bg = tr[:, 1]
+    assert bg.min() == w.min_bg and bg.max() == w.max_bg
+    assert int((bg < 3.0).sum()) == w.ticks_below_3
+    assert np.array_equal(np.bincount(np.searchsorted(THRESHOLDS, bg, side="right"), minlength=247), w.bg_hist)
+    assert np.array_equal(tr[:, 0], np.arange(H) * 60.0)
+    assert np.all(tr[::5, 5] >= 0) and np.all(np.diff(tr[:, 2])[np.arange(H - 1) % 5 != 4] == 0)
+    files = sorted(os.listdir(tmp_path))
+    assert len(files) == res.accumulator.n_patients
+    again = load_trace(os.path.join(tmp_path, f"patient_{w.patient_id:06d}.npz"))
+    assert np.array_equal(again, tr)
