@@ -288,6 +288,33 @@ int gt_generate_meals(int64_t n, int64_t pid0, uint64_t seed, const gt_meal_gen 
                       int64_t n_meals, double *start_s, double *end_s, double *carbs_g,
                       void *stream);
 
+/* ------------------------------------------- NorthernYear protocol builder */
+/* The reference's NorthernYearProtocol (simulation.py:420-453 ->
+ * protocol.py:191-394, default announcement policy) for patients
+ * pid0..pid0+n-1, planned on the device from the reference's own keyed numpy
+ * stream (derive_seed(trial_seed, pid, 3) -> Philox4x64) and written in the
+ * fused kernel's tick-compiled CSR layout at a fixed stride: patient i owns
+ * records [i*GT_NY_MEALS, (i+1)*GT_NY_MEALS) and [i*GT_NY_EX, (i+1)*GT_NY_EX).
+ * Events starting at or after horizon_s are inert (ticks INT_MAX).  Replaces
+ * the host path generator.build -> compile_protocol -> compile_ticks. */
+#define GT_NY_MEALS 1588
+#define GT_NY_EX 76
+typedef struct {
+    int64_t n, pid0;
+    uint64_t trial_seed;
+    double dt_s, period_s, horizon_s;
+    const double *params;           /* [n][30]; body weight = p[0] */
+    int32_t *meal_ks, *meal_ke, *meal_kp;
+    double *meal_rate, *meal_ann;   /* [n][GT_NY_MEALS] */
+    int32_t *ex_ks, *ex_ke;
+    double *ex_start_s, *ex_hrr, *ex_announced;  /* [n][GT_NY_EX] */
+    int32_t *n_meals, *n_ex;        /* optional [n]: events before the horizon
+                                       (n_meals = -1: week plan failed) */
+    uint16_t *week_days;            /* optional [52][n]: 2-bit day types
+                                       (standard, active, movie, late) */
+} gt_northern_args;
+int gt_northern_protocol(const gt_northern_args *a, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -102,6 +102,19 @@ class SamplerArgs(C.Structure):
     ]
 
 
+GT_NY_MEALS = 1588
+GT_NY_EX = 76
+
+
+class NorthernArgs(C.Structure):
+    _fields_ = [
+        ("n", I64), ("pid0", I64), ("trial_seed", U64), ("dt_s", D), ("period_s", D), ("horizon_s", D),
+        ("params", P), ("meal_ks", P), ("meal_ke", P), ("meal_kp", P), ("meal_rate", P), ("meal_ann", P),
+        ("ex_ks", P), ("ex_ke", P), ("ex_start_s", P), ("ex_hrr", P), ("ex_announced", P),
+        ("n_meals", P), ("n_ex", P), ("week_days", P),
+    ]
+
+
 # (name, restype, argtypes) of every symbol include/glucosim.h declares
 SIGNATURES = [
     ("gt_abi_version", C.c_int, []),
@@ -116,6 +129,7 @@ SIGNATURES = [
     ("gt_reduce_trial", C.c_int, [C.POINTER(ReduceArgs), P]),
     ("gt_sample_population", C.c_int, [C.POINTER(SamplerArgs), P]),
     ("gt_generate_meals", C.c_int, [I64, I64, U64, C.POINTER(MealGen), I64, P, P, P, P]),
+    ("gt_northern_protocol", C.c_int, [C.POINTER(NorthernArgs), P]),
 ]
 
 

@@ -40,6 +40,7 @@ int gt_launch_controller_init(int64_t n, const double* hyper, double icr_initial
                               const double* basal, double* c0, cudaStream_t st);
 int gt_launch_fast(const gt_fast_args* a, cudaStream_t st);
 int64_t gt_fast_scratch_need(int64_t n);
+int gt_launch_northern(const gt_northern_args* a, cudaStream_t st);
 int gt_launch_reduce(const gt_reduce_args* a, void* scratch_worst, int nblk, cudaStream_t st);
 int gt_launch_sampler(const gt_sampler_args* a, cudaStream_t st);
 int gt_launch_meals(int64_t n, int64_t pid0, uint64_t seed, const gt_meal_gen* g, int64_t n_meals,
@@ -213,6 +214,16 @@ int gt_generate_meals(int64_t n, int64_t pid0, uint64_t seed, const gt_meal_gen*
   REQUIRE(n * n_meals == 0 || (start_s && end_s && carbs_g), "gt_generate_meals: null output");
   REQUIRE(gen->jitter_s >= 0 && gen->duration_s > 0, "gt_generate_meals: bad generator spec");
   return gt_launch_meals(n, pid0, seed, gen, n_meals, start_s, end_s, carbs_g, S(stream));
+}
+
+int gt_northern_protocol(const gt_northern_args* a, void* stream) {
+  REQUIRE(a && a->n >= 0, "gt_northern_protocol: bad arguments");
+  if (a->n == 0) return GT_OK;
+  REQUIRE(a->params && a->meal_ks && a->meal_ke && a->meal_kp && a->meal_rate && a->meal_ann &&
+          a->ex_ks && a->ex_ke && a->ex_start_s && a->ex_hrr && a->ex_announced,
+          "gt_northern_protocol: null output pointer");
+  REQUIRE(a->dt_s > 0 && a->period_s > 0, "gt_northern_protocol: bad time step");
+  return gt_launch_northern(a, S(stream));
 }
 
 }  // extern "C"

@@ -240,6 +240,41 @@ def launch_fast(inputs: dict, outs: FastOutputs, sz: dict, dt_s: float, period_s
     check(_lib.load().gt_simulate_fast(C.byref(a), stream_ptr(device)), "gt_simulate_fast")
 
 
+def northern_csr(params, pid0: int, trial_seed: int, dt_s: float, period_s: float, horizon_s: float,
+                 device, week_days: bool = False) -> dict:
+    """Device NorthernYearProtocol in the fused kernel's CSR layout (fixed
+    stride GT_NY_MEALS / GT_NY_EX per patient; see include/glucosim.h).
+    Returns the CSR dict of FastTrial plus ``n_meals`` / ``n_ex`` (events
+    before the horizon) and optionally ``week_days`` [52, n] uint16."""
+    from ._lib import GT_NY_EX, GT_NY_MEALS, NorthernArgs
+    t = torch()
+    n = int(params.shape[0])
+    i32, f64 = t.int32, t.float64
+    out = {
+        "meal_ks": empty((n * GT_NY_MEALS,), i32, device), "meal_ke": empty((n * GT_NY_MEALS,), i32, device),
+        "meal_kp": empty((n * GT_NY_MEALS,), i32, device), "meal_rate": empty((n * GT_NY_MEALS,), f64, device),
+        "meal_ann": empty((n * GT_NY_MEALS,), f64, device),
+        "ex_ks": empty((n * GT_NY_EX,), i32, device), "ex_ke": empty((n * GT_NY_EX,), i32, device),
+        "ex_start_s": empty((n * GT_NY_EX,), f64, device), "ex_hrr": empty((n * GT_NY_EX,), f64, device),
+        "ex_announced": empty((n * GT_NY_EX,), f64, device),
+        "n_meals": empty((n,), i32, device), "n_ex": empty((n,), i32, device),
+        "meal_off": t.arange(n + 1, dtype=t.int64, device=device) * GT_NY_MEALS,
+        "ex_off": t.arange(n + 1, dtype=t.int64, device=device) * GT_NY_EX,
+    }
+    if week_days:
+        out["week_days"] = empty((52, n), t.int16, device)
+    a = NorthernArgs()
+    a.n, a.pid0, a.trial_seed = n, int(pid0), int(trial_seed) & 0xFFFFFFFFFFFFFFFF
+    a.dt_s, a.period_s, a.horizon_s = float(dt_s), float(period_s), float(horizon_s)
+    a.params = ptr(params.contiguous())
+    for k in ("meal_ks", "meal_ke", "meal_kp", "meal_rate", "meal_ann", "ex_ks", "ex_ke", "ex_start_s",
+              "ex_hrr", "ex_announced", "n_meals", "n_ex"):
+        setattr(a, k, ptr(out[k]))
+    a.week_days = ptr(out.get("week_days"))
+    check(_lib.load().gt_northern_protocol(C.byref(a), stream_ptr(device)), "gt_northern_protocol")
+    return out
+
+
 FIXED_PARAM_INDEX = tuple(range(15, 30))   # AG .. R: the table's fixed block (hovorka.py:53-55)
 
 

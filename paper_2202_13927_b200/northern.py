@@ -84,6 +84,26 @@ def _plan_week(week_type, g):
     raise ValueError(f"could not order week {week_type!r}")
 
 
+def plan_year_twin(seed: int):
+    """plan_year through the integer restatement of numpy's stream
+    (rng.NumpyPhiloxTwin) -- the algorithm csrc/gt_northern.cu runs."""
+    g = rng.NumpyPhiloxTwin(seed, (0,))
+    weeks, days = [], []
+    for season in SEASON_NAMES:
+        counts = SEASON_COMPOSITIONS[season]
+        wk = [w for w in WEEK_TYPES for _ in range(counts.get(w, 0))]
+        g.shuffle(wk)
+        for w in wk:
+            weeks.append(w)
+            days.append(_plan_week(w, g))
+    return weeks, days
+
+
+def week_day_codes(days) -> list:
+    """2-bit day-type codes per week (the device builder's week_days)."""
+    return [sum(DAY_TYPES.index(d) << (2 * i) for i, d in enumerate(wk)) for wk in days]
+
+
 def plan_year(seed: int):
     g = rng.stream(seed, 0)
     weeks, days = [], []
@@ -152,6 +172,13 @@ class NorthernYearProtocol:
             proto = apply_announcement_policy(proto, pol, rng.stream(trial_seed, patient.id,
                                                                      rng.ROLE_ANNOUNCEMENT))
         return proto
+
+    def on_device(self) -> bool:
+        """The device builder (csrc/gt_northern.cu) covers the default
+        announcement policy and the bundled basis days."""
+        pol = self.announcement
+        return (self.basis_days_path is None and pol.fraction_unannounced == 0.0
+                and tuple(pol.misannouncement_factor_range) == (1.0, 1.0))
 
     def describe(self) -> dict:
         return {"kind": "northern_year",

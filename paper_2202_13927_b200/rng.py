@@ -170,3 +170,133 @@ def u52(a: np.ndarray, b: np.ndarray) -> np.ndarray:
     """Open-interval uniform from two uint32 words (device: u52 / gen_meal)."""
     k = ((a.astype(np.uint64) >> np.uint64(6)) << np.uint64(26)) | (b.astype(np.uint64) >> np.uint64(6))
     return (2 * k + 1).astype(np.float64) * 1.1102230246251565404e-16
+
+
+# ------------------------------------------------- numpy stream restatement
+# The device NorthernYear planner (csrc/gt_northern.cu) draws from the
+# reference's own keyed streams, so it restates numpy's SeedSequence,
+# Philox4x64-10 bit generator and Generator.shuffle bit for bit.  These
+# pure-integer twins are that restatement on the host (checked against numpy
+# in tests/test_northern.py).
+_M32 = 0xFFFFFFFF
+_M64 = 0xFFFFFFFFFFFFFFFF
+
+
+def _u32_words(v: int) -> list:
+    """numpy _int_to_uint32_array: little-endian 32-bit words, [0] for 0."""
+    if v < 0:
+        raise ValueError("negative entropy")
+    if v == 0:
+        return [0]
+    out = []
+    while v > 0:
+        out.append(v & _M32)
+        v >>= 32
+    return out
+
+
+def seed_sequence_state(entropy: int, spawn_key: tuple, n_words32: int) -> list:
+    """SeedSequence(entropy, spawn_key).generate_state(n_words32, uint32),
+    pool size 4 (numpy/random/bit_generator.pyx)."""
+    run = _u32_words(entropy)
+    spawn = [w for k in spawn_key for w in _u32_words(int(k))]
+    if spawn and len(run) < 4:
+        run = run + [0] * (4 - len(run))
+    ent = run + spawn
+    hc = 0x43B0D7E5
+
+    def hashmix(v):
+        nonlocal hc
+        v = (v ^ hc) & _M32
+        hc = (hc * 0x931E8875) & _M32
+        v = (v * hc) & _M32
+        return v ^ (v >> 16)
+
+    def mix(x, y):
+        r = (0xCA01F9DD * x - 0x4973F715 * y) & _M32
+        return r ^ (r >> 16)
+
+    pool = [hashmix(ent[i]) if i < len(ent) else hashmix(0) for i in range(4)]
+    for s in range(4):
+        for d in range(4):
+            if s != d:
+                pool[d] = mix(pool[d], hashmix(pool[s]))
+    for s in range(4, len(ent)):
+        for d in range(4):
+            pool[d] = mix(pool[d], hashmix(ent[s]))
+    hb = 0x8B51F9DD
+    out = []
+    for i in range(n_words32):
+        v = pool[i % 4] ^ hb
+        hb = (hb * 0x58F38DED) & _M32
+        v = (v * hb) & _M32
+        out.append(v ^ (v >> 16))
+    return out
+
+
+def derive_seed_twin(seed: int, *key: int) -> int:
+    w = seed_sequence_state(seed, key, 2)
+    return w[0] | (w[1] << 32)
+
+
+def philox4x64_10(ctr: list, key: list) -> list:
+    c, k0, k1 = list(ctr), key[0], key[1]
+    for _ in range(10):
+        p0 = 0xD2E7470EE14C6C93 * c[0]
+        p1 = 0xCA5A826395121157 * c[2]
+        c = [((p1 >> 64) ^ c[1] ^ k0) & _M64, p1 & _M64, ((p0 >> 64) ^ c[3] ^ k1) & _M64, p0 & _M64]
+        k0 = (k0 + 0x9E3779B97F4A7C15) & _M64
+        k1 = (k1 + 0xBB67AE8584CAA73B) & _M64
+    return c
+
+
+class NumpyPhiloxTwin:
+    """numpy.random.Philox(SeedSequence(entropy, spawn_key)) as used by
+    ``stream``: next_uint64 / next_uint32 (low half first) / random_interval."""
+
+    def __init__(self, entropy: int, spawn_key: tuple):
+        w = seed_sequence_state(entropy, spawn_key, 4)
+        self.key = [w[0] | (w[1] << 32), w[2] | (w[3] << 32)]
+        self.ctr = [0, 0, 0, 0]
+        self.buf, self.pos = [0] * 4, 4
+        self.has32, self.u32 = False, 0
+
+    def next_uint64(self) -> int:
+        if self.pos < 4:
+            self.pos += 1
+            return self.buf[self.pos - 1]
+        for i in range(4):   # 256-bit counter increment with carry
+            self.ctr[i] = (self.ctr[i] + 1) & _M64
+            if self.ctr[i]:
+                break
+        self.buf, self.pos = philox4x64_10(self.ctr, self.key), 1
+        return self.buf[0]
+
+    def next_uint32(self) -> int:
+        if self.has32:
+            self.has32 = False
+            return self.u32
+        v = self.next_uint64()
+        self.has32, self.u32 = True, v >> 32
+        return v & _M32
+
+    def random_interval(self, mx: int) -> int:
+        if mx == 0:
+            return 0
+        mask = mx
+        for s in (1, 2, 4, 8, 16, 32):
+            mask |= mask >> s
+        if mx <= _M32:
+            while True:
+                v = self.next_uint32() & mask
+                if v <= mx:
+                    return v
+        while True:
+            v = self.next_uint64() & mask
+            if v <= mx:
+                return v
+
+    def shuffle(self, x: list) -> None:
+        for i in range(len(x) - 1, 0, -1):
+            j = self.random_interval(i)
+            x[i], x[j] = x[j], x[i]

@@ -91,6 +91,14 @@ class FastTrial:
     def _build_csr(self, generator):
         t = engine.torch()
         cfg = self.config
+        from .northern import NorthernYearProtocol
+        if isinstance(generator, NorthernYearProtocol) and generator.on_device():
+            # planned on the device from the reference's own keyed stream
+            csr = engine.northern_csr(self.params, self.pid0, cfg.seed, cfg.dt_s, cfg.controller_period_s,
+                                      cfg.horizon_s, self.device)
+            if bool((csr["n_meals"] < 0).any()):
+                raise SimulationError("NorthernYear week plan failed (no admissible day order)")
+            return csr
 
         class _P:  # minimal patient for generator.build
             def __init__(self, pid, w):
