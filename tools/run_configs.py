@@ -179,6 +179,33 @@ def c2(dev, scale):
             "quantiles": analytics.metric_quantiles(acc), "tir_report": rep.get("tir")}
 
 
+def c2n(dev, scale):
+    """C2 scale with the reference's own lifestyle protocol (NorthernYear,
+    planned on the device) instead of the BASELINE 3-meal generator."""
+    import torch
+    from paper_2202_13927_b200 import analytics
+    from paper_2202_13927_b200.config import SimulationConfig
+    from paper_2202_13927_b200.controller import ControllerHyperparameters
+    from paper_2202_13927_b200.northern import NorthernYearProtocol
+    from paper_2202_13927_b200.population import generate_population
+    from paper_2202_13927_b200.studies import _timed_step, _trial
+    n, weeks = int(1_000_000 * scale), 52
+    cfg = SimulationConfig(horizon_s=weeks * 7 * 86400.0, seed=2, dt_s=60.0)
+    pop = generate_population(2, n, device=dev, on_exhausted="redraw_weight")
+    _sync()
+    t0 = time.perf_counter()
+    ft = _trial(pop, ControllerHyperparameters(), cfg, dev, NorthernYearProtocol())
+    _sync()
+    setup_s = time.perf_counter() - t0
+    sim_ms, step_ms = _timed_step(ft)
+    acc = ft.accumulator()
+    return {"patients": n, "weeks": weeks, "protocol": "northern_year (device-planned)",
+            "setup_s_incl_protocol_build": setup_s, "sim_ms": sim_ms, "step_ms": step_ms,
+            "patient_weeks_per_s": n * weeks / (step_ms / 1000.0), "n_patients": acc.n_patients,
+            "n_aborted": acc.n_aborted, "peak_mem_gb": torch.cuda.max_memory_allocated(dev) / 1e9,
+            "quantiles": analytics.metric_quantiles(acc)}
+
+
 def c3(dev, scale):
     from paper_2202_13927_b200.studies import treatment_comparison
     return treatment_comparison(max(1000, int(250_000 * scale)), 12, seed=3, device=dev)
@@ -191,7 +218,7 @@ def c4(dev, scale):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="C0,C1,C2,C3,C4")
+    ap.add_argument("--only", default="C0,C1,C2,C2N,C3,C4")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "configs.json"))
     ap.add_argument("--scale", type=float, default=1.0)
     args = ap.parse_args()
@@ -200,7 +227,7 @@ def main():
     from paper_2202_13927_b200 import _lib
     _lib.load()
     out = {"device": torch.cuda.get_device_name(dev), "scale": args.scale}
-    fns = {"C0": c0, "C1": c1, "C2": c2, "C3": c3, "C4": c4}
+    fns = {"C0": c0, "C1": c1, "C2": c2, "C2N": c2n, "C3": c3, "C4": c4}
     for name in args.only.split(","):
         t0 = time.perf_counter()
         out[name] = fns[name](dev, args.scale)
