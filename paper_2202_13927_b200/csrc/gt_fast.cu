@@ -2,8 +2,8 @@
 //
 // One thread = one virtual patient.  SDE state, Philox counters and per-step
 // accumulators live in registers; the 247-bin BG histogram of each patient
-// lives in shared memory as uint8 counters (flushed into the patient's HBM
-// column every 254/period_steps periods), and the state that changes only on
+// lives in shared memory as uint8 counters (a counter that reaches 255 drains
+// into the patient's HBM column; all drain at the end of a slice), and the state that changes only on
 // controller ticks (controller memory, meal window, dose sums, BG extremes)
 // lives in shared memory, so HBM sees parameters in and metrics out only.
 //
@@ -242,8 +242,8 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
   __shared__ double s_hyper[GT_N_HYPER];
   __shared__ double s_hc[5];  // hyper-derived controller constants (same IEEE values)
   extern __shared__ uint32_t s_hist[];  // [kHistWords * kFastBS], dynamic (> 48 KB total)
-  __shared__ double s_d[N_SC][kFastBS];
-  __shared__ int32_t s_i[N_SI][kFastBS];
+  __shared__ double s_d[N_SC * kFastBS];   // [field][lane], flat
+  __shared__ int32_t s_i[N_SI * kFastBS];
   __shared__ gt_meal_gen s_gen;
   __shared__ uint16_t s_mk[3][3][kFastBS];  // THREE_MEAL day window: ks, ke, kp offsets
   __shared__ double s_mc[3][kFastBS];       // THREE_MEAL day window: carbs (g)
@@ -265,6 +265,8 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
   __syncthreads();  // no block-wide barrier after this point: warps run independently
 
   const int lane = tid & 31;
+  double* const sdl = s_d + tid;   // this lane's controller / extremes slots, field stride kFastBS
+  int32_t* const sil = s_i + tid;
   const int64_t n = a.n;
   const int64_t n_warps = sch.n_warps;
   const double* __restrict__ H = s_hyper;
@@ -352,15 +354,15 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       G = (R)x0[IGSC]; Z1 = (R)x0[IZ1]; Z2 = (R)x0[IZ2];
       if (HAS_EX) { E1 = (R)x0[IE1]; E2 = (R)x0[IE2]; E3 = (R)x0[IE3]; }
       const double* c0 = a.c0 + ii * NC;
-      s_d[SC_FILT][tid] = c0[CFILT]; s_d[SC_ICR][tid] = c0[CICR];
-      s_d[SC_SUSP][tid] = c0[CSUSPEND_UNTIL]; s_d[SC_LASTG][tid] = c0[CLASTGLUC];
-      s_d[SC_WEND][tid] = c0[CWINEND]; s_d[SC_WPEAK][tid] = c0[CWINPEAK]; s_d[SC_WMIN][tid] = c0[CWINMIN];
-      s_i[SI_FLAGS][tid] = (c0[CMODE] != 0.0) | ((c0[CEXBOLUSDONE] != 0.0) << 1) | ((c0[CINIT] != 0.0) << 2);
-      s_d[SC_ASSUMED][tid] = a.assumed_basal[ii];
-      s_d[SC_BGMIN][tid] = INFINITY;
-      s_d[SC_BGMAX][tid] = -INFINITY;
-      s_d[SC_DBOLUS][tid] = 0.0;
-      s_d[SC_DGLUC][tid] = 0.0;
+      sdl[(SC_FILT) * kFastBS] = c0[CFILT]; sdl[(SC_ICR) * kFastBS] = c0[CICR];
+      sdl[(SC_SUSP) * kFastBS] = c0[CSUSPEND_UNTIL]; sdl[(SC_LASTG) * kFastBS] = c0[CLASTGLUC];
+      sdl[(SC_WEND) * kFastBS] = c0[CWINEND]; sdl[(SC_WPEAK) * kFastBS] = c0[CWINPEAK]; sdl[(SC_WMIN) * kFastBS] = c0[CWINMIN];
+      sil[(SI_FLAGS) * kFastBS] = (c0[CMODE] != 0.0) | ((c0[CEXBOLUSDONE] != 0.0) << 1) | ((c0[CINIT] != 0.0) << 2);
+      sdl[(SC_ASSUMED) * kFastBS] = a.assumed_basal[ii];
+      sdl[(SC_BGMIN) * kFastBS] = INFINITY;
+      sdl[(SC_BGMAX) * kFastBS] = -INFINITY;
+      sdl[(SC_DBOLUS) * kFastBS] = 0.0;
+      sdl[(SC_DGLUC) * kFastBS] = 0.0;
       bg_sum = 0.0; day_basal = 0.0; hu_ins = 0; hu2 = 0;
       kb_min = INT_MAX; kb_max = -1; run39 = run30 = ev39 = ev30 = 0;
       m_ks = m_ke = INT_MAX; gin = 0;
@@ -368,11 +370,11 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         const MealT m0 = meal_at(0);
         m_ks = m0.ks; m_ke = m0.ke; gin = (R)(u.ginK * m0.rate);
         if (TRACE) tr_rate = m0.rate;
-        s_i[SI_MEALM][tid] = 0;
-        s_i[SI_ANNM][tid] = 0;
-        s_i[SI_ANNKP][tid] = m0.kp;
-        s_d[SC_ANNCARBS][tid] = m0.carbs;
-        s_i[SI_EXPTR][tid] = 0;
+        sil[(SI_MEALM) * kFastBS] = 0;
+        sil[(SI_ANNM) * kFastBS] = 0;
+        sil[(SI_ANNKP) * kFastBS] = m0.kp;
+        sdl[(SC_ANNCARBS) * kFastBS] = m0.carbs;
+        sil[(SI_EXPTR) * kFastBS] = 0;
       }
       if (inrange)
         for (int b = 0; b < GT_N_BG_BINS; ++b) a.bg_hist[(int64_t)b * n + i] = 0;
@@ -387,8 +389,8 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       if (HAS_EX) { E1 = (R)LDD(SD_E1); E2 = (R)LDD(SD_E2); E3 = (R)LDD(SD_E3); }
       bg_sum = LDD(SD_BGSUM); day_basal = LDD(SD_DAYBASAL);
       hu_ins = (R)LDD(SD_HUINS); hu2 = (R)LDD(SD_HU2); gin = (R)LDD(SD_GIN);
-      for (int q = 0; q < N_SC; ++q) s_d[q][tid] = LDD(SD_SC0 + q);
-      for (int q = 0; q < N_SI; ++q) s_i[q][tid] = LDI(SV_SI0 + q);
+      for (int q = 0; q < N_SC; ++q) sdl[(q) * kFastBS] = LDD(SD_SC0 + q);
+      for (int q = 0; q < N_SI; ++q) sil[(q) * kFastBS] = LDI(SV_SI0 + q);
       if (PROTO == GT_PROTO_THREE_MEAL) {
         for (int j = 0; j < 3; ++j) {
           s_mc[j][tid] = LDD(SD_MC0 + j);
@@ -428,7 +430,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         s_mk[2][j][tid] = ok ? (uint16_t)(mt.kp - day_ctl0) : (uint16_t)0xFFFF;
         s_mc[j][tid] = mt.carbs;
       }
-      s_i[SI_MEALM][tid] = 0;
+      sil[(SI_MEALM) * kFastBS] = 0;
       load_slot(0);
     };
     // flush the lane's uint8 histogram into its HBM column (bins 0..246;
@@ -455,8 +457,6 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
     int g_idx = next_grid_ctl / u.grid_ctl;
     int next_day_ctl = max(cpd, ((ctl_lo + cpd - 1) / cpd) * cpd);  // day flush (ctl > 0)
     int next_gen_ctl = ((ctl_lo + cpd - 1) / cpd) * cpd;             // day window generation
-    const int flush_every = max(1, 254 / ps);   // periods until a uint8 bin could reach 255
-    int next_flush_ctl = ctl_lo + flush_every;
 
     // ---------------------------------------------------------- one step
     auto step = [&](const int32_t k, const bool tick, const int32_t ctl, const int32_t sk) {
@@ -503,8 +503,8 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       // disturbances at tick k (_kernel.py:85-94)
       if (PROTO == GT_PROTO_CSR) {
         while (k >= m_ke) {
-          const int32_t m = s_i[SI_MEALM][tid] + 1;
-          s_i[SI_MEALM][tid] = m;
+          const int32_t m = sil[(SI_MEALM) * kFastBS] + 1;
+          sil[(SI_MEALM) * kFastBS] = m;
           const MealT mt = meal_at(m);
           m_ks = mt.ks; m_ke = mt.ke; gin = (R)(u.ginK * mt.rate);
           if (TRACE) tr_rate = mt.rate;
@@ -513,7 +513,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         // generated meals are >= one period apart, so the active window of
         // the current meal within this period [act_lo, act_hi) is fixed here
         while (m_ke <= k) {
-          const int j = ++s_i[SI_MEALM][tid];
+          const int j = ++sil[(SI_MEALM) * kFastBS];
           if (j < 3) load_slot(j);
           else { m_ks = m_ke = INT_MAX; gin = 0; }
         }
@@ -526,9 +526,9 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       bool ex_active = false;
       int ex_ptr = 0;
       if (HAS_EX) {
-        ex_ptr = s_i[SI_EXPTR][tid];
+        ex_ptr = sil[(SI_EXPTR) * kFastBS];
         while (ex_ptr < n_ex && k >= a.ex_ke[ex_lo + ex_ptr]) ++ex_ptr;
-        s_i[SI_EXPTR][tid] = ex_ptr;
+        sil[(SI_EXPTR) * kFastBS] = ex_ptr;
         ex_active = ex_ptr < n_ex && k >= a.ex_ks[ex_lo + ex_ptr];
         hrr = ex_active ? a.ex_hrr[ex_lo + ex_ptr] : 0.0;
       }
@@ -553,17 +553,17 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           for (int j = 0; j < 3; ++j)
             announced = A_(announced, s_mk[2][j][tid] == rel ? s_mc[j][tid] : 0.0);
         }
-        int32_t akp = PROTO == GT_PROTO_CSR ? s_i[SI_ANNKP][tid] : INT_MAX;
+        int32_t akp = PROTO == GT_PROTO_CSR ? sil[(SI_ANNKP) * kFastBS] : INT_MAX;
         if (akp <= ctl) {
-          int32_t am = s_i[SI_ANNM][tid];
-          double carbs = s_d[SC_ANNCARBS][tid];
+          int32_t am = sil[(SI_ANNM) * kFastBS];
+          double carbs = sdl[(SC_ANNCARBS) * kFastBS];
           while (akp <= ctl) {
             if (akp == ctl) announced += carbs;
             ++am;
             const MealT mt = meal_at(am);
             akp = mt.kp; carbs = mt.carbs;
           }
-          s_i[SI_ANNM][tid] = am; s_i[SI_ANNKP][tid] = akp; s_d[SC_ANNCARBS][tid] = carbs;
+          sil[(SI_ANNM) * kFastBS] = am; sil[(SI_ANNKP) * kFastBS] = akp; sdl[(SC_ANNCARBS) * kFastBS] = carbs;
         }
         double phase = -1.0;
         if (HAS_EX && ex_active && a.ex_announced[ex_lo + ex_ptr] != 0.0)
@@ -573,11 +573,11 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         // ---- controller_step_vec (controller.py:343-458); state in shared
         // memory.  Explicit IEEE operations in the reference's order: the
         // controller is bit-identical to the reference's for identical readings.
-        int flags = s_i[SI_FLAGS][tid];
-        double filt = s_d[SC_FILT][tid], prev;
+        int flags = sil[(SI_FLAGS) * kFastBS];
+        double filt = sdl[(SC_FILT) * kFastBS], prev;
         if (!(flags & 4)) { filt = y; prev = y; flags |= 4; }
         else { prev = filt; filt = A_(M_(s_hc[1], filt), M_(H[HFILTER], y)); }
-        s_d[SC_FILT][tid] = filt;
+        sdl[(SC_FILT) * kFastBS] = filt;
         const double trend = S_(filt, prev);
         const bool exercising = HAS_EX && phase >= 0.0;
         const double setpoint = exercising ? H[HEXSETPOINT] : H[HSETPOINT];
@@ -590,7 +590,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
             flags |= 2;
             if (filt < H[HEXBOLUSBG]) {
               b_gluc = fmin(H[HEXBOLUS], H[HMAXGLUC]);
-              s_d[SC_LASTG][tid] = t_s;
+              sdl[(SC_LASTG) * kFastBS] = t_s;
               done = true;
             }
           }
@@ -604,42 +604,42 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           } else {
             if (filt >= (exercising ? s_hc[4] : s_hc[3]) && pred >= gluc_thr) flags &= ~1;
           }
-          const double wend = s_d[SC_WEND][tid];
+          const double wend = sdl[(SC_WEND) * kFastBS];
           if (wend > 0.0) {
-            const double wpeak = fmax(s_d[SC_WPEAK][tid], filt);
-            const double wmin = fmin(s_d[SC_WMIN][tid], filt);
-            s_d[SC_WPEAK][tid] = wpeak; s_d[SC_WMIN][tid] = wmin;
+            const double wpeak = fmax(sdl[(SC_WPEAK) * kFastBS], filt);
+            const double wmin = fmin(sdl[(SC_WMIN) * kFastBS], filt);
+            sdl[(SC_WPEAK) * kFastBS] = wpeak; sdl[(SC_WMIN) * kFastBS] = wmin;
             if (t_s >= wend) {
-              double icr = s_d[SC_ICR][tid];
+              double icr = sdl[(SC_ICR) * kFastBS];
               if (wmin < H[HUNDERBG]) icr = M_(icr, A_(1.0, H[HICRSTEPUP]));
               else if (S_(wpeak, H[HSETPOINT]) > H[HEXCHI]) icr = M_(icr, S_(1.0, H[HICRSTEP]));
               if (icr < H[HICRMIN]) icr = H[HICRMIN];
               if (icr > H[HICRMAX]) icr = H[HICRMAX];
-              s_d[SC_ICR][tid] = icr;
-              s_d[SC_WEND][tid] = 0.0;
+              sdl[(SC_ICR) * kFastBS] = icr;
+              sdl[(SC_WEND) * kFastBS] = 0.0;
             }
           }
           if (flags & 1) {
-            if (filt < gluc_thr && trend < -H[HMICROTREND] && S_(t_s, s_d[SC_LASTG][tid]) >= s_hc[2]) {
+            if (filt < gluc_thr && trend < -H[HMICROTREND] && S_(t_s, sdl[(SC_LASTG) * kFastBS]) >= s_hc[2]) {
               if (micro > H[HMAXGLUC]) micro = H[HMAXGLUC];
               b_gluc = micro;
-              s_d[SC_LASTG][tid] = t_s;
+              sdl[(SC_LASTG) * kFastBS] = t_s;
             }
           } else {
-            const double assumed = s_d[SC_ASSUMED][tid];
+            const double assumed = sdl[(SC_ASSUMED) * kFastBS];
             if (announced > 0.0) {
-              const double icr = s_d[SC_ICR][tid];
+              const double icr = sdl[(SC_ICR) * kFastBS];
               double b = A_(D_(announced, icr), D_(S_(filt, setpoint), M_(H[HCFICR], icr)));
               if (filt > H[HSUPBG]) b = A_(b, D_(M_(M_(H[HSUPFRAC], assumed), H[HSUSPMIN]), 60.0));
               if (b < 0.0) b = 0.0;
               if (b > H[HMAXBOLUS]) b = H[HMAXBOLUS];
               b_bolus = b;
-              s_d[SC_SUSP][tid] = A_(t_s, M_(H[HSUSPMIN], 60.0));
-              s_d[SC_WEND][tid] = A_(t_s, M_(H[HMEALWIN], 60.0));
-              s_d[SC_WPEAK][tid] = filt;
-              s_d[SC_WMIN][tid] = filt;
+              sdl[(SC_SUSP) * kFastBS] = A_(t_s, M_(H[HSUSPMIN], 60.0));
+              sdl[(SC_WEND) * kFastBS] = A_(t_s, M_(H[HMEALWIN], 60.0));
+              sdl[(SC_WPEAK) * kFastBS] = filt;
+              sdl[(SC_WMIN) * kFastBS] = filt;
             }
-            if (!(t_s < s_d[SC_SUSP][tid])) {
+            if (!(t_s < sdl[(SC_SUSP) * kFastBS])) {
               double factor = A_(A_(1.0, M_(H[HBKP], S_(filt, setpoint))), M_(H[HBKD], trend));
               if (factor < 0.0) factor = 0.0;
               if (factor > H[HBFMAX]) factor = H[HBFMAX];
@@ -649,14 +649,14 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
             }
           }
         }
-        s_i[SI_FLAGS][tid] = flags;
+        sil[(SI_FLAGS) * kFastBS] = flags;
         day_basal = fma(b_basal, (double)ps, day_basal);  // basal held for the whole period
         if (TRACE) { tr_basal = b_basal; tr_bolus = b_bolus; tr_gluc = b_gluc; }
         hu_ins = (R)fma(b_bolus, u.u_bolus_k, b_basal * u.u_basal_k);   // h * (u[0] + u[1])
         hu2 = (R)(b_gluc * u.u_gluc_k);                                 // h * u[2]
         if (b_bolus > 0.0 || b_gluc > 0.0) {
-          s_d[SC_DBOLUS][tid] += b_bolus;
-          s_d[SC_DGLUC][tid] += b_gluc;
+          sdl[(SC_DBOLUS) * kFastBS] += b_bolus;
+          sdl[(SC_DGLUC) * kFastBS] += b_gluc;
         }
       }
       // statistics at tick k (_kernel.py:137-160)
@@ -686,17 +686,22 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           kb += (s_thr[kb + 1] <= bb) - (s_thr[kb] > bb);
         }
         kb = alive ? kb : GT_N_BG_BINS;  // dead lanes count into the padding bin 247
-        {  // byte ((kb >> 2) * kFastBS + tid) * 4 + (kb & 3); < 255 between flushes
+        {  // byte ((kb >> 2) * kFastBS + tid) * 4 + (kb & 3)
           const uint32_t ha = hist_lane + ((uint32_t)(kb & ~3) << 7) + (uint32_t)(kb & 3);
-          asm volatile("{\n\t.reg .u32 c;\n\tld.shared.u8 c, [%0];\n\tadd.u32 c, c, 1;\n\t"
-                       "st.shared.u8 [%0], c;\n\t}" :: "r"(ha));
+          uint32_t c;
+          asm volatile("{\n\t.reg .u32 t;\n\tld.shared.u8 t, [%1];\n\tadd.u32 %0, t, 1;\n\t"
+                       "st.shared.u8 [%1], %0;\n\t}" : "=r"(c) : "r"(ha));
+          if (__builtin_expect(c == 255u, 0)) {  // a full counter drains into the HBM column
+            if (kb < GT_N_BG_BINS && inrange) atomicAdd(&a.bg_hist[(int64_t)kb * n + i], 255);
+            asm volatile("st.shared.u8 [%0], 0;" :: "r"(ha));
+          }
         }
         bg_sum += bg;
         // extremes: only a tick in the lowest/highest bin so far can move them;
         // hypo runs: only ticks below 3.9 mmol/L (or ending such a run) matter
         if (__builtin_expect(kb <= trig_lo || kb >= kb_max, 0) && alive) {
-          if (kb <= kb_min) { const double o = s_d[SC_BGMIN][tid]; s_d[SC_BGMIN][tid] = bg < o ? bg : o; kb_min = kb; }
-          if (kb >= kb_max) { const double o = s_d[SC_BGMAX][tid]; s_d[SC_BGMAX][tid] = bg > o ? bg : o; kb_max = kb; }
+          if (kb <= kb_min) { const double o = sdl[(SC_BGMIN) * kFastBS]; sdl[(SC_BGMIN) * kFastBS] = bg < o ? bg : o; kb_min = kb; }
+          if (kb >= kb_max) { const double o = sdl[(SC_BGMAX) * kFastBS]; sdl[(SC_BGMAX) * kFastBS] = bg > o ? bg : o; kb_max = kb; }
           run39 = kb <= 34 ? run39 + 1 : 0;  // bg < 3.9 (THRESHOLDS[34])
           run30 = kb <= 25 ? run30 + 1 : 0;  // bg < 3.0 (THRESHOLDS[25])
           ev39 += run39 == u.hypoL;
@@ -772,16 +777,15 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
     // ------------------------------------------------- the slice's periods
     int ctl = ctl_lo;
     for (; ctl < ctl_hi; ++ctl) {
-      if (ctl == next_flush_ctl) { next_flush_ctl += flush_every; flush_hist(); }
       // day boundary: flush the finished day's dose sums (_kernel.py:133-149)
       if (ctl == next_day_ctl) {
         next_day_ctl += cpd;
         const int64_t day = ctl / cpd - 1;
         if (inrange) {
           double* dd = a.day_dose + (day * 3) * n + i;
-          dd[0] = day_basal; dd[n] = s_d[SC_DBOLUS][tid]; dd[2 * n] = s_d[SC_DGLUC][tid];
+          dd[0] = day_basal; dd[n] = sdl[(SC_DBOLUS) * kFastBS]; dd[2 * n] = sdl[(SC_DGLUC) * kFastBS];
         }
-        day_basal = 0.0; s_d[SC_DBOLUS][tid] = 0.0; s_d[SC_DGLUC][tid] = 0.0;
+        day_basal = 0.0; sdl[(SC_DBOLUS) * kFastBS] = 0.0; sdl[(SC_DGLUC) * kFastBS] = 0.0;
       }
       if (PROTO == GT_PROTO_THREE_MEAL && ctl == next_gen_ctl) {
         next_gen_ctl += cpd;
@@ -817,8 +821,8 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         if (HAS_EX) { STD(SD_E1, E1); STD(SD_E2, E2); STD(SD_E3, E3); }
         STD(SD_BGSUM, bg_sum); STD(SD_DAYBASAL, day_basal); STD(SD_HUINS, hu_ins);
         STD(SD_HU2, hu2); STD(SD_GIN, gin);
-        for (int q = 0; q < N_SC; ++q) STD(SD_SC0 + q, s_d[q][tid]);
-        for (int q = 0; q < N_SI; ++q) STI(SV_SI0 + q, s_i[q][tid]);
+        for (int q = 0; q < N_SC; ++q) STD(SD_SC0 + q, sdl[(q) * kFastBS]);
+        for (int q = 0; q < N_SI; ++q) STI(SV_SI0 + q, sil[(q) * kFastBS]);
         if (PROTO == GT_PROTO_THREE_MEAL) {
           for (int j = 0; j < 3; ++j) {
             STD(SD_MC0 + j, s_mc[j][tid]);
@@ -836,11 +840,11 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       // ---- final outputs
       const int64_t last_day = a.n_days - 1;
       double* dd = a.day_dose + (last_day * 3) * n + i;
-      dd[0] = day_basal; dd[n] = s_d[SC_DBOLUS][tid]; dd[2 * n] = s_d[SC_DGLUC][tid];
+      dd[0] = day_basal; dd[n] = sdl[(SC_DBOLUS) * kFastBS]; dd[2 * n] = sdl[(SC_DGLUC) * kFastBS];
       a.status[i] = status;
       a.ticks[i] = status == GT_STATUS_OK ? a.horizon_ticks : (death_tick < 0 ? 0 : death_tick);
-      a.bg_stats[i] = s_d[SC_BGMIN][tid];
-      a.bg_stats[n + i] = s_d[SC_BGMAX][tid];
+      a.bg_stats[i] = sdl[(SC_BGMIN) * kFastBS];
+      a.bg_stats[n + i] = sdl[(SC_BGMAX) * kFastBS];
       a.bg_stats[2 * n + i] = bg_sum;
       a.hypo_events[i] = ev39;
       a.hypo_events[n + i] = ev30;
