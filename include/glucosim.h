@@ -56,6 +56,7 @@ extern "C" {
 
 /* controllers (device registry; mirrors controller.py:506-527) */
 #define GT_CTRL_DUAL_HORMONE 0
+#define GT_CTRL_PID_PUMP 1      /* PID basal + pump quantisation (pid.py; BASELINE's controller) */
 
 /* ------------------------------------------------------------------ info */
 int gt_abi_version(void);
@@ -117,6 +118,8 @@ typedef struct gt_parity_args {
     double *x_out;      /* [n][16] or NULL */
     double *c_out;      /* [n][11] or NULL */
     double *trace;      /* [n][horizon][8] or NULL (simulation.py:61-64) */
+    int32_t controller; /* GT_CTRL_* (hyper/c0 in that controller's layout) */
+    int32_t pad;
 } gt_parity_args;
 int gt_simulate_parity(const gt_parity_args *a, void *stream);
 

@@ -209,6 +209,54 @@ void oracle_controller_step(double *c, double y, double announced_cho_g,
 /* CPython / numba float floor division (Objects/floatobject.c float_divmod;
  * numba/cpython/numbers.py real_divmod) as used by `t // 86400.0`
  * (_kernel.py:133, :148) and `day_totals // width` (analytics.py:256). */
+/* ------------------------------------------------------------------------ */
+/* PID + pump quantisation (paper_2202_13927_b200/pid.py pid_step_vec): the  */
+/* BASELINE controller, a plug-in the reference runs through _python_block.  */
+/* Restated operation by operation; same state-vector layout.                */
+void oracle_pid_step(double *c, double y, double announced_cho_g, double exercise_phase_s,
+                     double t_s, double period_s, const double *hyper, double assumed_basal_uh,
+                     double *out)
+{
+    (void)exercise_phase_s; (void)t_s;
+    const double a = hyper[0];
+    if (c[CINIT] == 0.0) {
+        c[CFILT] = y; c[CPREV] = y; c[CINIT] = 1.0;
+    } else {
+        c[CPREV] = c[CFILT];
+        c[CFILT] = (1.0 - a) * c[CFILT] + a * y;
+    }
+    const double filt = c[CFILT];
+    const double e = filt - hyper[1];
+    const double trend = filt - c[CPREV];
+    const double ph = period_s / 3600.0;
+    double integ = c[CWINEND] + e * ph;
+    const double imax = hyper[6];
+    if (integ > imax) integ = imax;
+    if (integ < -imax) integ = -imax;
+    c[CWINEND] = integ;
+    double factor = 1.0 + hyper[2] * e + hyper[3] * integ + hyper[4] * trend;
+    if (factor < 0.0) factor = 0.0;
+    if (factor > hyper[5]) factor = hyper[5];
+    const double vol = assumed_basal_uh * factor * ph + c[CSUSPEND_UNTIL];
+    const double q = hyper[7];
+    double pulses = floor(vol / q);
+    if (pulses < 0.0) pulses = 0.0;
+    const double delivered = pulses * q;
+    c[CSUSPEND_UNTIL] = vol - delivered;
+    out[0] = delivered / ph;
+    out[1] = 0.0;
+    if (announced_cho_g > 0.0) {
+        double b = announced_cho_g / c[CICR];
+        if (b > hyper[9]) b = hyper[9];
+        out[1] = floor(b / hyper[8]) * hyper[8];
+    }
+    out[2] = 0.0;
+}
+
+/* controller selected for oracle_simulate_block: 0 dual_hormone, 1 pid_pump */
+static int g_controller = 0;
+void oracle_set_controller(int code) { g_controller = code; }
+
 double oracle_py_floordiv(double vx, double wx)
 {
     double mod = fmod(vx, wx);
@@ -302,8 +350,11 @@ int oracle_simulate_block(
             double y = x[IGSC] + sqrt_r * meas_norm[tick_idx];
             tick_idx++;
             scal[SCAL_LAST_Y] = y;
-            oracle_controller_step(c, y, announced, phase, t, period_s, hyper,
-                                   assumed_basal_uh, dec);
+            if (g_controller == 1)
+                oracle_pid_step(c, y, announced, phase, t, period_s, hyper, assumed_basal_uh, dec);
+            else
+                oracle_controller_step(c, y, announced, phase, t, period_s, hyper,
+                                       assumed_basal_uh, dec);
             basal_uh = dec[0]; bolus_u = dec[1]; glucagon_ug = dec[2];
             u[0] = basal_uh * 1000.0 / 60.0;
             u[1] = bolus_u * 1000.0 / (period_s / 60.0);

@@ -24,6 +24,7 @@ GT_PROTO_THREE_MEAL = 1
 GT_NOISE_INJECTED = 0
 GT_NOISE_PHILOX = 1
 GT_CTRL_DUAL_HORMONE = 0
+GT_CTRL_PID_PUMP = 1
 
 P = C.c_void_p
 I64 = C.c_int64
@@ -51,6 +52,7 @@ class ParityArgs(C.Structure):
         ("wiener", P), ("has_noise", P), ("meas", P),
         ("status", P), ("ticks", P), ("tir_ticks", P), ("bg_hist", P), ("scal", P),
         ("day_dose", P), ("timeline", P), ("x_out", P), ("c_out", P), ("trace", P),
+        ("controller", I32), ("pad", I32),
     ]
 
 

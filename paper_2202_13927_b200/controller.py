@@ -21,7 +21,7 @@ import numpy as np
 import yaml
 
 from . import layout
-from ._lib import GT_CTRL_DUAL_HORMONE
+from ._lib import GT_CTRL_DUAL_HORMONE, GT_CTRL_PID_PUMP
 
 
 class ProfileError(ValueError):
@@ -172,3 +172,4 @@ def get_controller_factory(controller_id: str):
 
 
 register_controller("dual_hormone", GT_CTRL_DUAL_HORMONE)
+register_controller("pid_pump", GT_CTRL_PID_PUMP)   # pid.py: PIDProfile / PIDController

@@ -117,6 +117,8 @@ int gt_simulate_parity(const gt_parity_args* a, void* stream) {
               a->ex_off && a->wiener && a->has_noise && a->meas && a->status && a->ticks &&
               a->tir_ticks && a->bg_hist && a->scal && a->day_dose && a->timeline,
           "gt_simulate_parity: null required pointer");
+  REQUIRE(a->controller == GT_CTRL_DUAL_HORMONE || a->controller == GT_CTRL_PID_PUMP,
+          "gt_simulate_parity: unknown controller %d", a->controller);
   return gt_launch_parity(a, S(stream));
 }
 
@@ -143,8 +145,8 @@ int gt_simulate_fast(const gt_fast_args* a, void* stream) {
   REQUIRE(a->params && a->x0 && a->c0 && a->hyper && a->assumed_basal && a->status && a->ticks &&
               a->bg_hist && a->bg_stats && a->day_dose && a->hypo_events && a->timeline_warp,
           "gt_simulate_fast: null required pointer");
-  REQUIRE(a->controller == GT_CTRL_DUAL_HORMONE, "gt_simulate_fast: unknown controller %d",
-          a->controller);
+  REQUIRE(a->controller == GT_CTRL_DUAL_HORMONE || a->controller == GT_CTRL_PID_PUMP,
+          "gt_simulate_fast: unknown controller %d", a->controller);
   if (a->proto_kind == GT_PROTO_CSR)
     REQUIRE(a->meal_off && a->meal_ks && a->meal_ke && a->meal_kp && a->meal_rate &&
                 a->meal_ann && a->ex_off && a->ex_ks && a->ex_ke && a->ex_start_s && a->ex_hrr &&

@@ -579,11 +579,35 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         else { prev = filt; filt = A_(M_(s_hc[1], filt), M_(H[HFILTER], y)); }
         sdl[(SC_FILT) * kFastBS] = filt;
         const double trend = S_(filt, prev);
+        double b_basal = 0.0, b_bolus = 0.0, b_gluc = 0.0;
+        if (a.controller == GT_CTRL_PID_PUMP) {
+          // ---- PID + pump quantisation (pid.py pid_step_vec), same filter;
+          // slots: SC_WEND = integral, SC_SUSP = pump carry
+          const double e = S_(filt, H[1]);
+          const double ph = D_(u.period, 3600.0);
+          double integ = A_(sdl[(SC_WEND) * kFastBS], M_(e, ph));
+          if (integ > H[6]) integ = H[6];
+          if (integ < -H[6]) integ = -H[6];
+          sdl[(SC_WEND) * kFastBS] = integ;
+          double factor = A_(A_(A_(1.0, M_(H[2], e)), M_(H[3], integ)), M_(H[4], trend));
+          if (factor < 0.0) factor = 0.0;
+          if (factor > H[5]) factor = H[5];
+          const double vol = A_(M_(M_(sdl[(SC_ASSUMED) * kFastBS], factor), ph), sdl[(SC_SUSP) * kFastBS]);
+          double pulses = floor(D_(vol, H[7]));
+          if (pulses < 0.0) pulses = 0.0;
+          const double delivered = M_(pulses, H[7]);
+          sdl[(SC_SUSP) * kFastBS] = S_(vol, delivered);
+          b_basal = D_(delivered, ph);
+          if (announced > 0.0) {
+            double bb = D_(announced, sdl[(SC_ICR) * kFastBS]);
+            if (bb > H[9]) bb = H[9];
+            b_bolus = M_(floor(D_(bb, H[8])), H[8]);
+          }
+        } else {
         const bool exercising = HAS_EX && phase >= 0.0;
         const double setpoint = exercising ? H[HEXSETPOINT] : H[HSETPOINT];
         const double gluc_thr = exercising ? H[HEXGLUCTHR] : H[HGLUCTHR];
         double micro = exercising ? H[HEXMICROUG] : H[HMICROUG];
-        double b_basal = 0.0, b_bolus = 0.0, b_gluc = 0.0;
         bool done = false;
         if (exercising) {
           if (!(flags & 2)) {
@@ -649,6 +673,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
             }
           }
         }
+        }  // dual_hormone
         sil[(SI_FLAGS) * kFastBS] = flags;
         day_basal = fma(b_basal, (double)ps, day_basal);  // basal held for the whole period
         if (TRACE) { tr_basal = b_basal; tr_bolus = b_bolus; tr_gluc = b_gluc; }

@@ -9,6 +9,45 @@
 namespace gt {
 
 // controller.py:343-458 controller_step_vec
+// PID + pump quantisation (pid.py pid_step_vec), operation by operation; this
+// translation unit is compiled without contraction.
+__device__ void pid_ref(double* c, double y, double announced_cho_g, double period_s,
+                        const double* hyper, double assumed_basal_uh, double* out) {
+  const double a = hyper[0];
+  if (c[CINIT] == 0.0) {
+    c[CFILT] = y; c[CPREV] = y; c[CINIT] = 1.0;
+  } else {
+    c[CPREV] = c[CFILT];
+    c[CFILT] = (1.0 - a) * c[CFILT] + a * y;
+  }
+  const double filt = c[CFILT];
+  const double e = filt - hyper[1];
+  const double trend = filt - c[CPREV];
+  const double ph = period_s / 3600.0;
+  double integ = c[CWINEND] + e * ph;
+  const double imax = hyper[6];
+  if (integ > imax) integ = imax;
+  if (integ < -imax) integ = -imax;
+  c[CWINEND] = integ;
+  double factor = 1.0 + hyper[2] * e + hyper[3] * integ + hyper[4] * trend;
+  if (factor < 0.0) factor = 0.0;
+  if (factor > hyper[5]) factor = hyper[5];
+  const double vol = assumed_basal_uh * factor * ph + c[CSUSPEND_UNTIL];
+  const double q = hyper[7];
+  double pulses = floor(vol / q);
+  if (pulses < 0.0) pulses = 0.0;
+  const double delivered = pulses * q;
+  c[CSUSPEND_UNTIL] = vol - delivered;
+  out[0] = delivered / ph;
+  out[1] = 0.0;
+  if (announced_cho_g > 0.0) {
+    double b = announced_cho_g / c[CICR];
+    if (b > hyper[9]) b = hyper[9];
+    out[1] = floor(b / hyper[8]) * hyper[8];
+  }
+  out[2] = 0.0;
+}
+
 __device__ void controller_ref(double* c, double y, double announced_cho_g, double phase,
                                double t_s, double period_s, const double* hyper,
                                double assumed_basal_uh, double* out) {
@@ -183,7 +222,10 @@ __global__ void parity_kernel(gt_parity_args a) {
         const double y = x[IGSC] + sqrt_r * meas[tick_idx];
         tick_idx++;
         scal[3] = y;
-        controller_ref(c, y, announced, phase, t, period_s, s_hyper, assumed, dec);
+        if (a.controller == GT_CTRL_PID_PUMP)
+          pid_ref(c, y, announced, period_s, s_hyper, assumed, dec);
+        else
+          controller_ref(c, y, announced, phase, t, period_s, s_hyper, assumed, dec);
         basal_uh = dec[0]; bolus_u = dec[1]; glucagon_ug = dec[2];
         u[0] = basal_uh * 1000.0 / 60.0;
         u[1] = bolus_u * 1000.0 / (period_s / 60.0);

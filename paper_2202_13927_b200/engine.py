@@ -102,6 +102,7 @@ class ParityBatch:
     has_noise: np.ndarray     # [n] uint8
     meas: np.ndarray          # [n,H/ps]
     active: np.ndarray | None = None
+    controller: int = 0       # GT_CTRL_*
 
 
 def run_parity(batch: ParityBatch, sz: dict, dt_s: float, period_s: float,
@@ -135,6 +136,7 @@ def run_parity(batch: ParityBatch, sz: dict, dt_s: float, period_s: float,
     a.n, a.dt_s, a.period_s = n, float(dt_s), float(period_s)
     a.period_steps, a.horizon_ticks, a.grid_step_ticks = sz["period_steps"], H, sz["grid_step_ticks"]
     a.n_days, a.n_grid, a.block_ticks = nd, ng, sz["block_ticks"]
+    a.controller = int(batch.controller)
     for k in ("params", "x0", "c0", "hyper", "assumed_basal", "active", "meal_off", "ex_off",
               "wiener", "has_noise", "meas"):
         setattr(a, k, ptr(ins[k]))

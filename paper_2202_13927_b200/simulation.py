@@ -80,17 +80,22 @@ def pack_params(values: dict) -> np.ndarray:
 
 
 def _controller_inputs(controller):
-    """(hyper[30], assumed basal, c0[11]) from a reference DualHormoneController
-    or a DeviceController."""
+    """(hyper[30], assumed basal, c0[11] or None, device code) from a reference
+    DualHormoneController, a PIDController (pid.py) or a DeviceController."""
     if hasattr(controller, "initial_state") and hasattr(controller, "hyper_vec"):
-        if type(controller).__name__ != "DualHormoneController":
-            raise SimulationError("fast engine requires the hovorka_ext model with the dual_hormone controller")
+        name = type(controller).__name__
+        if name == "DualHormoneController":
+            code = device_code("dual_hormone")
+        elif name == "PIDController":
+            code = device_code("pid_pump")
+        else:
+            raise SimulationError(f"controller {name!r} has no device implementation")
         c0 = np.asarray(controller.initial_state().to_vec(), dtype=np.float64)
-        return np.asarray(controller.hyper_vec, np.float64), float(controller.assumed_basal_u_per_h), c0
+        return np.asarray(controller.hyper_vec, np.float64), float(controller.assumed_basal_u_per_h), c0, code
     if hasattr(controller, "code") and hasattr(controller, "profile"):
-        device_code(controller.controller_id)
-        return hyper_vector(controller.profile), float(controller.assumed_basal_u_per_h), None
-    raise SimulationError("fast engine requires the hovorka_ext model with the dual_hormone controller")
+        code = device_code(controller.controller_id)
+        return hyper_vector(controller.profile), float(controller.assumed_basal_u_per_h), None, code
+    raise SimulationError("controller has no device implementation")
 
 
 def _noise_flags(p: np.ndarray):
@@ -125,7 +130,7 @@ def _stats_from_parity(out: dict, i: int, config, sz) -> PatientStats:
     return st
 
 
-def _parity_run(items, config, hyper, device, record_trace=False):
+def _parity_run(items, config, hyper, device, record_trace=False, controller=0):
     """items: list of (pid, p[30], x0[16], c0[11], basal, ProtocolArrays)."""
     sz = sizes(config)
     H, ps = sz["horizon_ticks"], sz["period_steps"]
@@ -146,7 +151,7 @@ def _parity_run(items, config, hyper, device, record_trace=False):
         c0=np.stack([it[3] for it in items]), hyper=hyper,
         assumed_basal=np.array([it[4] for it in items], dtype=np.float64),
         meal_off=moff, meals=meals, ex_off=eoff, ex=ex, wiener=wiener, has_noise=has_noise,
-        meas=meas)
+        meas=meas, controller=int(controller))
     return engine.run_parity(batch, sz, config.dt_s, config.controller_period_s,
                              record_trace=record_trace, device=device), sz
 
@@ -163,7 +168,7 @@ def simulate_closed_loop(patient, parameter_set, protocol, controller, model,
             raise SimulationError(f"invalid protocol: {v[:3]}")
     if record_trace is None:
         record_trace = config.store_trace == "always"
-    hyper, basal, c0 = _controller_inputs(controller)
+    hyper, basal, c0, code = _controller_inputs(controller)
     p = pack_params(parameter_set.values)
     x0, _ub, ok = engine.steady_state(p[None, :], config.initial_bg_mmol_per_l, device)
     if int(ok.cpu()[0]) != GT_STATUS_OK:
@@ -172,7 +177,7 @@ def simulate_closed_loop(patient, parameter_set, protocol, controller, model,
     if c0 is None:
         c0 = engine.controller_init(hyper, icr_initial_factor(controller.profile), [basal], device).cpu().numpy()[0]
     pa = compile_protocol(protocol, config.horizon_s)
-    out, sz = _parity_run([(int(patient.id), p, x0, c0, basal, pa)], config, hyper, device, record_trace)
+    out, sz = _parity_run([(int(patient.id), p, x0, c0, basal, pa)], config, hyper, device, record_trace, code)
     st = _stats_from_parity(out, 0, config, sz)
     status = "ok" if int(out["status"][0]) == GT_STATUS_OK else "nonfinite"
     trace = out["trace"][0][:st.ticks] if record_trace else None
@@ -242,6 +247,7 @@ def _run_trial_parity(population, generator, controller_id, profile, model_id, c
     t0 = time.perf_counter()
     ids, params, basal = _population_arrays(population, basal_scale)
     hyper = hyper_vector(profile)
+    code = device_code(controller_id)
     x0_d, _ub, ok_d = engine.steady_state(params, config.initial_bg_mmol_per_l, device)
     c0 = engine.controller_init(hyper, icr_initial_factor(profile), basal, device).cpu().numpy()
     x0, ok = x0_d.cpu().numpy(), ok_d.cpu().numpy()
@@ -259,7 +265,7 @@ def _run_trial_parity(population, generator, controller_id, profile, model_id, c
             items.append((int(ids[i]), params[i], x0[i], c0[i], basal[i], pa))
             idx.append(i)
         if items:
-            out, sz = _parity_run(items, config, hyper, device, record_trace=record)
+            out, sz = _parity_run(items, config, hyper, device, record_trace=record, controller=code)
             for j, i in enumerate(idx):
                 if int(out["status"][j]) != GT_STATUS_OK:
                     acc.add_aborted(int(ids[i]))
@@ -281,7 +287,7 @@ def _run_trial_parity(population, generator, controller_id, profile, model_id, c
         wi = int(np.nonzero(ids == acc.worst.patient_id)[0][0])
         pa = compile_protocol(generator.build(config.seed, population[wi][0]), config.horizon_s)
         out, sz = _parity_run([(int(ids[wi]), params[wi], x0[wi], c0[wi], basal[wi], pa)],
-                              config, hyper, device, record_trace=True)
+                              config, hyper, device, record_trace=True, controller=code)
         worst_trace = out["trace"][0][: int(out["ticks"][0])]
     return TrialResult(report=report, accumulator=acc, worst_trace=worst_trace, wall_s=wall_s,
                        n_patients=len(population))

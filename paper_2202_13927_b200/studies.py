@@ -31,11 +31,20 @@ METRICS = ("tir", "tbr70", "tbr54", "tar180", "tar250", "hypo_events_lt70", "hyp
 Q = (0.05, 0.25, 0.5, 0.75, 0.95)
 
 
-def default_arms(base: ControllerHyperparameters | None = None) -> dict:
-    """BASELINE configs[3] arms.  The reference controller's basal law is a PD
-    on the filtered CGM (controller.py:449-457), so "PID gains x s" scales
-    basal_kp and basal_kd.  "Bolus-only" sets both to 0, which leaves the
-    assumed basal rate plus the meal-bolus calculator."""
+def default_arms(base=None, controller_id: str = "dual_hormone") -> dict:
+    """BASELINE configs[3] arms: gains x0.5 / x1 / x1.5 and bolus-only.
+
+    * ``pid_pump`` (pid.py, the BASELINE's PID): kp, ki, kd scaled together;
+      bolus-only = all three 0, i.e. the pump-quantised assumed basal plus
+      meal boluses.
+    * ``dual_hormone`` (the reference's controller): its basal law is a PD on
+      the filtered CGM (controller.py:449-457), so the gains are basal_kp and
+      basal_kd; bolus-only sets both to 0."""
+    if controller_id == "pid_pump":
+        from .pid import PIDProfile
+        base = base or PIDProfile()
+        return {"pid_x0.5": base.scaled(0.5), "pid_x1": base, "pid_x1.5": base.scaled(1.5),
+                "bolus_only": base.scaled(0.0)}
     base = base or ControllerHyperparameters()
     return {"pd_x0.5": base.scaled(0.5, 0.5), "pd_x1": base, "pd_x1.5": base.scaled(1.5, 1.5),
             "bolus_only": base.scaled(0.0, 0.0)}
@@ -57,10 +66,10 @@ def _timed_step(ft):
     return ev[0].elapsed_time(ev[1]), ev[0].elapsed_time(ev[2])
 
 
-def _trial(pop, profile, cfg, device, generator=None, **kw):
+def _trial(pop, profile, cfg, device, generator=None, controller_id="dual_hormone", **kw):
     from .trial import FastTrial
     return FastTrial(pop.pid0, pop.params_device, pop.basal_device, generator or ThreeMealProtocol(),
-                     profile, cfg, device=device, per_patient_metrics=True, **kw)
+                     profile, cfg, controller_id=controller_id, device=device, per_patient_metrics=True, **kw)
 
 
 def _per_patient(ft) -> dict:
@@ -80,29 +89,35 @@ def _dist(x: np.ndarray) -> dict:
 
 
 def treatment_comparison(n: int, weeks: int, seed: int, device=None, arms: dict | None = None,
-                         reference_arm: str = "pd_x1", dt_s: float = 60.0, pid0: int = 0,
-                         population_seed: int | None = None, generator=None) -> dict:
+                         reference_arm: str | None = None, dt_s: float = 60.0, pid0: int = 0,
+                         population_seed: int | None = None, generator=None,
+                         controller_id: str = "dual_hormone") -> dict:
     """BASELINE configs[3]: ``arms`` (name -> profile) x one shared population
     under common random numbers.  Returns per-arm report quantiles, per-arm
     per-patient metric distributions, and paired differences (arm minus
     ``reference_arm``) over the patients that finished in both arms."""
     from .population import generate_population
     device = engine.require_device(device)
-    arms = arms or default_arms()
+    arms = arms or default_arms(controller_id=controller_id)
+    if reference_arm is None:
+        reference_arm = "pid_x1" if controller_id == "pid_pump" else "pd_x1"
     if reference_arm not in arms:
         raise ValueError(f"reference arm {reference_arm!r} is not among {sorted(arms)}")
     cfg = SimulationConfig(horizon_s=weeks * 7 * 86400.0, seed=seed, dt_s=dt_s)
     pop = generate_population(seed if population_seed is None else population_seed, n, pid0=pid0,
                               device=device, on_exhausted="redraw_weight")
     per, out = {}, {"config": {"patients": n, "weeks": weeks, "seed": seed, "dt_s": dt_s,
+                               "controller": controller_id,
                                "crn": "streams keyed by (seed, patient id, role)"}, "arms": {}}
     for name, prof in arms.items():
-        ft = _trial(pop, prof, cfg, device, generator)
+        ft = _trial(pop, prof, cfg, device, generator, controller_id)
         sim_ms, step_ms = _timed_step(ft)
         acc = ft.accumulator()
         per[name] = _per_patient(ft)
         out["arms"][name] = {
-            "basal_kp": prof.basal_kp, "basal_kd": prof.basal_kd, "n_patients": acc.n_patients,
+            "gains": ({"kp": prof.kp, "ki": prof.ki, "kd": prof.kd} if controller_id == "pid_pump"
+                      else {"basal_kp": prof.basal_kp, "basal_kd": prof.basal_kd}),
+            "n_patients": acc.n_patients,
             "n_aborted": acc.n_aborted, "sim_ms": sim_ms, "step_ms": step_ms,
             "patient_weeks_per_s": n * weeks / (step_ms / 1000.0),
             "quantiles": analytics.metric_quantiles(acc),
@@ -121,7 +136,7 @@ def treatment_comparison(n: int, weeks: int, seed: int, device=None, arms: dict 
 
 
 def precision_study(n: int, weeks: int, seed: int, device=None, agg: int = 10, dt_s: float = 60.0,
-                    pid0: int = 0, profile=None, generator=None) -> dict:
+                    pid0: int = 0, profile=None, generator=None, controller_id: str = "dual_hormone") -> dict:
     """BASELINE configs[4]: FP64 at dt, FP64 at dt/agg, FP32 at dt on one
     population.  Variants:
 
@@ -134,7 +149,12 @@ def precision_study(n: int, weeks: int, seed: int, device=None, agg: int = 10, d
     Returns each variant's throughput and the per-patient metric deviations."""
     from .population import generate_population
     device = engine.require_device(device)
-    profile = profile or ControllerHyperparameters()
+    if profile is None:
+        if controller_id == "pid_pump":
+            from .pid import PIDProfile
+            profile = PIDProfile()
+        else:
+            profile = ControllerHyperparameters()
     pop = generate_population(seed, n, pid0=pid0, device=device, on_exhausted="redraw_weight")
     fine = dt_s / agg
     variants = {
@@ -145,7 +165,7 @@ def precision_study(n: int, weeks: int, seed: int, device=None, agg: int = 10, d
                                "fine_dt_s": fine}, "variants": {}}
     for name, (dt, a, fp32) in variants.items():
         cfg = SimulationConfig(horizon_s=weeks * 7 * 86400.0, seed=seed, dt_s=dt)
-        ft = _trial(pop, profile, cfg, device, generator, noise_agg=a, fp32=fp32)
+        ft = _trial(pop, profile, cfg, device, generator, controller_id, noise_agg=a, fp32=fp32)
         _timed_step(ft)                       # warm-up (module load, allocator)
         sim_ms, step_ms = _timed_step(ft)
         acc = ft.accumulator()

@@ -148,8 +148,10 @@ class _P:
         self.id, self.body_weight_kg = pid, w
 
 
-def sim_fixture(name, entries, generator, cfg, trace_for=(0, 1), extra_params=None):
-    prof = load_profile()
+def sim_fixture(name, entries, generator, cfg, trace_for=(0, 1), extra_params=None, make_ctl=None,
+                prof=None):
+    prof = prof or load_profile()
+    make_ctl = make_ctl or (lambda basal: DualHormoneController(prof, basal))
     model = get_model("hovorka_ext")
     rec = {"ids": [], "params": [], "x0": [], "c0": [], "basal": [], "status": [], "ticks": [],
            "tir": [], "hist": [], "scal": [], "day_dose": [], "timeline": [], "meal_off": [0],
@@ -161,7 +163,7 @@ def sim_fixture(name, entries, generator, cfg, trace_for=(0, 1), extra_params=No
         if extra_params and patient.id in extra_params:
             values.update(extra_params[patient.id])
         p = hovorka.pack_params(values)
-        ctl = DualHormoneController(prof, pset.u_basal_u_per_h)
+        ctl = make_ctl(pset.u_basal_u_per_h)
         pa = compile_protocol(generator.build(cfg.seed, patient), cfg.horizon_s)
         try:
             x0, _ = hovorka.steady_state(p, cfg.initial_bg_mmol_per_l)
@@ -204,7 +206,7 @@ def sim_fixture(name, entries, generator, cfg, trace_for=(0, 1), extra_params=No
         arrays[nm] = np.concatenate(meals[k]) if meals[k] else np.zeros(0)
     for k, nm in enumerate(("ex_start", "ex_end", "ex_hrr", "ex_announced")):
         arrays[nm] = np.concatenate(ex[k]) if ex[k] else np.zeros(0)
-    arrays["hyper"] = load_profile().to_vec()
+    arrays["hyper"] = prof.to_vec()
     arrays["config"] = np.array([cfg.horizon_s, cfg.seed, cfg.dt_s, cfg.controller_period_s,
                                  cfg.grid_step_s, cfg.initial_bg_mmol_per_l])
     arrays.update(traces)
@@ -276,7 +278,32 @@ def flop_fixture():
         json.dump(counts, fh, indent=1, sort_keys=True)
 
 
+def pid_fixtures():
+    """The BASELINE PID + pump-quantisation controller (paper_2202_13927_b200/pid.py)
+    registered in the REFERENCE's controller registry and run by the reference's
+    own generic engine (_python_block, simulation.py:199-298)."""
+    from glucotrial.controller import register_controller as ref_register
+    from paper_2202_13927_b200.pid import PIDController, PIDProfile
+    try:
+        ref_register("pid_pump", lambda profile, basal: PIDController(profile, basal))
+    except ValueError:
+        pass
+    prof = PIDProfile()
+    e0, _ = generate_population(seed=0, n=64)
+    e101, _ = generate_population(seed=101, n=12)
+    tm = ThreeMealProtocol()
+    cfg_tm = SimulationConfig(horizon_s=3 * DAY, seed=0, dt_s=60.0)
+    sim_fixture("sim_pid_threemeal_dt60.npz", e0[:8], tm, cfg_tm, prof=prof,
+                make_ctl=lambda basal: PIDController(prof, basal))
+    cfg_ny = SimulationConfig(horizon_s=2 * DAY, seed=33)
+    sim_fixture("sim_pid_northern_dt30.npz", e101[:4], NorthernYearProtocol(), cfg_ny, prof=prof,
+                make_ctl=lambda basal: PIDController(prof, basal))
+
+
 def main():
+    if "--only-pid" in sys.argv:
+        pid_fixtures()
+        return
     pop = population_fixture()
     flop_fixture()
     steady_fixture(pop)
@@ -307,6 +334,7 @@ def main():
     worst_cfg = dataclasses.replace(cfg_ny, store_trace="worst_case_only")
     res = run_trial(e101[:4], nyp, "dual_hormone", load_profile(), "hovorka_ext", worst_cfg)
     _save("worst_trace.npz", trace=res.worst_trace, worst_id=np.array(res.accumulator.worst.patient_id))
+    pid_fixtures()
     # one empty-protocol day, no noise: fixed point (test_simulation.py:133-144)
     with open(os.path.join(HERE, "versions.json"), "w") as fh:
         json.dump({"numpy": np.__version__, "scipy": scipy.__version__, "numba": numba.__version__,
