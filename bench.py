@@ -4,8 +4,9 @@ the fused integrator and the reference-path CPU baseline.
 
 Workload (BASELINE configs[1]): 100,000 virtual patients x 4 weeks per GPU,
 FP64, Euler-Maruyama at 1-min step with process noise, 5-min CGM with sensor
-noise, the reference dual-hormone AP controller (PD basal + heuristic meal
-bolus), 3 meals/day ~N(50/70/80 g, 10 g) with U(+-30 min)
+noise, the BASELINE's PID controller with pump quantisation (pid.py; its
+golden run is the reference's own generic engine) -- or, with
+--controller dual_hormone, the reference's own AP controller -- 3 meals/day ~N(50/70/80 g, 10 g) with U(+-30 min)
 jitter, seed 1, population drawn by the device sampler from the reference
 distribution table.  One "step" = one pass of the hot path over the batch:
 fused integrator + population reduction (histograms, quantile bins, exact
@@ -118,21 +119,31 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_baseline(n_sample: int, weeks: int, threads: int):
+def controller_setup(controller_id: str):
+    """(profile, device code, config label) of the benchmarked controller."""
+    if controller_id == "pid_pump":
+        from paper_2202_13927_b200.pid import PIDProfile
+        return PIDProfile(), 1, "pid_pump (PID basal + pump quantisation 0.05 U, meal bolus; BASELINE)"
+    from paper_2202_13927_b200.controller import ControllerHyperparameters
+    return ControllerHyperparameters(), 0, "dual_hormone (reference AP: PD basal + heuristic meal bolus)"
+
+
+def cpu_baseline(n_sample: int, weeks: int, threads: int, controller_id: str = "pid_pump"):
     """Reference path on the host cores: the oracle's C restatement of the
     numba kernel (bitwise equal to it on injected inputs), OpenMP over
     patients, per-patient noise + schedule generation included."""
     sys.path.insert(0, os.path.join(REPO, "oracle"))
     import oracle
     from paper_2202_13927_b200.config import SimulationConfig, sizes
-    from paper_2202_13927_b200.controller import ControllerHyperparameters, initial_icr
+    from paper_2202_13927_b200.controller import initial_icr
     from paper_2202_13927_b200.protocol import ThreeMealProtocol
     from paper_2202_13927_b200.rng import ROLE_DEVICE_NOISE
     cfg = SimulationConfig(horizon_s=weeks * 7 * 86400.0, seed=SEED, dt_s=DT_S)
     sz = sizes(cfg)
     pop = golden_population(n_sample)
     params, ub, x0 = pop
-    prof = ControllerHyperparameters()
+    prof, code, _ = controller_setup(controller_id)
+    oracle.set_controller(code)
     c0 = np.zeros((n_sample, 11))
     c0[:, 3] = [initial_icr(u, prof) for u in ub]
     c0[:, 6] = -1e18
@@ -168,7 +179,7 @@ def run_reference_arm(args):
     n_sample = max(threads * 64, 512)
     vals = []
     for i in range(args.warmup + args.steps):
-        v, wall = cpu_baseline(n_sample, WEEKS, threads)
+        v, wall = cpu_baseline(n_sample, WEEKS, threads, args.controller)
         if i >= args.warmup:
             vals.append(v)
     v = float(np.mean(vals))
@@ -179,7 +190,8 @@ def run_reference_arm(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"BASELINE configs[1] shape ({N_PATIENTS} patients x {WEEKS} weeks), "
                                f"timed on a {n_sample}-patient sample at full horizon",
-                   "dt_s": DT_S, "seed": SEED, "controller": "dual_hormone", "protocol": "three_meal"},
+                   "dt_s": DT_S, "seed": SEED, "controller": controller_setup(args.controller)[2],
+                   "protocol": "three_meal"},
         "cpu_baseline": {"value": v, "unit": "patient-weeks/s", "cores": threads, "kind": "port",
                          "sample": f"{n_sample} patients x {WEEKS} weeks, dt 60 s, all {threads} host threads"},
         "e2e": {"value": v, "unit": "patient-weeks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -200,7 +212,6 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=device)
     from paper_2202_13927_b200 import analytics, engine, flops
     from paper_2202_13927_b200.config import SimulationConfig
-    from paper_2202_13927_b200.controller import ControllerHyperparameters
     from paper_2202_13927_b200.parallel import allreduce_accumulator
     from paper_2202_13927_b200.population import generate_population
     from paper_2202_13927_b200.protocol import ThreeMealProtocol
@@ -209,13 +220,14 @@ def run_ours(args):
     n = args.patients
     cfg = SimulationConfig(horizon_s=WEEKS * 7 * 86400.0, seed=SEED, dt_s=DT_S)
     pid0 = rank * n
-    prof = ControllerHyperparameters()
+    prof, _code, ctl_label = controller_setup(args.controller)
     gen = ThreeMealProtocol()
     t_s0 = time.perf_counter()
     pop = generate_population(SEED, n, pid0=pid0, device=device, on_exhausted="redraw_weight")
     torch.cuda.synchronize()
     sampler_s = time.perf_counter() - t_s0
-    ft = FastTrial(pid0, pop.params_device, pop.basal_device, gen, prof, cfg, device=device,
+    ft = FastTrial(pid0, pop.params_device, pop.basal_device, gen, prof, cfg, controller_id=args.controller,
+                   device=device,
                    per_patient_metrics=True)
     stream = torch.cuda.current_stream(device)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)  # > 126 MB L2
@@ -262,7 +274,8 @@ def run_ours(args):
     for k in range(max(1, min(args.steps, 3)) + 1):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        acc_e, met = run_population_arrays(params_h, basal_h, gen, prof, cfg, pid0=pid0, device=device)
+        acc_e, met = run_population_arrays(params_h, basal_h, gen, prof, cfg, pid0=pid0, device=device,
+                                           controller_id=args.controller)
         torch.cuda.synchronize()
         if k > 0:
             e2e_ms.append(1000 * (time.perf_counter() - t0))
@@ -280,7 +293,7 @@ def run_ours(args):
         return 0
     pw_per_step = n * WEEKS * ws
     value = pw_per_step / (tot_ms / args.steps / 1000.0)
-    F = flops.flops_per_step(ft.sz["period_steps"])
+    F = flops.flops_per_step(ft.sz["period_steps"], args.controller)
     flop_per_launch = F * n * ft.sz["horizon_ticks"]
     sim_s = float(np.mean(sim_ms)) / 1000.0
     peak, peak_src = fp64_peak()
@@ -289,7 +302,7 @@ def run_ours(args):
     if not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         cpu_n = max(threads * 64, 512)
-        cpu_v, cpu_wall = cpu_baseline(cpu_n, WEEKS, threads)
+        cpu_v, cpu_wall = cpu_baseline(cpu_n, WEEKS, threads, args.controller)
     q = analytics.metric_quantiles(acc_all)
     h2d = params_h.numel() * 8 + basal_h.numel() * 8
     d2h = n * (5 * 4 + 2 * 4 + 4) + 8 * (4 + 5 + 5 * 201 + 247 + 2 * 246 + 2 + 3 * ft.sz["n_grid"] + 603 + 3 + 4 + 7 * 201)
@@ -302,7 +315,7 @@ def run_ours(args):
         "config": {"workload": f"BASELINE configs[1]: {n} patients x {WEEKS} weeks per GPU, dt 60 s, "
                                "controller period 300 s, seed 1",
                    "patients_per_gpu": n, "weeks": WEEKS, "dt_s": DT_S, "seed": SEED,
-                   "controller": "dual_hormone (reference AP: PD basal + heuristic meal bolus)",
+                   "controller": ctl_label,
                    "protocol": "three_meal N(50/70/80,10) g, U(+-30 min)", "noise": "philox4x32-10",
                    "parallelism": f"patients sharded over {ws} GPU(s), NCCL all-reduce of exact accumulators",
                    "l2": "flushed (256 MB write) between timed iterations"},
@@ -339,6 +352,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--patients", type=int, default=N_PATIENTS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--controller", default="pid_pump", choices=["pid_pump", "dual_hormone"])
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)

@@ -9,7 +9,9 @@ hovorka.py:76-136) + diffusion_diag 3 + 16 x (x += f*dt) 32 + 3 x
 15 (typical) + y 2 + u conversions 7 + announcement horizon 1 = 25.
 tests/golden/flop_counts.json holds the drift/controller counts measured by
 an op-counting float over the reference's own functions (make_golden.py);
-tests/test_flops.py pins these constants to it.
+tests/test_flops.py pins these constants to it.  The BASELINE's PID
+controller (pid.py, run by the reference's generic engine) takes 22 on its
+typical branch (no meal bolus), counted the same way over pid_step_vec.
 """
 
 DRIFT_TYPICAL = 69
@@ -17,11 +19,13 @@ CONTROLLER_TYPICAL = 15
 STEP_OTHER = 2 + 1 + 1 + 1 + 1 + 3 + 32 + 9
 STEP = STEP_OTHER + DRIFT_TYPICAL            # 119
 TICK = CONTROLLER_TYPICAL + 2 + 7 + 1        # 25
+PID_CONTROLLER_TYPICAL = 22
+PID_TICK = PID_CONTROLLER_TYPICAL + 2 + 7 + 1   # 32
 
 
-def flops_per_step(period_steps: int) -> float:
-    return STEP + TICK / period_steps
+def flops_per_step(period_steps: int, controller: str = "dual_hormone") -> float:
+    return STEP + (PID_TICK if controller == "pid_pump" else TICK) / period_steps
 
 
-def flops_per_patient_week(dt_s: float, period_steps: int) -> float:
-    return flops_per_step(period_steps) * 604800.0 / dt_s
+def flops_per_patient_week(dt_s: float, period_steps: int, controller: str = "dual_hormone") -> float:
+    return flops_per_step(period_steps, controller) * 604800.0 / dt_s

@@ -14,3 +14,40 @@ def test_flop_constants_pinned_to_reference_counts():
     assert c["diffusion"] == 3
     assert flops.STEP == 119 and flops.TICK == 25
     assert abs(flops.flops_per_patient_week(60.0, 5) - 1.2499e6) < 1e3
+
+
+def test_pid_controller_op_count():
+    """PID_CONTROLLER_TYPICAL = FP64 +,-,*,/ of pid_step_vec on its typical
+    branch (no meal bolus), counted with an op-counting float."""
+    import numpy as np
+    from paper_2202_13927_b200 import pid
+
+    class CF(float):
+        n = 0
+
+        def _w(op):
+            def f(self, o):
+                CF.n += 1
+                return CF(getattr(float, op)(self, o))
+            return f
+        __add__, __radd__ = _w("__add__"), _w("__radd__")
+        __sub__, __rsub__ = _w("__sub__"), _w("__rsub__")
+        __mul__, __rmul__ = _w("__mul__"), _w("__rmul__")
+        __truediv__, __rtruediv__ = _w("__truediv__"), _w("__rtruediv__")
+
+        def __neg__(self):
+            return CF(-float(self))
+
+    prof = pid.PIDProfile()
+    h = [CF(v) for v in prof.to_vec()]
+    c = [CF(v) for v in pid.PIDController(prof, 0.8).initial_state().to_vec()]
+    g = np.random.default_rng(1)
+    counts = []
+    for k in range(300):
+        CF.n = 0
+        pid.pid_step_vec(c, CF(float(np.clip(g.normal(7, 1.5), 2, 20))), CF(0.0), CF(-1.0), CF(300.0 * k),
+                         CF(300.0), h, CF(0.8), [0, 0, 0])
+        counts.append(CF.n)
+    vals, cnt = np.unique(counts[1:], return_counts=True)
+    assert int(vals[np.argmax(cnt)]) == flops.PID_CONTROLLER_TYPICAL
+    assert flops.flops_per_step(5, "pid_pump") == 119 + 32 / 5
