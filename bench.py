@@ -55,11 +55,14 @@ def fp64_peak():
         37.2, "nominal 148 SM x 64 DFMA x 2 x 1.965 GHz (fallback)")
 
 
-def measured_traffic(n_patients):
+TRAFFIC_FILES = {"pid_pump": "r01b_fast_kernel_pid_traffic.json", "dual_hormone": "r01_traffic.json"}
+
+
+def measured_traffic(n_patients, controller="pid_pump"):
     """DRAM bytes (read + write) per launch of the fused kernel from the
     committed ncu --set full capture of this exact workload, else None."""
     try:
-        d = json.load(open(os.path.join(REPO, "profiles", "r01_traffic.json")))
+        d = json.load(open(os.path.join(REPO, "profiles", TRAFFIC_FILES[controller])))
     except OSError:
         return None
     if n_patients != N_PATIENTS:
@@ -320,7 +323,7 @@ def run_ours(args):
                    "parallelism": f"patients sharded over {ws} GPU(s), NCCL all-reduce of exact accumulators",
                    "l2": "flushed (256 MB write) between timed iterations"},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": measured_traffic(n),
+                     "frac": achieved / peak, "traffic": measured_traffic(n, args.controller),
                      "kernel": "gt::fast_kernel<THREE_MEAL, PHILOX>",
                      "algorithmic_flops_per_launch": flop_per_launch,
                      "flops_per_step": F, "peak_source": peak_src,
