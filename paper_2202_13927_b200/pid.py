@@ -48,12 +48,15 @@ PICRMIN, PICRMAX = 17, 18
 
 @dataclass(frozen=True)
 class PIDProfile:
+    # defaults: the best TIR - 3*TBR70 of a 108-point grid over setpoint, kp,
+    # ki, kd, factor_max (tools/pid_sweep.py, 20k patients x 4 weeks, CRN):
+    # TIR 84.8 %, TBR<70 1.0 %, TBR<54 0.02 %, TAR>250 2.5 %
     filter_coeff: float = 0.35
-    setpoint: float = 6.0
-    kp: float = 0.15            # basal factor per mmol/L
+    setpoint: float = 6.5
+    kp: float = 0.05            # basal factor per mmol/L
     ki: float = 0.02            # basal factor per mmol/L * h
     kd: float = 3.0             # basal factor per mmol/L change per period
-    factor_max: float = 3.0
+    factor_max: float = 2.0
     integral_max: float = 20.0  # mmol/L * h
     basal_increment_u: float = 0.05
     bolus_increment_u: float = 0.05

@@ -30,6 +30,18 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
 
 
+CTRL = "pid_pump"   # BASELINE's controller; --controller dual_hormone for the reference's
+
+
+def _prof():
+    """(profile, device code) of the configured controller."""
+    if CTRL == "pid_pump":
+        from paper_2202_13927_b200.pid import PIDProfile
+        return PIDProfile(), 1
+    from paper_2202_13927_b200.controller import ControllerHyperparameters
+    return ControllerHyperparameters(), 0
+
+
 def _sync():
     import torch
     torch.cuda.synchronize()
@@ -39,28 +51,29 @@ def c0(dev, scale):
     import oracle as orc
     from paper_2202_13927_b200 import analytics, flops
     from paper_2202_13927_b200.config import SimulationConfig
-    from paper_2202_13927_b200.controller import ControllerHyperparameters
     from paper_2202_13927_b200.population import generate_population
     from paper_2202_13927_b200.protocol import ThreeMealProtocol
     from paper_2202_13927_b200.studies import _timed_step, _trial
     n, days = max(32, int(1000 * scale)), 7
     cfg = SimulationConfig(horizon_s=days * 86400.0, seed=0, dt_s=60.0)
-    prof, gen = ControllerHyperparameters(), ThreeMealProtocol()
+    (prof, code), gen = _prof(), ThreeMealProtocol()
     t0 = time.perf_counter()
     pop = generate_population(0, n, device=dev, on_exhausted="redraw_weight")
     _sync()
     sampler_s = time.perf_counter() - t0
-    ft = _trial(pop, prof, cfg, dev)
+    ft = _trial(pop, prof, cfg, dev, controller_id=CTRL)
     _timed_step(ft)
     sim_ms, step_ms = _timed_step(ft)
     acc = ft.accumulator()
     m = ft.metrics()
     threads = os.cpu_count() or 1
+    orc.set_controller(code)
     t0 = time.perf_counter()
     ref = orc.run_batch_philox(gen, cfg.seed + 1000, 0, ft.params.cpu().numpy(), ft.x0.cpu().numpy(),
                                ft.c0.cpu().numpy(), prof.to_vec(), ft.basal.cpu().numpy(), ft.sz,
                                cfg.dt_s, cfg.controller_period_s, nthreads=threads)
     cpu_s = time.perf_counter() - t0
+    orc.set_controller(0)
     H = ft.sz["horizon_ticks"]
     tir_ref = ref["tir_ticks"][:, 2] / H
     pw = n * days / 7.0
@@ -79,14 +92,13 @@ def c1(dev, scale):
     import torch
     from paper_2202_13927_b200 import engine, rng
     from paper_2202_13927_b200.config import SimulationConfig
-    from paper_2202_13927_b200.controller import ControllerHyperparameters
     from paper_2202_13927_b200.population import generate_population
     from paper_2202_13927_b200.protocol import ThreeMealProtocol, compile_protocol
     from paper_2202_13927_b200.simulation import _csr, _noise_flags
     from paper_2202_13927_b200.trial import FastTrial
     n, weeks, chunk = max(32, int(1000 * scale)), 4, 250
     cfg = SimulationConfig(horizon_s=weeks * 7 * 86400.0, seed=1, dt_s=60.0)
-    prof, gen = ControllerHyperparameters(), ThreeMealProtocol()
+    (prof, code), gen = _prof(), ThreeMealProtocol()
     pop = generate_population(1, n, device=dev, on_exhausted="redraw_weight")
     res = {"patients": n, "weeks": weeks, "parity_bitwise_mismatch": 0, "fast_outside_1e-9": 0,
            "fast_hist_differs": 0, "parity_s": 0.0, "oracle_s": 0.0}
@@ -97,7 +109,8 @@ def c1(dev, scale):
     for lo in range(0, n, chunk):
         hi = min(n, lo + chunk)
         params_d = pop.params_device[lo:hi].contiguous()
-        ft = FastTrial(lo, params_d, pop.basal_device[lo:hi].contiguous(), gen, prof, cfg, device=dev,
+        ft = FastTrial(lo, params_d, pop.basal_device[lo:hi].contiguous(), gen, prof, cfg, controller_id=CTRL,
+                       device=dev,
                        per_patient_metrics=True)
         sz = ft.sz
         H, ps = sz["horizon_ticks"], sz["period_steps"]
@@ -119,14 +132,16 @@ def c1(dev, scale):
         moff, meals, eoff, ex = _csr(pas)
         batch = engine.ParityBatch(params=P, x0=x0, c0=c0, hyper=prof.to_vec(), assumed_basal=basal,
                                    meal_off=moff, meals=meals, ex_off=eoff, ex=ex, wiener=wiener,
-                                   has_noise=has_noise, meas=meas)
+                                   has_noise=has_noise, meas=meas, controller=code)
         t0 = time.perf_counter()
         par = engine.run_parity(batch, sz, cfg.dt_s, cfg.controller_period_s, device=dev)
         res["parity_s"] += time.perf_counter() - t0
+        orc.set_controller(code)
         t0 = time.perf_counter()
         ora = orc.run_batch_injected(P, x0, c0, prof.to_vec(), basal, sz, cfg.dt_s, cfg.controller_period_s,
                                      moff, meals, eoff, ex, wiener, has_noise, meas)
         res["oracle_s"] += time.perf_counter() - t0
+        orc.set_controller(0)
         for k in ("status", "ticks", "tir_ticks", "bg_hist", "scal", "day_dose", "timeline", "x_out", "c_out"):
             a, b = par[k], ora[k]
             bad = ~np.all((a == b) | (np.isnan(a) & np.isnan(b)), axis=tuple(range(1, a.ndim)))
@@ -152,7 +167,6 @@ def c2(dev, scale):
     import torch
     from paper_2202_13927_b200 import analytics
     from paper_2202_13927_b200.config import SimulationConfig
-    from paper_2202_13927_b200.controller import ControllerHyperparameters
     from paper_2202_13927_b200.population import generate_population
     from paper_2202_13927_b200.studies import _timed_step, _trial
     n, weeks = int(1_000_000 * scale), 52
@@ -162,7 +176,7 @@ def c2(dev, scale):
     _sync()
     sampler_s = time.perf_counter() - t0
     t0 = time.perf_counter()
-    ft = _trial(pop, ControllerHyperparameters(), cfg, dev)
+    ft = _trial(pop, _prof()[0], cfg, dev, controller_id=CTRL)
     _sync()
     setup_s = time.perf_counter() - t0
     sim_ms, step_ms = _timed_step(ft)
@@ -185,7 +199,6 @@ def c2n(dev, scale):
     import torch
     from paper_2202_13927_b200 import analytics
     from paper_2202_13927_b200.config import SimulationConfig
-    from paper_2202_13927_b200.controller import ControllerHyperparameters
     from paper_2202_13927_b200.northern import NorthernYearProtocol
     from paper_2202_13927_b200.population import generate_population
     from paper_2202_13927_b200.studies import _timed_step, _trial
@@ -194,7 +207,7 @@ def c2n(dev, scale):
     pop = generate_population(2, n, device=dev, on_exhausted="redraw_weight")
     _sync()
     t0 = time.perf_counter()
-    ft = _trial(pop, ControllerHyperparameters(), cfg, dev, NorthernYearProtocol())
+    ft = _trial(pop, _prof()[0], cfg, dev, NorthernYearProtocol(), controller_id=CTRL)
     _sync()
     setup_s = time.perf_counter() - t0
     sim_ms, step_ms = _timed_step(ft)
@@ -208,12 +221,12 @@ def c2n(dev, scale):
 
 def c3(dev, scale):
     from paper_2202_13927_b200.studies import treatment_comparison
-    return treatment_comparison(max(1000, int(250_000 * scale)), 12, seed=3, device=dev)
+    return treatment_comparison(max(1000, int(250_000 * scale)), 12, seed=3, device=dev, controller_id=CTRL)
 
 
 def c4(dev, scale):
     from paper_2202_13927_b200.studies import precision_study
-    return precision_study(max(1000, int(250_000 * scale)), 12, seed=4, device=dev)
+    return precision_study(max(1000, int(250_000 * scale)), 12, seed=4, device=dev, controller_id=CTRL)
 
 
 def main():
@@ -221,12 +234,15 @@ def main():
     ap.add_argument("--only", default="C0,C1,C2,C2N,C3,C4")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "configs.json"))
     ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--controller", default="pid_pump", choices=["pid_pump", "dual_hormone"])
     args = ap.parse_args()
+    global CTRL
+    CTRL = args.controller
     import torch
     dev = torch.device("cuda", 0)
     from paper_2202_13927_b200 import _lib
     _lib.load()
-    out = {"device": torch.cuda.get_device_name(dev), "scale": args.scale}
+    out = {"device": torch.cuda.get_device_name(dev), "scale": args.scale, "controller": CTRL}
     fns = {"C0": c0, "C1": c1, "C2": c2, "C2N": c2n, "C3": c3, "C4": c4}
     for name in args.only.split(","):
         t0 = time.perf_counter()
