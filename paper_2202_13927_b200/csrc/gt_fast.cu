@@ -452,6 +452,15 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       }
     };
     double hrr = 0.0;
+    // CSR exercise: the current session (first with end > k) held in registers;
+    // the cursor in shared memory moves only when a session ends
+    int32_t ex_ks_c = INT_MAX, ex_ke_c = INT_MAX;
+    double ex_hrr_c = 0.0;
+    auto load_session = [&](int p) {
+      if (p < n_ex) { ex_ks_c = a.ex_ks[ex_lo + p]; ex_ke_c = a.ex_ke[ex_lo + p]; ex_hrr_c = a.ex_hrr[ex_lo + p]; }
+      else { ex_ks_c = ex_ke_c = INT_MAX; ex_hrr_c = 0.0; }
+    };
+    if (HAS_EX) load_session(sil[(SI_EXPTR) * kFastBS]);
     // warp-uniform cursors derived from the slice start
     int next_grid_ctl = ((ctl_lo + u.grid_ctl - 1) / u.grid_ctl) * u.grid_ctl;
     int g_idx = next_grid_ctl / u.grid_ctl;
@@ -524,13 +533,15 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       const R gin_k = PROTO == GT_PROTO_CSR ? ((k >= m_ks) ? gin : (R)0)
                                             : ((uint32_t)(sk - act_lo) < act_len ? gin : (R)0);
       bool ex_active = false;
-      int ex_ptr = 0;
       if (HAS_EX) {
-        ex_ptr = sil[(SI_EXPTR) * kFastBS];
-        while (ex_ptr < n_ex && k >= a.ex_ke[ex_lo + ex_ptr]) ++ex_ptr;
-        sil[(SI_EXPTR) * kFastBS] = ex_ptr;
-        ex_active = ex_ptr < n_ex && k >= a.ex_ks[ex_lo + ex_ptr];
-        hrr = ex_active ? a.ex_hrr[ex_lo + ex_ptr] : 0.0;
+        if (__builtin_expect(k >= ex_ke_c, 0)) {  // the session ended: advance the cursor
+          int p = sil[(SI_EXPTR) * kFastBS];
+          while (p < n_ex && k >= a.ex_ke[ex_lo + p]) ++p;
+          sil[(SI_EXPTR) * kFastBS] = p;
+          load_session(p);
+        }
+        ex_active = k >= ex_ks_c;   // (k < ex_ke_c here)
+        hrr = ex_active ? ex_hrr_c : 0.0;
       }
       // controller tick (_kernel.py:98-135)
       if (tick) {
@@ -566,8 +577,10 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           sil[(SI_ANNM) * kFastBS] = am; sil[(SI_ANNKP) * kFastBS] = akp; sdl[(SC_ANNCARBS) * kFastBS] = carbs;
         }
         double phase = -1.0;
-        if (HAS_EX && ex_active && a.ex_announced[ex_lo + ex_ptr] != 0.0)
-          phase = t_s - a.ex_start_s[ex_lo + ex_ptr];
+        if (HAS_EX && ex_active) {
+          const int p = sil[(SI_EXPTR) * kFastBS];
+          if (a.ex_announced[ex_lo + p] != 0.0) phase = t_s - a.ex_start_s[ex_lo + p];
+        }
         const double y = A_((double)G, M_(u.sqrtR, zm));
         if (TRACE) tr_y = y;
         // ---- controller_step_vec (controller.py:343-458); state in shared
