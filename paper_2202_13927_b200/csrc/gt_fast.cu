@@ -49,7 +49,7 @@ struct Uni {
   double h, ginK, aS, hS, aZ1, hTg, aZ2, cG;
   double aE1, bE1, aE2, bE2, aE3, bE3, qex, sex;
   double sqG, sigEh, sqrtR, rK1, pred_k, u_basal_k, u_bolus_k, u_gluc_k;
-  double dt, period, horizon_s, meal_dur_min, rs_agg;
+  double dt, period, horizon_s, meal_dur_min, rs_agg, pid_ph;
   int32_t ps, n_ctl, ctl_per_day, grid_ctl, hypoL, agg;
   uint32_t rk[20];  // Philox round keys (k0 + r*W0, k1 + r*W1): constant-bank operands
 };
@@ -339,6 +339,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
     R hu_ins, hu2, gin;  // per-step inputs, in the integrator precision
     double bg_sum, day_basal;
     int32_t m_ks, m_ke, act_lo = 0;
+    int ann_rel = 0xFFFF;  // THREE_MEAL: period (from the day start) of the day's next announcement
     uint32_t act_len = 0;  // THREE_MEAL: meal input on for steps act_lo <= s < act_lo + act_len of this period
     int kb_min, kb_max, run39, run30, ev39, ev30, trig_lo;
     double tr_rate = 0.0, tr_y = 0.0, tr_basal = 0.0;  // TRACE only (held trace columns)
@@ -398,6 +399,10 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         }
       }
       m_ks = LDI(SV_MKS); m_ke = LDI(SV_MKE);  // act_lo / act_len are set at the slice's first tick
+      if (PROTO == GT_PROTO_THREE_MEAL) {
+        const int j = sil[(SI_ANNM) * kFastBS];
+        ann_rel = j < 3 ? (int)s_mk[2][j][tid] : 0xFFFF;
+      }
       kb_min = LDI(SV_KBMIN); kb_max = LDI(SV_KBMAX); run39 = LDI(SV_RUN39); run30 = LDI(SV_RUN30);
       ev39 = LDI(SV_EV39); ev30 = LDI(SV_EV30); alive = LDI(SV_ALIVE) != 0;
       status = LDI(SV_STATUS); death_tick = LDI(SV_DEATH);
@@ -432,6 +437,8 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       }
       sil[(SI_MEALM) * kFastBS] = 0;
       load_slot(0);
+      sil[(SI_ANNM) * kFastBS] = 0;
+      ann_rel = s_mk[2][0][tid];
     };
     // flush the lane's uint8 histogram into its HBM column (bins 0..246;
     // bin 247 is the dead-lane sink) and clear it
@@ -547,22 +554,28 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       if (tick) {
         const double t_s = (double)k * u.dt;
         if (alive) {
-          // x * 0 is +-0 for finite x and NaN for Inf/NaN: one FMA per state
+          // x * 0 is +-0 for finite x and NaN for Inf/NaN: one FMA per state,
+          // in four short chains
           const R z = 0;
-          R acc = FMR(Q1, z, FMR(Q2, z, FMR(S1, z, FMR(S2, z, FMR(I, z, FMR(X1, z, FMR(X2, z, FMR(X3, z, z))))))));
-          acc = FMR(D1, z, FMR(D2, z, FMR(G, z, FMR(Z1, z, FMR(Z2, z, acc)))));
-          if (HAS_EX) acc = FMR(E1, z, FMR(E2, z, FMR(E3, z, acc)));
+          R a0 = FMR(Q1, z, FMR(Q2, z, FMR(S1, z, z)));
+          R a1 = FMR(S2, z, FMR(I, z, FMR(X1, z, z)));
+          R a2 = FMR(X2, z, FMR(X3, z, FMR(D1, z, z)));
+          R a3 = FMR(D2, z, FMR(G, z, FMR(Z1, z, FMR(Z2, z, z))));
+          if (HAS_EX) { a0 = FMR(E1, z, a0); a1 = FMR(E2, z, a1); a2 = FMR(E3, z, a2); }
+          const R acc = (a0 + a1) + (a2 + a3);
           if (acc != acc) { alive = false; status = GT_STATUS_NONFINITE; death_tick = k; }
         }
         // announced carbs starting within [t, t+P)
         double announced = 0.0;
         if (PROTO == GT_PROTO_THREE_MEAL) {
-          // meals are >= 1 h apart: at most one starts in a period; adding
-          // the others' 0.0 keeps the reference's sum exact
-          const int rel = ctl - day_ctl0;
-#pragma unroll
-          for (int j = 0; j < 3; ++j)
-            announced = A_(announced, s_mk[2][j][tid] == rel ? s_mc[j][tid] : 0.0);
+          // meals are >= 1 h apart, so at most one starts in a period: the
+          // day's next announcement is a cursor (0 + carbs = the reference's sum)
+          if (ctl - day_ctl0 == ann_rel) {
+            const int j = sil[(SI_ANNM) * kFastBS];
+            announced = A_(0.0, s_mc[j][tid]);
+            sil[(SI_ANNM) * kFastBS] = j + 1;
+            ann_rel = j + 1 < 3 ? (int)s_mk[2][j + 1][tid] : 0xFFFF;
+          }
         }
         int32_t akp = PROTO == GT_PROTO_CSR ? sil[(SI_ANNKP) * kFastBS] : INT_MAX;
         if (akp <= ctl) {
@@ -597,7 +610,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           // ---- PID + pump quantisation (pid.py pid_step_vec), same filter;
           // slots: SC_WEND = integral, SC_SUSP = pump carry
           const double e = S_(filt, H[1]);
-          const double ph = D_(u.period, 3600.0);
+          const double ph = u.pid_ph;   // period / 3600, folded on the host (same IEEE quotient)
           double integ = A_(sdl[(SC_WEND) * kFastBS], M_(e, ph));
           if (integ > H[6]) integ = H[6];
           if (integ < -H[6]) integ = -H[6];
@@ -931,6 +944,7 @@ static Uni make_uni(const gt_fast_args& a) {
   u.hypoL = (int32_t)a.hypo_min_ticks;
   u.agg = a.noise_agg < 1 ? 1 : a.noise_agg;
   u.rs_agg = 1.0 / std::sqrt((double)u.agg);
+  u.pid_ph = a.period_s / 3600.0;
   uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
   for (int r = 0; r < 10; ++r) {
     u.rk[2 * r] = k0; u.rk[2 * r + 1] = k1;

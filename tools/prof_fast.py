@@ -1,6 +1,6 @@
 """Profiling driver: stage a FastTrial and run simulate+reduce a few times.
 
-    python tools/prof_fast.py [n_patients] [weeks] [reps]
+    python tools/prof_fast.py [n_patients] [weeks] [reps] [three_meal|northern] [dual_hormone|pid_pump]
 """
 import os
 import sys
@@ -20,11 +20,22 @@ from paper_2202_13927_b200.trial import FastTrial  # noqa: E402
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 20000
 weeks = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+proto = sys.argv[4] if len(sys.argv) > 4 else "three_meal"
+ctrl = sys.argv[5] if len(sys.argv) > 5 else "dual_hormone"
 dev = torch.device("cuda", 0)
 cfg = SimulationConfig(horizon_s=weeks * 7 * 86400.0, seed=1, dt_s=60.0)
 pop = generate_population(1, n, device=dev, on_exhausted="redraw_weight")
-ft = FastTrial(0, pop.params_device, pop.basal_device, ThreeMealProtocol(), ControllerHyperparameters(),
-               cfg, device=dev)
+if proto == "northern":
+    from paper_2202_13927_b200.northern import NorthernYearProtocol
+    gen = NorthernYearProtocol()
+else:
+    gen = ThreeMealProtocol()
+if ctrl == "pid_pump":
+    from paper_2202_13927_b200.pid import PIDProfile
+    prof = PIDProfile()
+else:
+    prof = ControllerHyperparameters()
+ft = FastTrial(0, pop.params_device, pop.basal_device, gen, prof, cfg, controller_id=ctrl, device=dev)
 for r in range(reps):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
