@@ -91,3 +91,50 @@ def allreduce_accumulator(acc: TrialAccumulator, device=None, group=None) -> Tri
                               ticks=best[4], tir_ticks=np.array(best[5], np.int64),
                               bg_hist=np.array(best[6], np.int64))
     return out
+
+
+def gather_per_patient(arrays: dict, lo: int, n_total: int, device=None, group=None) -> dict:
+    """All-gather per-patient arrays (same keys on every rank, this rank's
+    contiguous slice starting at global id ``lo``) into global-id order.
+    Shards differ in size by at most one patient, so every rank pads to the
+    largest shard (one collective per array, NCCL all-gather over NVLink on
+    GPUs, gloo on CPU)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    dev = device if device is not None else torch.device("cpu")
+    sizes = [shard_range(n_total, r, world) for r in range(world)]
+    width = max(hi - l for l, hi in sizes)
+    out = {}
+    for k in sorted(arrays):
+        a = np.ascontiguousarray(arrays[k])
+        buf = np.zeros((width,) + a.shape[1:], dtype=a.dtype)
+        buf[: a.shape[0]] = a
+        t = torch.as_tensor(buf, device=dev)
+        parts = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(parts, t, group=group)
+        out[k] = np.concatenate([p.cpu().numpy()[: hi - l] for p, (l, hi) in zip(parts, sizes)])
+    return out
+
+
+def run_trial_sharded(n_total: int, population_seed: int, generator, controller_id: str, profile, config, *,
+                      device=None, group=None, gather_metrics: bool = False, hypo_min_s: float = 900.0):
+    """One rank's part of a multi-GPU trial (launch one process per GPU, e.g.
+    torchrun): this rank samples and simulates global ids
+    ``shard_range(n_total, rank, world)`` with pid-keyed streams, then the
+    exact accumulators are combined.  Every rank returns the same
+    ``(report, accumulator, metrics)``; ``metrics`` (per-patient arrays in
+    global-id order) only with ``gather_metrics``."""
+    import torch.distributed as dist
+    from . import analytics
+    from .population import generate_population
+    from .trial import FastTrial
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    lo, hi = shard_range(n_total, rank, world)
+    pop = generate_population(population_seed, hi - lo, pid0=lo, device=device, on_exhausted="redraw_weight")
+    ft = FastTrial(lo, pop.params_device, pop.basal_device, generator, profile, config, controller_id,
+                   device, hypo_min_s=hypo_min_s, per_patient_metrics=gather_metrics)
+    ft.step()
+    acc = allreduce_accumulator(ft.accumulator(), device, group)
+    metrics = gather_per_patient(ft.metrics(), lo, n_total, device, group) if gather_metrics else None
+    return analytics.build_trial_report(acc, {}), acc, metrics

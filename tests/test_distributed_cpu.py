@@ -76,3 +76,37 @@ def test_shard_ranges_tile(n, world):
         assert b == c
     sizes = [b - a for a, b in got]
     assert max(sizes) - min(sizes) <= 1
+
+
+def _gather_worker(rank, world, port, q):
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, os.path.dirname(here))
+    import torch.distributed as dist
+    from paper_2202_13927_b200.parallel import gather_per_patient, shard_range
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n = 11
+    lo, hi = shard_range(n, rank, world)
+    ids = np.arange(lo, hi)
+    out = gather_per_patient({"tir": (ids * 0.5).astype(np.float32), "status": ids.astype(np.int32) % 3},
+                             lo, n)
+    q.put((rank, out["tir"].tolist(), out["status"].tolist()))
+    dist.destroy_process_group()
+
+
+def test_gather_per_patient_world3():
+    """Per-patient arrays of unequal shards come back in global-id order."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_gather_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=120) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, tir, st in res:
+        assert tir == [i * 0.5 for i in range(11)] and st == [i % 3 for i in range(11)]

@@ -337,3 +337,35 @@ def test_fast_worst_trace_reproduces_the_worst_case(dev, tmp_path):
     assert len(files) == res.accumulator.n_patients
     again = load_trace(os.path.join(tmp_path, f"patient_{w.patient_id:06d}.npz"))
     assert np.array_equal(again, tr)
+
+
+def test_run_trial_sharded_world1_equals_single_trial(dev):
+    """parallel.run_trial_sharded over NCCL (world size 1 on the one GPU the
+    tests have) returns the single-process report and the per-patient arrays."""
+    import socket
+    import torch.distributed as dist
+    from paper_2202_13927_b200 import analytics
+    from paper_2202_13927_b200.config import SimulationConfig
+    from paper_2202_13927_b200.parallel import run_trial_sharded
+    from paper_2202_13927_b200.pid import PIDProfile
+    from paper_2202_13927_b200.population import generate_population
+    from paper_2202_13927_b200.protocol import ThreeMealProtocol
+    from paper_2202_13927_b200.trial import FastTrial
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cfg = SimulationConfig(horizon_s=3 * 86400.0, seed=8, dt_s=60.0)
+    dist.init_process_group("nccl", rank=0, world_size=1, init_method=f"tcp://127.0.0.1:{port}", device_id=dev)
+    try:
+        rep, acc, met = run_trial_sharded(500, 9, ThreeMealProtocol(), "pid_pump", PIDProfile(), cfg, device=dev,
+                                          gather_metrics=True)
+    finally:
+        dist.destroy_process_group()
+    pop = generate_population(9, 500, device=dev, on_exhausted="redraw_weight")
+    ft = FastTrial(0, pop.params_device, pop.basal_device, ThreeMealProtocol(), PIDProfile(), cfg, "pid_pump", dev,
+                   per_patient_metrics=True)
+    ft.step()
+    ref = ft.accumulator()
+    assert analytics.report_bytes(rep) == analytics.report_bytes(analytics.build_trial_report(ref, {}))
+    assert np.array_equal(met["tir"], ft.metrics()["tir"])
