@@ -209,6 +209,12 @@ typedef struct gt_fast_args {
     double *trace;
 } gt_fast_args;
 int gt_simulate_fast(const gt_fast_args *a, void *stream);
+/* The fused kernel's Philox noise, materialised for inspection / tests:
+ * out[n][n_ticks][4] = the 4 FP32 normals of ticks k0..k0+n_ticks-1 of
+ * patients pid0..pid0+n-1 (lanes 0-2 Wiener increments, 3 CGM noise), drawn by
+ * the same device code as gt_simulate_fast with noise_agg = 1. */
+int gt_noise_normals(int64_t n, int64_t pid0, uint64_t seed, uint32_t role, int64_t k0,
+                     int64_t n_ticks, float *out, void *stream);
 int64_t gt_fast_num_warps(int64_t n);
 int64_t gt_fast_scratch_bytes(int64_t n);
 

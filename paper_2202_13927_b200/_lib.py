@@ -128,6 +128,7 @@ SIGNATURES = [
     ("gt_simulate_fast", C.c_int, [C.POINTER(FastArgs), P]),
     ("gt_fast_num_warps", I64, [I64]),
     ("gt_fast_scratch_bytes", I64, [I64]),
+    ("gt_noise_normals", C.c_int, [I64, I64, U64, U32, I64, I64, P, P]),
     ("gt_reduce_trial", C.c_int, [C.POINTER(ReduceArgs), P]),
     ("gt_sample_population", C.c_int, [C.POINTER(SamplerArgs), P]),
     ("gt_generate_meals", C.c_int, [I64, I64, U64, C.POINTER(MealGen), I64, P, P, P, P]),

@@ -40,6 +40,8 @@ int gt_launch_controller_init(int64_t n, const double* hyper, double icr_initial
                               const double* basal, double* c0, cudaStream_t st);
 int gt_launch_fast(const gt_fast_args* a, cudaStream_t st);
 int64_t gt_fast_scratch_need(int64_t n);
+int gt_launch_noise_normals(int64_t n, int64_t pid0, uint64_t seed, uint32_t role, int64_t k0,
+                            int64_t n_ticks, float* out, cudaStream_t st);
 int gt_launch_northern(const gt_northern_args* a, cudaStream_t st);
 int gt_launch_reduce(const gt_reduce_args* a, void* scratch_worst, int nblk, cudaStream_t st);
 int gt_launch_sampler(const gt_sampler_args* a, cudaStream_t st);
@@ -216,6 +218,14 @@ int gt_generate_meals(int64_t n, int64_t pid0, uint64_t seed, const gt_meal_gen*
   REQUIRE(n * n_meals == 0 || (start_s && end_s && carbs_g), "gt_generate_meals: null output");
   REQUIRE(gen->jitter_s >= 0 && gen->duration_s > 0, "gt_generate_meals: bad generator spec");
   return gt_launch_meals(n, pid0, seed, gen, n_meals, start_s, end_s, carbs_g, S(stream));
+}
+
+int gt_noise_normals(int64_t n, int64_t pid0, uint64_t seed, uint32_t role, int64_t k0, int64_t n_ticks,
+                     float* out, void* stream) {
+  REQUIRE(n >= 0 && n_ticks >= 0 && k0 >= 0, "gt_noise_normals: bad sizes");
+  REQUIRE(n * n_ticks == 0 || out, "gt_noise_normals: null output");
+  REQUIRE(k0 + n_ticks <= (int64_t)UINT32_MAX + 1, "gt_noise_normals: tick index beyond 32 bits");
+  return gt_launch_noise_normals(n, pid0, seed, role, k0, n_ticks, out, S(stream));
 }
 
 int gt_northern_protocol(const gt_northern_args* a, void* stream) {

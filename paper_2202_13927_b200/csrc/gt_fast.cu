@@ -33,9 +33,19 @@
 #include <cmath>
 #include <climits>
 #include <cstdlib>
+#include <cstdio>
 #include "gt_common.cuh"
 
 namespace gt {
+
+// Debug builds (-DGT_DEBUG_BOUNDS) check every computed index of the fused
+// kernel and trap with the failing site; release builds compile them out.
+#ifdef GT_DEBUG_BOUNDS
+#define GT_CHECK(c, tag) do { if (!(c)) { printf("GT_CHECK %s failed: block %d thread %d\n", tag, \
+                                                  (int)blockIdx.x, (int)threadIdx.x); __trap(); } } while (0)
+#else
+#define GT_CHECK(c, tag) do { } while (0)
+#endif
 
 #ifndef GT_FAST_MINB
 #define GT_FAST_MINB 4  // resident 128-thread blocks per SM (register budget 128)
@@ -125,6 +135,17 @@ __device__ __forceinline__ unsigned absbits(float x) { return __float_as_uint(x)
 template <typename R> struct kNonfiniteBits;
 template <> struct kNonfiniteBits<double> { static constexpr unsigned v = 0x7ff00000u; };
 template <> struct kNonfiniteBits<float> { static constexpr unsigned v = 0x7f800000u; };
+
+// Rare path of the shared histogram: counter `ha` of bin kb reached 255;
+// add it to the lane's HBM column and clear it.  Out of line so the column
+// address is computed only when a counter actually fills (inlined, the
+// compiler hoists that 64-bit address arithmetic into every step).
+__device__ __noinline__ void drain_bin(int32_t* __restrict__ bg_hist, int64_t n, int64_t warp_global, int kb,
+                                       uint32_t ha) {
+  const int64_t i = warp_global * 32 + (threadIdx.x & 31);
+  if (kb < GT_N_BG_BINS && i < n) atomicAdd(&bg_hist[(int64_t)kb * n + i], 255);
+  asm volatile("st.shared.u8 [%0], 0;" :: "r"(ha));
+}
 
 // ------------------------------------------------------------ noise
 __device__ __forceinline__ void mulwide(uint32_t a, uint32_t b, uint32_t& lo, uint32_t& hi) {
@@ -285,6 +306,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
     if (unit >= sch.n_units) break;
     const int chunk = unit / sch.n_warps;
     const int64_t warp_global = unit - (int64_t)chunk * sch.n_warps;
+    GT_CHECK(warp_global >= 0 && warp_global < sch.n_warps && chunk < sch.n_chunks, "unit");
     const int ctl_lo = chunk * sch.chunk_ctl;
     const int ctl_hi = min(u.n_ctl, ctl_lo + sch.chunk_ctl);
     const bool first = chunk == 0, last = chunk == sch.n_chunks - 1;
@@ -380,10 +402,13 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       if (inrange)
         for (int b = 0; b < GT_N_BG_BINS; ++b) a.bg_hist[(int64_t)b * n + i] = 0;
     } else {
-      const double* sd = sch.sd + ii;
-      const int* si = sch.si + ii;
-#define LDD(f) sd[(int64_t)(f) * n]
-#define LDI(f) si[(int64_t)(f) * n]
+      // every lane (padding included) restores its own slot: a padding lane
+      // must not read a patient slot another warp may still be writing
+      const int64_t npad = (int64_t)sch.n_warps * 32;
+      const double* sd = sch.sd + i;
+      const int* si = sch.si + i;
+#define LDD(f) sd[(int64_t)(f) * npad]
+#define LDI(f) si[(int64_t)(f) * npad]
       Q1 = (R)LDD(SD_Q1); Q2 = (R)LDD(SD_Q2); S1 = (R)LDD(SD_S1); S2 = (R)LDD(SD_S2); I = (R)LDD(SD_I);
       X1 = (R)LDD(SD_X1); X2 = (R)LDD(SD_X2); X3 = (R)LDD(SD_X3); D1 = (R)LDD(SD_D1); D2 = (R)LDD(SD_D2);
       G = (R)LDD(SD_G); Z1 = (R)LDD(SD_Z1); Z2 = (R)LDD(SD_Z2);
@@ -401,6 +426,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       m_ks = LDI(SV_MKS); m_ke = LDI(SV_MKE);  // act_lo / act_len are set at the slice's first tick
       if (PROTO == GT_PROTO_THREE_MEAL) {
         const int j = sil[(SI_ANNM) * kFastBS];
+        GT_CHECK(j >= 0 && j <= 3, "restore ann cursor");
         ann_rel = j < 3 ? (int)s_mk[2][j][tid] : 0xFFFF;
       }
       kb_min = LDI(SV_KBMIN); kb_max = LDI(SV_KBMAX); run39 = LDI(SV_RUN39); run30 = LDI(SV_RUN30);
@@ -420,6 +446,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
     int32_t day_ctl0 = (ctl_lo / cpd) * cpd;
     int32_t day_k0 = day_ctl0 * ps;
     auto load_slot = [&](int j) {
+      GT_CHECK(j >= 0 && j < 3, "load_slot");
       const int ks = s_mk[0][j][tid];
       if (ks == 0xFFFF) { m_ks = m_ke = INT_MAX; gin = 0; return; }
       m_ks = day_k0 + ks; m_ke = day_k0 + s_mk[1][j][tid];
@@ -572,6 +599,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           // day's next announcement is a cursor (0 + carbs = the reference's sum)
           if (ctl - day_ctl0 == ann_rel) {
             const int j = sil[(SI_ANNM) * kFastBS];
+            GT_CHECK(j >= 0 && j < 3, "announce cursor");
             announced = A_(0.0, s_mc[j][tid]);
             sil[(SI_ANNM) * kFastBS] = j + 1;
             ann_rel = j + 1 < 3 ? (int)s_mk[2][j + 1][tid] : 0xFFFF;
@@ -738,14 +766,13 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         }
         kb = alive ? kb : GT_N_BG_BINS;  // dead lanes count into the padding bin 247
         {  // byte ((kb >> 2) * kFastBS + tid) * 4 + (kb & 3)
+          GT_CHECK(kb >= 0 && kb <= GT_N_BG_BINS, "histogram bin");
           const uint32_t ha = hist_lane + ((uint32_t)(kb & ~3) << 7) + (uint32_t)(kb & 3);
           uint32_t c;
           asm volatile("{\n\t.reg .u32 t;\n\tld.shared.u8 t, [%1];\n\tadd.u32 %0, t, 1;\n\t"
                        "st.shared.u8 [%1], %0;\n\t}" : "=r"(c) : "r"(ha));
-          if (__builtin_expect(c == 255u, 0)) {  // a full counter drains into the HBM column
-            if (kb < GT_N_BG_BINS && inrange) atomicAdd(&a.bg_hist[(int64_t)kb * n + i], 255);
-            asm volatile("st.shared.u8 [%0], 0;" :: "r"(ha));
-          }
+          if (__builtin_expect(c == 255u, 0))  // a full counter drains into the HBM column
+            drain_bin(a.bg_hist, n, warp_global, kb, ha);
         }
         bg_sum += bg;
         // extremes: only a tick in the lowest/highest bin so far can move them;
@@ -767,7 +794,9 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         const long long smin = warp_min64(alive ? v : LLONG_MAX);
         const long long smax = warp_max64(alive ? v : LLONG_MIN);
         if (lane == 0) {
-          long long* dst = (long long*)a.timeline_warp + ((int64_t)g_idx * n_warps + warp_global) * 3;
+          GT_CHECK(g_idx >= 0 && g_idx < a.n_grid, "timeline");
+          GT_CHECK(g_idx >= 0 && g_idx < a.n_grid, "timeline tail");
+        long long* dst = (long long*)a.timeline_warp + ((int64_t)g_idx * n_warps + warp_global) * 3;
           dst[0] = ssum; dst[1] = smin; dst[2] = smax;
         }
         if (a.timeline_pp && inrange) a.timeline_pp[(int64_t)g_idx * n + i] = alive ? bg : 0.0;
@@ -832,6 +861,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       if (ctl == next_day_ctl) {
         next_day_ctl += cpd;
         const int64_t day = ctl / cpd - 1;
+        GT_CHECK(day >= 0 && day < a.n_days, "day flush");
         if (inrange) {
           double* dd = a.day_dose + (day * 3) * n + i;
           dd[0] = day_basal; dd[n] = sdl[(SC_DBOLUS) * kFastBS]; dd[2 * n] = sdl[(SC_DGLUC) * kFastBS];
@@ -851,6 +881,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
     // an all-dead warp stops early: its remaining timeline partials are identities
     for (; next_grid_ctl < ctl_hi; next_grid_ctl += u.grid_ctl, ++g_idx)
       if (lane == 0) {
+        GT_CHECK(g_idx >= 0 && g_idx < a.n_grid, "timeline tail");
         long long* dst = (long long*)a.timeline_warp + ((int64_t)g_idx * n_warps + warp_global) * 3;
         dst[0] = 0; dst[1] = LLONG_MAX; dst[2] = LLONG_MIN;
       }
@@ -860,12 +891,13 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       alive = false; status = GT_STATUS_NONFINITE; death_tick = (int)a.horizon_ticks;
     }
     if (!last) {
-      // ---- save the lane state for the next slice
-      if (inrange) {
+      // ---- save the lane state for the next slice (padding lanes too)
+      {
+        const int64_t npad = (int64_t)sch.n_warps * 32;
         double* sd = sch.sd + i;
         int* si = sch.si + i;
-#define STD(f, v) sd[(int64_t)(f) * n] = (v)
-#define STI(f, v) si[(int64_t)(f) * n] = (v)
+#define STD(f, v) sd[(int64_t)(f) * npad] = (v)
+#define STI(f, v) si[(int64_t)(f) * npad] = (v)
         STD(SD_Q1, Q1); STD(SD_Q2, Q2); STD(SD_S1, S1); STD(SD_S2, S2); STD(SD_I, I);
         STD(SD_X1, X1); STD(SD_X2, X2); STD(SD_X3, X3); STD(SD_D1, D1); STD(SD_D2, D2);
         STD(SD_G, G); STD(SD_Z1, Z1); STD(SD_Z2, Z2);
@@ -995,7 +1027,8 @@ static int launch_sched(const gt_fast_args* a, const gt::Uni& u, cudaStream_t st
   s.n_units = (int)(warps * s.n_chunks);
   // scratch: counter + done flags (+ saved lane state when slicing)
   const size_t bytes_i = sizeof(int) * (1 + (size_t)warps);
-  const size_t bytes_state = s.n_chunks > 1 ? (size_t)a->n * (gt::SD_N * sizeof(double) + gt::SV_N * sizeof(int)) : 0;
+  const size_t n_pad = (size_t)warps * 32;   // every lane of a warp owns a saved-state slot
+  const size_t bytes_state = s.n_chunks > 1 ? n_pad * (gt::SD_N * sizeof(double) + gt::SV_N * sizeof(int)) : 0;
   const size_t need = ((bytes_i + 15) & ~size_t(15)) + bytes_state;
   char* scratch = static_cast<char*>(a->scratch);
   const bool own = scratch == nullptr;
@@ -1015,7 +1048,7 @@ static int launch_sched(const gt_fast_args* a, const gt::Uni& u, cudaStream_t st
   if (bytes_state) {
     char* base = scratch + ((bytes_i + 15) & ~size_t(15));
     s.sd = reinterpret_cast<double*>(base);
-    s.si = reinterpret_cast<int*>(base + (size_t)a->n * gt::SD_N * sizeof(double));
+    s.si = reinterpret_cast<int*>(base + n_pad * gt::SD_N * sizeof(double));
   }
   const int64_t blocks_needed = (warps + 3) / 4;
   const unsigned grid = (unsigned)std::min<int64_t>((int64_t)sms * per_sm, blocks_needed);
@@ -1031,11 +1064,43 @@ static int launch_one(const gt_fast_args* a, const gt::Uni& u, cudaStream_t st) 
   return launch_sched<PROTO, NOISE, R, AGG, false>(a, u, st);
 }
 
+// The fused kernel's noise stream, materialised: out[(i * n_ticks + j) * 4 + l]
+// = normal l of tick k0 + j of patient pid0 + i, drawn exactly as the kernel
+// draws it (philox_fast + FP32 SFU Box-Muller; lanes 0-2 = Wiener, 3 = CGM).
+namespace gt {
+__global__ void noise_normals_kernel(int64_t n, int64_t pid0, uint32_t role, int64_t k0, int64_t n_ticks,
+                                     const Uni u, float* out) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n * n_ticks) return;
+  const int64_t i = idx / n_ticks, j = idx - i * n_ticks;
+  const U4 r = philox_fast((uint32_t)(k0 + j), (uint32_t)(pid0 + i), role, 0u, u.rk);
+  float f0, f1, f2, f3;
+  box_muller(r.x, r.y, f0, f1);
+  box_muller(r.z, r.w, f2, f3);
+  float* o = out + idx * 4;
+  o[0] = f0; o[1] = f1; o[2] = f2; o[3] = f3;
+}
+}  // namespace gt
+
+int gt_launch_noise_normals(int64_t n, int64_t pid0, uint64_t seed, uint32_t role, int64_t k0,
+                            int64_t n_ticks, float* out, cudaStream_t st) {
+  if (n <= 0 || n_ticks <= 0) return GT_OK;
+  gt::Uni u{};
+  uint32_t key0 = (uint32_t)seed, key1 = (uint32_t)(seed >> 32);
+  for (int r = 0; r < 10; ++r) {
+    u.rk[2 * r] = key0; u.rk[2 * r + 1] = key1;
+    key0 += 0x9E3779B9u; key1 += 0xBB67AE85u;
+  }
+  const int64_t total = n * n_ticks;
+  gt::noise_normals_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(n, pid0, role, k0, n_ticks, u, out);
+  return gt_check_launch("noise_normals_kernel");
+}
+
 // Upper bound of launch_one's scratch (sliced schedule) for n patients.
 int64_t gt_fast_scratch_need(int64_t n) {
   const int64_t warps = (n + 31) / 32;
   const int64_t bytes_i = (int64_t)sizeof(int) * (1 + warps);
-  return ((bytes_i + 15) & ~int64_t(15)) + n * (int64_t)(gt::SD_N * sizeof(double) + gt::SV_N * sizeof(int));
+  return ((bytes_i + 15) & ~int64_t(15)) + warps * 32 * (int64_t)(gt::SD_N * sizeof(double) + gt::SV_N * sizeof(int));
 }
 
 int gt_launch_fast(const gt_fast_args* a, cudaStream_t st) {

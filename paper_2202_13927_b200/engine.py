@@ -277,6 +277,15 @@ def northern_csr(params, pid0: int, trial_seed: int, dt_s: float, period_s: floa
     return out
 
 
+def noise_normals(n: int, pid0: int, seed: int, role: int, k0: int, n_ticks: int, device):
+    """The fused kernel's noise stream as a [n, n_ticks, 4] float32 tensor."""
+    t = torch()
+    out = empty((n, n_ticks, 4), t.float32, device)
+    check(_lib.load().gt_noise_normals(n, pid0, int(seed) & 0xFFFFFFFFFFFFFFFF, role, k0, n_ticks, ptr(out),
+                                       stream_ptr(device)), "gt_noise_normals")
+    return out
+
+
 FIXED_PARAM_INDEX = tuple(range(15, 30))   # AG .. R: the table's fixed block (hovorka.py:53-55)
 
 

@@ -239,3 +239,16 @@ def test_metric_quantiles_nearest_rank():
     q = analytics.metric_quantiles(acc)["tir_70_180"]
     assert q["p5"] == pytest.approx(4.5 / 200) and q["p50"] == pytest.approx(49.5 / 200)
     assert q["p95"] == pytest.approx(94.5 / 200)
+
+
+def test_empty_population_rejected():
+    """test_simulation.py:318-322: an empty population raises SimulationError
+    (before any device work)."""
+    import pytest
+    from paper_2202_13927_b200.config import SimulationConfig, SimulationError
+    from paper_2202_13927_b200.controller import ControllerHyperparameters
+    from paper_2202_13927_b200.northern import NorthernYearProtocol
+    from paper_2202_13927_b200.simulation import run_trial
+    with pytest.raises(SimulationError):
+        run_trial([], NorthernYearProtocol(), "dual_hormone", ControllerHyperparameters(), "hovorka_ext",
+                  SimulationConfig(horizon_s=86400.0, seed=1))
