@@ -105,3 +105,34 @@ def generate_population(seed: int, n: int, table=None, target_bg: float = 6.0, p
                        rejected_outside_sd=int(rc[1]), rejected_no_steady_state=int(rc[2]),
                        rejected_basal=int(rc[3]))
     return DevicePopulation(pid0, out["params"], out["u_basal"], out["x0"], st)
+
+
+def validate_parameter_sets(params, u_basal, table=None, target_bg: float = 6.0, device=None) -> list:
+    """Batched ``validate_parameter_set`` (population.py:262-282): the three
+    acceptance rules re-checked for every row of ``params`` [n, 30] with its
+    stored basal rate; the steady state is re-solved on the device.  Returns
+    one list of violation strings per patient (empty = valid)."""
+    import math
+    from .layout import PARAM_INDEX
+    table = table or tables.default_parameter_table()
+    p = params.detach().cpu().numpy() if hasattr(params, "detach") else np.asarray(params, np.float64)
+    ub = u_basal.detach().cpu().numpy() if hasattr(u_basal, "detach") else np.asarray(u_basal, np.float64)
+    x0, ub_solved, st = engine.steady_state(np.ascontiguousarray(p, np.float64), target_bg, device)
+    ub_solved, st = ub_solved.cpu().numpy(), st.cpu().numpy()
+    out = []
+    for i in range(p.shape[0]):
+        v = []
+        for k, name in enumerate(PARAM_NAMES):
+            if p[i, k] < 0.0:
+                v.append(f"{name} is negative")
+        for name, spec in table.sampled.items():
+            if spec.kind == "normal" and abs(p[i, PARAM_INDEX[name]] - spec.mean) > spec.sd:
+                v.append(f"{name} outside one standard deviation")
+        if ub[i] < tables.MIN_BASAL_U_PER_H:
+            v.append(f"u_basal {ub[i]:.3f} U/h below {tables.MIN_BASAL_U_PER_H}")
+        if st[i] != 0:
+            v.append("steady state failed")
+        elif not math.isclose(float(ub_solved[i]), float(ub[i]), rel_tol=1e-9, abs_tol=1e-12):
+            v.append("stored u_basal does not match the steady-state solve")
+        out.append(v)
+    return out

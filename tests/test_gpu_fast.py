@@ -369,3 +369,21 @@ def test_run_trial_sharded_world1_equals_single_trial(dev):
     ref = ft.accumulator()
     assert analytics.report_bytes(rep) == analytics.report_bytes(analytics.build_trial_report(ref, {}))
     assert np.array_equal(met["tir"], ft.metrics()["tir"])
+
+
+def test_validate_parameter_sets(dev):
+    """Every sampled set passes the reference's three acceptance rules
+    (population.py:262-282); corrupted sets are reported."""
+    from paper_2202_13927_b200.layout import PARAM_INDEX
+    from paper_2202_13927_b200.population import generate_population, validate_parameter_sets
+    pop = generate_population(12, 300, device=dev, on_exhausted="redraw_weight")
+    assert all(v == [] for v in validate_parameter_sets(pop.params_device, pop.basal_device, device=dev))
+    p = pop.params_device[:4].clone()
+    ub = pop.basal_device[:4].clone()
+    p[0, PARAM_INDEX["EGP0"]] = -1.0
+    p[1, PARAM_INDEX["k12"]] += 10.0
+    ub[2] = 0.1
+    ub[3] *= 1.01
+    v = validate_parameter_sets(p, ub, device=dev)
+    assert any("negative" in s for s in v[0]) and any("standard deviation" in s for s in v[1])
+    assert any("below" in s for s in v[2]) and any("does not match" in s for s in v[3])
