@@ -15,6 +15,9 @@ from .protocol import (Disturbance, FixedProtocol, Protocol, ThreeMealProtocol,
                        compile_protocol, validate_protocol)
 from .simulation import (SimulationResult, SteadyStateError, TrialResult, run_trial,
                          simulate_closed_loop)
+from .northern import NorthernYearProtocol
+from .pid import PIDController, PIDProfile
+from .population import validate_parameter_sets
 
 __all__ = [
     "PatientStats", "TrialAccumulator", "build_trial_report", "merge", "metric_quantiles",
@@ -22,5 +25,6 @@ __all__ = [
     "get_controller_factory", "load_profile", "register_controller", "DevicePopulation",
     "ParameterSet", "Patient", "generate_population", "Disturbance", "FixedProtocol", "Protocol",
     "ThreeMealProtocol", "compile_protocol", "validate_protocol", "SimulationResult",
-    "SteadyStateError", "TrialResult", "run_trial", "simulate_closed_loop",
+    "SteadyStateError", "TrialResult", "run_trial", "simulate_closed_loop", "NorthernYearProtocol",
+    "PIDController", "PIDProfile", "validate_parameter_sets",
 ]
