@@ -334,7 +334,7 @@ def run_ours(args):
         "e2e": {"value": pw_per_step / (e2e / 1000.0), "unit": "patient-weeks/s",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "path": "trial.run_population_arrays (pinned host params -> report fields + per-patient metrics)"},
-        "gpu_launches": args.steps * 5,
+        "gpu_launches": args.steps * 6,   # per step: fused kernel + exclusion re-run + 4 reduction kernels
         "clocks": clk.summary(),
         "sampler_s": sampler_s,
         "trial": {"n_patients": acc_all.n_patients, "n_aborted": acc_all.n_aborted,
