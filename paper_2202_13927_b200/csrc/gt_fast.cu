@@ -253,7 +253,7 @@ enum { SD_Q1, SD_Q2, SD_S1, SD_S2, SD_I, SD_X1, SD_X2, SD_X3, SD_D1, SD_D2, SD_G
 enum { SV_MKS, SV_MKE, SV_KBMIN, SV_KBMAX, SV_RUN39, SV_RUN30, SV_EV39,
        SV_EV30, SV_ALIVE, SV_STATUS, SV_DEATH, SV_MK0, SV_SI0 = SV_MK0 + 9, SV_N = SV_SI0 + N_SI };
 
-template <int PROTO, int NOISE, typename R, bool AGG, bool TRACE>
+template <int PROTO, int NOISE, typename R, bool AGG, bool TRACE, int CTRL>
 __global__ void __launch_bounds__(kFastBS, GT_FAST_MINB)
 fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
   constexpr bool HAS_EX = (PROTO == GT_PROTO_CSR);
@@ -634,7 +634,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         sdl[(SC_FILT) * kFastBS] = filt;
         const double trend = S_(filt, prev);
         double b_basal = 0.0, b_bolus = 0.0, b_gluc = 0.0;
-        if (a.controller == GT_CTRL_PID_PUMP) {
+        if (CTRL == GT_CTRL_PID_PUMP) {   // the controller is a template parameter: one per kernel
           // ---- PID + pump quantisation (pid.py pid_step_vec), same filter;
           // slots: SC_WEND = integral, SC_SUSP = pump carry
           const double e = S_(filt, H[1]);
@@ -1000,10 +1000,10 @@ static int choose_chunks(int64_t warps, int64_t slots, int n_ctl) {
   return best;
 }
 
-template <int PROTO, int NOISE, typename R, bool AGG, bool TRACE>
+template <int PROTO, int NOISE, typename R, bool AGG, bool TRACE, int CTRL>
 static int launch_sched(const gt_fast_args* a, const gt::Uni& u, cudaStream_t st) {
   constexpr int kDyn = gt::kHistWords * gt::kFastBS * 4;
-  auto kern = gt::fast_kernel<PROTO, NOISE, R, AGG, TRACE>;
+  auto kern = gt::fast_kernel<PROTO, NOISE, R, AGG, TRACE, CTRL>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
@@ -1060,8 +1060,12 @@ static int launch_sched(const gt_fast_args* a, const gt::Uni& u, cudaStream_t st
 
 template <int PROTO, int NOISE, typename R = double, bool AGG = false>
 static int launch_one(const gt_fast_args* a, const gt::Uni& u, cudaStream_t st) {
-  if (a->trace) return launch_sched<PROTO, NOISE, R, AGG, true>(a, u, st);
-  return launch_sched<PROTO, NOISE, R, AGG, false>(a, u, st);
+  const bool pid = a->controller == GT_CTRL_PID_PUMP;
+  if (a->trace)
+    return pid ? launch_sched<PROTO, NOISE, R, AGG, true, GT_CTRL_PID_PUMP>(a, u, st)
+               : launch_sched<PROTO, NOISE, R, AGG, true, GT_CTRL_DUAL_HORMONE>(a, u, st);
+  return pid ? launch_sched<PROTO, NOISE, R, AGG, false, GT_CTRL_PID_PUMP>(a, u, st)
+             : launch_sched<PROTO, NOISE, R, AGG, false, GT_CTRL_DUAL_HORMONE>(a, u, st);
 }
 
 // The fused kernel's noise stream, materialised: out[(i * n_ticks + j) * 4 + l]
