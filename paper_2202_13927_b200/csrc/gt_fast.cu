@@ -232,6 +232,15 @@ __device__ __forceinline__ long long warp_max64(long long v) {
   return v;
 }
 
+// Exact per-warp timeline partials on 64-bit values (rare: a live BG >= 128
+// mmol/L or non-finite); out of line to keep the step loop small.
+__device__ __noinline__ void timeline_partials64(bool alive, long long v, long long& ssum, long long& smin,
+                                                 long long& smax) {
+  ssum = warp_sum64(alive ? v : 0LL);
+  smin = warp_min64(alive ? v : LLONG_MAX);
+  smax = warp_max64(alive ? v : LLONG_MIN);
+}
+
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -790,9 +799,21 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       if (tick && ctl == next_grid_ctl) {  // timeline point (warp-uniform)
         next_grid_ctl += u.grid_ctl;
         const long long v = __double2ll_rn(bg * kFpScale);
-        const long long ssum = warp_sum64(alive ? v : 0LL);
-        const long long smin = warp_min64(alive ? v : LLONG_MAX);
-        const long long smax = warp_max64(alive ? v : LLONG_MIN);
+        // 0 <= v < 2^31 (bg < 128 mmol/L) for every live lane: four 32-bit
+        // REDUX; otherwise (or a NaN) the exact 64-bit shuffle path, out of line
+        long long ssum, smin, smax;
+        if (__builtin_expect(__any_sync(0xffffffffu, alive && (v < 0 || v > 0x7FFFFFFELL)), 0)) {
+          timeline_partials64(alive, v, ssum, smin, smax);
+        } else {
+          const unsigned vv = alive ? (unsigned)v : 0u;
+          const unsigned lo = __reduce_add_sync(0xffffffffu, vv & 0xFFFFu);
+          const unsigned hi = __reduce_add_sync(0xffffffffu, vv >> 16);
+          const unsigned mn = __reduce_min_sync(0xffffffffu, alive ? vv : 0xFFFFFFFFu);
+          const int mx = __reduce_max_sync(0xffffffffu, alive ? (int)vv : -1);
+          ssum = ((long long)hi << 16) + (long long)lo;
+          smin = mn == 0xFFFFFFFFu ? LLONG_MAX : (long long)mn;
+          smax = mx < 0 ? LLONG_MIN : (long long)mx;
+        }
         if (lane == 0) {
           GT_CHECK(g_idx >= 0 && g_idx < a.n_grid, "timeline");
           GT_CHECK(g_idx >= 0 && g_idx < a.n_grid, "timeline tail");
