@@ -347,6 +347,66 @@ def run_ours(args):
     return 0
 
 
+def run_trial1m(args):
+    """BASELINE configs[2] / the north_star's headline trial: 1M patients x 52
+    weeks, seed 2, strong-scaled over the launched ranks (each rank samples and
+    simulates shard_range(1M, rank, world) with global-id streams; the exact
+    accumulators are combined with NCCL).  Wall-clock = device sampler +
+    staging + fused kernel + reduction + combine, max over ranks."""
+    import torch
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=device)
+    from paper_2202_13927_b200 import analytics
+    from paper_2202_13927_b200.config import SimulationConfig
+    from paper_2202_13927_b200.parallel import allreduce_accumulator, shard_range
+    from paper_2202_13927_b200.population import generate_population
+    from paper_2202_13927_b200.protocol import ThreeMealProtocol
+    from paper_2202_13927_b200.trial import FastTrial
+    n_total, weeks = args.patients if args.patients != N_PATIENTS else 1_000_000, 52
+    cfg = SimulationConfig(horizon_s=weeks * 7 * 86400.0, seed=2, dt_s=DT_S)
+    prof, _code, ctl_label = controller_setup(args.controller)
+    lo, hi = shard_range(n_total, rank, ws)
+    walls = []
+    for it in range(args.warmup + args.steps):
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        pop = generate_population(2, hi - lo, pid0=lo, device=device, on_exhausted="redraw_weight")
+        ft = FastTrial(lo, pop.params_device, pop.basal_device, ThreeMealProtocol(), prof, cfg,
+                       controller_id=args.controller, device=device, per_patient_metrics=True)
+        ft.step()
+        acc = ft.accumulator()
+        if ws > 1:
+            acc = allreduce_accumulator(acc, device)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        if ws > 1:
+            t = torch.tensor([wall], device=device)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            wall = float(t.item())
+        if it >= args.warmup:
+            walls.append(wall)
+        del ft, pop
+    if rank == 0:
+        w = float(np.median(walls))
+        print(json.dumps({
+            "metric": "1M-patient x 52-week trial wall-clock", "value": w, "unit": "s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": False, "scaling": "strong",
+            "patient_weeks_per_s": n_total * weeks / w, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"BASELINE configs[2]: {n_total} patients x {weeks} weeks, seed 2, dt 60 s",
+                       "controller": ctl_label, "protocol": "three_meal",
+                       "timed": "sampler + staging + fused kernel + reduction + NCCL combine (host wall, max over ranks)"},
+            "quantiles": analytics.metric_quantiles(acc)}), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -356,7 +416,11 @@ def main():
     ap.add_argument("--patients", type=int, default=N_PATIENTS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--controller", default="pid_pump", choices=["pid_pump", "dual_hormone"])
+    ap.add_argument("--workload", default="c1", choices=["c1", "trial1m"],
+                    help="c1: BASELINE configs[1] throughput (default); trial1m: the 1M x 52 w trial wall-clock")
     args = ap.parse_args()
+    if args.workload == "trial1m" and args.impl == "ours":
+        return run_trial1m(args)
     if args.impl == "reference":
         return run_reference_arm(args)
     return run_ours(args)
