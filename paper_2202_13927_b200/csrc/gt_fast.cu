@@ -123,6 +123,11 @@ __device__ __forceinline__ float zero_if_neg(float x) { return x < 0.0f ? 0.0f :
 __device__ __forceinline__ float pos_or_zero(float x) { return x > 0.0f ? x : 0.0f; }
 __device__ __forceinline__ float lt_or(float x, float c) { return x < c ? x : c; }
 
+// Opaque copy: the compiler must keep the value (or spill it) rather than
+// rematerialise it from its inputs (e.g. a reload of the parameters from HBM).
+__device__ __forceinline__ double opaque(double x) { double r; asm("mov.b64 %0, %1;" : "=d"(r) : "d"(x)); return r; }
+__device__ __forceinline__ float opaque(float x) { float r; asm("mov.b32 %0, %1;" : "=f"(r) : "f"(x)); return r; }
+
 // explicit-rounding multiply / fma in the integrator precision (no mixed
 // overloads: a double constant reaching the FP32 integrator fails to compile)
 __device__ __forceinline__ double MR_(double a, double b) { return __dmul_rn(a, b); }
@@ -270,7 +275,9 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
   // s_thr[k+1] = bits of THRESHOLDS[k]; s_thr[0] = -inf, s_thr[247] = +inf
   __shared__ long long s_thr[GT_N_THRESHOLDS + 2];
   __shared__ double s_hyper[GT_N_HYPER];
-  __shared__ double s_hc[5];  // hyper-derived controller constants (same IEEE values)
+  __shared__ double s_hc[6];  // hyper-derived controller constants (same IEEE values)
+  constexpr int kPulseTab = 64;
+  __shared__ double s_prate[kPulseTab];  // PID: basal rate of p whole pulses, (p * q) / P_h
   extern __shared__ uint32_t s_hist[];  // [kHistWords * kFastBS], dynamic (> 48 KB total)
   __shared__ double s_d[N_SC * kFastBS];   // [field][lane], flat
   __shared__ int32_t s_i[N_SI * kFastBS];
@@ -291,12 +298,19 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
     s_hc[2] = M_(s_hyper[HLOCKMIN], 60.0);
     s_hc[3] = A_(s_hyper[HGLUCTHR], s_hyper[HHYST]);
     s_hc[4] = A_(s_hyper[HEXGLUCTHR], s_hyper[HHYST]);
+    s_hc[5] = CTRL == GT_CTRL_PID_PUMP ? D_(1.0, s_hyper[7]) : 0.0;  // PID: RN(1 / pulse size)
   }
+  if (CTRL == GT_CTRL_PID_PUMP)
+    for (int q = tid; q < kPulseTab; q += kFastBS) s_prate[q] = D_(M_((double)q, s_hyper[7]), u.pid_ph);
   __syncthreads();  // no block-wide barrier after this point: warps run independently
 
   const int lane = tid & 31;
-  double* const sdl = s_d + tid;   // this lane's controller / extremes slots, field stride kFastBS
-  int32_t* const sil = s_i + tid;
+  // this lane's controller / extremes slots, field stride kFastBS; the lane
+  // index is opaque so the base is kept instead of rebuilt from SR_TID
+  int tid_o;
+  asm("mov.b32 %0, %1;" : "=r"(tid_o) : "r"(tid));
+  double* const sdl = s_d + tid_o;
+  int32_t* const sil = s_i + tid_o;
   const int64_t n = a.n;
   const int64_t n_warps = sch.n_warps;
   const double* __restrict__ H = s_hyper;
@@ -346,7 +360,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       for (int k = 0; k < NP; ++k) p[k] = a.params[ii * NP + k];
       make_pc(p, u, pc);
     }
-    R sqE = pc.sqE, sqG = (R)u.sqG;
+    R sqE = opaque(pc.sqE), sqG = (R)u.sqG;   // kept, not re-derived from the parameters in HBM
     if (NOISE == GT_NOISE_INJECTED && a.has_noise[ii] == 0) { sqE = 0; sqG = 0; }
     int64_t moff = 0, n_meals_csr = 0, ex_lo = 0, n_ex = 0;
     if (PROTO == GT_PROTO_CSR) {
@@ -656,11 +670,18 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           if (factor < 0.0) factor = 0.0;
           if (factor > H[5]) factor = H[5];
           const double vol = A_(M_(M_(sdl[(SC_ASSUMED) * kFastBS], factor), ph), sdl[(SC_SUSP) * kFastBS]);
-          double pulses = floor(D_(vol, H[7]));
+          // floor(vol / q) of the IEEE quotient: vol * RN(1/q) is within 1e-13
+          // of it, so its floor is exact unless it lies within 1e-9 of an
+          // integer (then the division is done)
+          const double qf = M_(vol, s_hc[5]);
+          double pulses = floor(qf);
+          const double fr = S_(qf, pulses);
+          if (!(fr > 1e-9 && fr < 1.0 - 1e-9 && qf < 1e6)) pulses = floor(D_(vol, H[7]));
           if (pulses < 0.0) pulses = 0.0;
           const double delivered = M_(pulses, H[7]);
           sdl[(SC_SUSP) * kFastBS] = S_(vol, delivered);
-          b_basal = D_(delivered, ph);
+          // (p * q) / P_h from the table (same operations), else computed
+          b_basal = pulses < (double)kPulseTab ? s_prate[(int)pulses] : D_(delivered, ph);
           if (announced > 0.0) {
             double bb = D_(announced, sdl[(SC_ICR) * kFastBS]);
             if (bb > H[9]) bb = H[9];

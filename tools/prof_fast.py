@@ -22,8 +22,9 @@ weeks = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 proto = sys.argv[4] if len(sys.argv) > 4 else "three_meal"
 ctrl = sys.argv[5] if len(sys.argv) > 5 else "dual_hormone"
+dt_s = float(sys.argv[6]) if len(sys.argv) > 6 else 60.0
 dev = torch.device("cuda", 0)
-cfg = SimulationConfig(horizon_s=weeks * 7 * 86400.0, seed=1, dt_s=60.0)
+cfg = SimulationConfig(horizon_s=weeks * 7 * 86400.0, seed=1, dt_s=dt_s)
 pop = generate_population(1, n, device=dev, on_exhausted="redraw_weight")
 if proto == "northern":
     from paper_2202_13927_b200.northern import NorthernYearProtocol
@@ -42,4 +43,7 @@ for r in range(reps):
     ft.step()
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    print(f"rep {r}: {dt * 1000:.2f} ms  {n * weeks / dt:.4g} patient-weeks/s", flush=True)
+    from paper_2202_13927_b200 import flops
+    tf = flops.flops_per_step(ft.sz["period_steps"], ctrl) * n * ft.sz["horizon_ticks"] / dt / 1e12
+    print(f"rep {r}: {dt * 1000:.2f} ms  {n * weeks / dt:.4g} patient-weeks/s  {tf:.2f} TFLOP/s (wall, incl. reduce)",
+          flush=True)

@@ -224,9 +224,32 @@ def c3(dev, scale):
     return treatment_comparison(max(1000, int(250_000 * scale)), 12, seed=3, device=dev, controller_id=CTRL)
 
 
+def _peaks():
+    """Measured DFMA / FFMA peaks (tools/fp64_peak.cu, profiles/fp64_peak_r01.jsonl)."""
+    best = {"dfma": 0.0, "ffma": 0.0}
+    for line in open(os.path.join(ROOT, "profiles", "fp64_peak_r01.jsonl")):
+        d = json.loads(line)
+        if d.get("kernel") in best:
+            best[d["kernel"]] = max(best[d["kernel"]], d["tflops"])
+    return best
+
+
 def c4(dev, scale):
+    from paper_2202_13927_b200 import flops
     from paper_2202_13927_b200.studies import precision_study
-    return precision_study(max(1000, int(250_000 * scale)), 12, seed=4, device=dev, controller_id=CTRL)
+    n, weeks = max(1000, int(250_000 * scale)), 12
+    out = precision_study(n, weeks, seed=4, device=dev, controller_id=CTRL)
+    peaks = _peaks()
+    for name, v in out["variants"].items():
+        ps = int(round(300.0 / v["dt_s"]))
+        steps = n * weeks * 7 * 86400.0 / v["dt_s"]
+        tf = flops.flops_per_step(ps, CTRL) * steps / (v["sim_ms"] / 1000.0) / 1e12
+        peak = peaks["ffma"] if v["integrator"] == "fp32" else peaks["dfma"]
+        v["roofline"] = {"achieved_tflops": tf, "peak_tflops": peak, "frac": tf / peak,
+                         "peak": "measured FFMA" if v["integrator"] == "fp32" else "measured DFMA",
+                         "note": "algorithmic flops of the reference (flops.py); the FP32 variant keeps the "
+                                 "controller and statistics in FP64"}
+    return out
 
 
 def main():
