@@ -61,7 +61,7 @@ struct Uni {
   double sqG, sigEh, sqrtR, rK1, pred_k, u_basal_k, u_bolus_k, u_gluc_k;
   double dt, period, horizon_s, meal_dur_min, rs_agg, pid_ph;
   int32_t ps, n_ctl, ctl_per_day, grid_ctl, hypoL, agg;
-  uint32_t rk[20];  // Philox round keys (k0 + r*W0, k1 + r*W1): constant-bank operands
+  uint32_t nz_c2, nz_c3;  // noise counter words 2-3: seed_lo, seed_hi ^ role << 24
 };
 
 // Persistent work distribution (see the header comment).
@@ -159,17 +159,21 @@ __device__ __forceinline__ void mulwide(uint32_t a, uint32_t b, uint32_t& lo, ui
   asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(p));
 }
 
-// Philox4x32-10 with the round keys precomputed in the kernel-parameter
-// bank: per round 2 IMAD.WIDE.U32 + 2 LOP3 (3-input XOR with a c[] key).
-__device__ __forceinline__ U4 philox_fast(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
-                                          const uint32_t* __restrict__ rk) {
+// Noise stream: Philox4x32-10 under a FIXED key, so the 20 round keys are
+// compile-time immediates of the LOP3s (no uniform registers, no constant
+// loads); the trial seed enters the counter instead:
+//   counter = (index, pid, seed_lo, seed_hi ^ role << 24)
+// which is injective in (index, pid, seed) for the one role the kernel draws.
+// Per round: 2 IMAD.WIDE.U32 + 2 LOP3.
+constexpr uint32_t kNoiseKey0 = 0xA4093822u, kNoiseKey1 = 0x299F31D0u;  // digits of pi
+__device__ __forceinline__ U4 philox_fast(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3) {
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
     uint32_t lo0, hi0, lo1, hi1;
     mulwide(c0, 0xD2511F53u, lo0, hi0);
     mulwide(c2, 0xCD9E8D57u, lo1, hi1);
-    const uint32_t n0 = hi1 ^ c1 ^ rk[2 * r];
-    const uint32_t n2 = hi0 ^ c3 ^ rk[2 * r + 1];
+    const uint32_t n0 = hi1 ^ c1 ^ (kNoiseKey0 + (uint32_t)r * 0x9E3779B9u);
+    const uint32_t n2 = hi0 ^ c3 ^ (kNoiseKey1 + (uint32_t)r * 0xBB67AE85u);
     c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
   }
   return U4{c0, c1, c2, c3};
@@ -536,7 +540,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       auto draw_noise = [&]() {
         if (NOISE == GT_NOISE_PHILOX) {
           if (!AGG) {
-            const U4 r = philox_fast((uint32_t)k, pid, a.noise_role, 0u, u.rk);
+            const U4 r = philox_fast((uint32_t)k, pid, u.nz_c2, u.nz_c3);
             float f0, f1, f2, f3;
             box_muller(r.x, r.y, f0, f1);
             box_muller(r.z, r.w, f2, f3);
@@ -549,7 +553,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
             R s0 = 0, s1 = 0, s2 = 0;
             const uint32_t kf = (uint32_t)k * (uint32_t)u.agg;
             for (int j = 0; j < u.agg; ++j) {
-              const U4 r = philox_fast(kf + (uint32_t)j, pid, a.noise_role, 0u, u.rk);
+              const U4 r = philox_fast(kf + (uint32_t)j, pid, u.nz_c2, u.nz_c3);
               float f0, f1, f2, f3;
               box_muller(r.x, r.y, f0, f1);
               box_muller(r.z, r.w, f2, f3);
@@ -1019,11 +1023,8 @@ static Uni make_uni(const gt_fast_args& a) {
   u.agg = a.noise_agg < 1 ? 1 : a.noise_agg;
   u.rs_agg = 1.0 / std::sqrt((double)u.agg);
   u.pid_ph = a.period_s / 3600.0;
-  uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
-  for (int r = 0; r < 10; ++r) {
-    u.rk[2 * r] = k0; u.rk[2 * r + 1] = k1;
-    k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
-  }
+  u.nz_c2 = (uint32_t)a.seed;
+  u.nz_c3 = (uint32_t)(a.seed >> 32) ^ (a.noise_role << 24);
   return u;
 }
 
@@ -1114,12 +1115,12 @@ static int launch_one(const gt_fast_args* a, const gt::Uni& u, cudaStream_t st) 
 // = normal l of tick k0 + j of patient pid0 + i, drawn exactly as the kernel
 // draws it (philox_fast + FP32 SFU Box-Muller; lanes 0-2 = Wiener, 3 = CGM).
 namespace gt {
-__global__ void noise_normals_kernel(int64_t n, int64_t pid0, uint32_t role, int64_t k0, int64_t n_ticks,
-                                     const Uni u, float* out) {
+__global__ void noise_normals_kernel(int64_t n, int64_t pid0, int64_t k0, int64_t n_ticks, const Uni u,
+                                     float* out) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= n * n_ticks) return;
   const int64_t i = idx / n_ticks, j = idx - i * n_ticks;
-  const U4 r = philox_fast((uint32_t)(k0 + j), (uint32_t)(pid0 + i), role, 0u, u.rk);
+  const U4 r = philox_fast((uint32_t)(k0 + j), (uint32_t)(pid0 + i), u.nz_c2, u.nz_c3);
   float f0, f1, f2, f3;
   box_muller(r.x, r.y, f0, f1);
   box_muller(r.z, r.w, f2, f3);
@@ -1132,13 +1133,10 @@ int gt_launch_noise_normals(int64_t n, int64_t pid0, uint64_t seed, uint32_t rol
                             int64_t n_ticks, float* out, cudaStream_t st) {
   if (n <= 0 || n_ticks <= 0) return GT_OK;
   gt::Uni u{};
-  uint32_t key0 = (uint32_t)seed, key1 = (uint32_t)(seed >> 32);
-  for (int r = 0; r < 10; ++r) {
-    u.rk[2 * r] = key0; u.rk[2 * r + 1] = key1;
-    key0 += 0x9E3779B9u; key1 += 0xBB67AE85u;
-  }
+  u.nz_c2 = (uint32_t)seed;
+  u.nz_c3 = (uint32_t)(seed >> 32) ^ (role << 24);
   const int64_t total = n * n_ticks;
-  gt::noise_normals_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(n, pid0, role, k0, n_ticks, u, out);
+  gt::noise_normals_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(n, pid0, k0, n_ticks, u, out);
   return gt_check_launch("noise_normals_kernel");
 }
 
