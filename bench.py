@@ -131,6 +131,17 @@ def controller_setup(controller_id: str):
     return ControllerHyperparameters(), 0, "dual_hormone (reference AP: PD basal + heuristic meal bolus)"
 
 
+CPU_SAMPLE_SECONDS = 10.0   # target CPU work per baseline sample
+
+
+def cpu_sample_size(weeks: int, threads: int, controller_id: str) -> int:
+    """Patients per CPU-baseline sample: a short pilot run sizes the sample
+    to about CPU_SAMPLE_SECONDS of work on this host."""
+    pilot = max(threads * 16, 128)
+    rate, _wall = cpu_baseline(pilot, weeks, threads, controller_id)
+    return int(min(max(pilot, rate * CPU_SAMPLE_SECONDS / weeks), 400_000))
+
+
 def cpu_baseline(n_sample: int, weeks: int, threads: int, controller_id: str = "pid_pump"):
     """Reference path on the host cores: the oracle's C restatement of the
     numba kernel (bitwise equal to it on injected inputs), OpenMP over
@@ -179,7 +190,7 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    n_sample = max(threads * 64, 512)
+    n_sample = cpu_sample_size(WEEKS, threads, args.controller)
     vals = []
     for i in range(args.warmup + args.steps):
         v, wall = cpu_baseline(n_sample, WEEKS, threads, args.controller)
@@ -304,7 +315,7 @@ def run_ours(args):
     cpu_v, cpu_wall = (None, None)
     if not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        cpu_n = max(threads * 64, 512)
+        cpu_n = cpu_sample_size(WEEKS, threads, args.controller)
         cpu_v, cpu_wall = cpu_baseline(cpu_n, WEEKS, threads, args.controller)
     q = analytics.metric_quantiles(acc_all)
     h2d = params_h.numel() * 8 + basal_h.numel() * 8
@@ -329,7 +340,7 @@ def run_ours(args):
                      "flops_per_step": F, "peak_source": peak_src,
                      "kernel_ms": sim_s * 1000.0, "share_of_step": float(np.mean(sim_ms) / np.mean(step_ms))},
         "cpu_baseline": ({"value": cpu_v, "unit": "patient-weeks/s", "cores": os.cpu_count(), "kind": "port",
-                          "sample": f"{max((os.cpu_count() or 1) * 64, 512)} patients x {WEEKS} weeks (oracle C "
+                          "sample": f"{cpu_n} patients x {WEEKS} weeks (oracle C "
                                     f"restatement, OpenMP, {cpu_wall:.1f} s wall)"} if cpu_v else None),
         "e2e": {"value": pw_per_step / (e2e / 1000.0), "unit": "patient-weeks/s",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
