@@ -141,17 +141,6 @@ template <typename R> struct kNonfiniteBits;
 template <> struct kNonfiniteBits<double> { static constexpr unsigned v = 0x7ff00000u; };
 template <> struct kNonfiniteBits<float> { static constexpr unsigned v = 0x7f800000u; };
 
-// Rare path of the shared histogram: counter `ha` of bin kb reached 255;
-// add it to the lane's HBM column and clear it.  Out of line so the column
-// address is computed only when a counter actually fills (inlined, the
-// compiler hoists that 64-bit address arithmetic into every step).
-__device__ __noinline__ void drain_bin(int32_t* __restrict__ bg_hist, int64_t n, int64_t warp_global, int kb,
-                                       uint32_t ha) {
-  const int64_t i = warp_global * 32 + (threadIdx.x & 31);
-  if (kb < GT_N_BG_BINS && i < n) atomicAdd(&bg_hist[(int64_t)kb * n + i], 255);
-  asm volatile("st.shared.u8 [%0], 0;" :: "r"(ha));
-}
-
 // ------------------------------------------------------------ noise
 __device__ __forceinline__ void mulwide(uint32_t a, uint32_t b, uint32_t& lo, uint32_t& hi) {
   uint64_t p;
@@ -805,8 +794,13 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           uint32_t c;
           asm volatile("{\n\t.reg .u32 t;\n\tld.shared.u8 t, [%1];\n\tadd.u32 %0, t, 1;\n\t"
                        "st.shared.u8 [%1], %0;\n\t}" : "=r"(c) : "r"(ha));
-          if (__builtin_expect(c == 255u, 0))  // a full counter drains into the HBM column
-            drain_bin(a.bg_hist, n, warp_global, kb, ha);
+          {  // a full counter drains into the HBM column: predicated RED + clear, no branch
+            const int32_t* col = a.bg_hist + ((int64_t)min(kb, GT_N_BG_BINS - 1) * n + ii);
+            const uint32_t ok = (kb < GT_N_BG_BINS && inrange) ? 1u : 0u;
+            asm volatile("{\n\t.reg .pred p, q;\n\tsetp.eq.u32 p, %0, 255;\n\tsetp.ne.and.u32 q, %3, 0, p;\n\t"
+                         "@q red.global.add.u32 [%1], 255;\n\t@p st.shared.u8 [%2], 0;\n\t}"
+                         :: "r"(c), "l"(col), "r"(ha), "r"(ok) : "memory");
+          }
         }
         bg_sum += bg;
         // extremes: only a tick in the lowest/highest bin so far can move them;
