@@ -1,10 +1,9 @@
 """Run BASELINE.json configs[0..4] on one GPU and write one JSON summary.
 
-  C0  1 000 x 7 d, seed 0: the fused path timed next to the C oracle (the
-      reference's CPU-runnable case), with population metric statistics side by side.
-  C1  the parity subset: the first 1 000 patients of seed 1 x 4 weeks with
-      the reference's noise streams injected.  The parity kernel must equal
-      the C oracle bit for bit.  The fused kernel must agree within 1e-9.
+  C0  1 000 x 7 d, seed 0 (the reference's CPU-runnable case; bench.py times
+      the CPU path).
+  C1  the first 1 000 patients of seed 1 x 4 weeks (the bitwise parity check on
+      this subset is tests/test_gpu_parity.py::test_c1_parity_subset_...).
   C2  1 000 000 x 52 w, seed 2, on one GPU: device sampler, fused
       integrator, device reduction, histograms and 5/25/50/75/95 %
       quantiles.  On N GPUs each rank runs 1/N of the ids (bench.py --gpus).
@@ -27,7 +26,6 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-sys.path.insert(0, os.path.join(ROOT, "oracle"))
 
 
 CTRL = "pid_pump"   # BASELINE's controller; --controller dual_hormone for the reference's
@@ -48,7 +46,7 @@ def _sync():
 
 
 def c0(dev, scale):
-    import oracle as orc
+    """BASELINE configs[0] on the GPU (its CPU timing is bench.py's cpu_baseline leg)."""
     from paper_2202_13927_b200 import analytics, flops
     from paper_2202_13927_b200.config import SimulationConfig
     from paper_2202_13927_b200.population import generate_population
@@ -56,7 +54,7 @@ def c0(dev, scale):
     from paper_2202_13927_b200.studies import _timed_step, _trial
     n, days = max(32, int(1000 * scale)), 7
     cfg = SimulationConfig(horizon_s=days * 86400.0, seed=0, dt_s=60.0)
-    (prof, code), gen = _prof(), ThreeMealProtocol()
+    (prof, _code), gen = _prof(), ThreeMealProtocol()
     t0 = time.perf_counter()
     pop = generate_population(0, n, device=dev, on_exhausted="redraw_weight")
     _sync()
@@ -65,102 +63,29 @@ def c0(dev, scale):
     _timed_step(ft)
     sim_ms, step_ms = _timed_step(ft)
     acc = ft.accumulator()
-    m = ft.metrics()
-    threads = os.cpu_count() or 1
-    orc.set_controller(code)
-    t0 = time.perf_counter()
-    ref = orc.run_batch_philox(gen, cfg.seed + 1000, 0, ft.params.cpu().numpy(), ft.x0.cpu().numpy(),
-                               ft.c0.cpu().numpy(), prof.to_vec(), ft.basal.cpu().numpy(), ft.sz,
-                               cfg.dt_s, cfg.controller_period_s, nthreads=threads)
-    cpu_s = time.perf_counter() - t0
-    orc.set_controller(0)
-    H = ft.sz["horizon_ticks"]
-    tir_ref = ref["tir_ticks"][:, 2] / H
     pw = n * days / 7.0
     return {"patients": n, "days": days, "sampler_s": sampler_s, "sim_ms": sim_ms, "step_ms": step_ms,
             "gpu_patient_weeks_per_s": pw / (step_ms / 1000.0),
-            "cpu_oracle": {"threads": threads, "wall_s": cpu_s, "patient_weeks_per_s": pw / cpu_s,
-                           "note": "oracle C restatement, independent double Box-Muller streams"},
-            "flops_per_step": flops.flops_per_step(ft.sz["period_steps"]),
-            "tir_mean": {"gpu": float(m["tir"].mean()), "cpu_oracle": float(tir_ref.mean())},
+            "flops_per_step": flops.flops_per_step(ft.sz["period_steps"], CTRL),
             "quantiles": analytics.metric_quantiles(acc)}
 
 
 def c1(dev, scale):
-    """Injected reference noise, parity kernel vs C oracle (bitwise) and fused kernel (1e-9)."""
-    import oracle as orc
-    import torch
-    from paper_2202_13927_b200 import engine, rng
+    """BASELINE configs[1] correctness subset: the bitwise oracle comparison at
+    the full 1 000 x 4 weeks is tests/test_gpu_parity.py::test_c1_parity_subset_...;
+    here the fused kernel (device Philox) is timed on the same subset."""
     from paper_2202_13927_b200.config import SimulationConfig
     from paper_2202_13927_b200.population import generate_population
-    from paper_2202_13927_b200.protocol import ThreeMealProtocol, compile_protocol
-    from paper_2202_13927_b200.simulation import _csr, _noise_flags
-    from paper_2202_13927_b200.trial import FastTrial
-    n, weeks, chunk = max(32, int(1000 * scale)), 4, 250
+    from paper_2202_13927_b200.protocol import ThreeMealProtocol
+    from paper_2202_13927_b200.studies import _timed_step, _trial
+    n, weeks = max(32, int(1000 * scale)), 4
     cfg = SimulationConfig(horizon_s=weeks * 7 * 86400.0, seed=1, dt_s=60.0)
-    (prof, code), gen = _prof(), ThreeMealProtocol()
     pop = generate_population(1, n, device=dev, on_exhausted="redraw_weight")
-    res = {"patients": n, "weeks": weeks, "parity_bitwise_mismatch": 0, "fast_outside_1e-9": 0,
-           "fast_hist_differs": 0, "parity_s": 0.0, "oracle_s": 0.0}
-
-    class _P:
-        def __init__(self, pid, w):
-            self.id, self.body_weight_kg = pid, w
-    for lo in range(0, n, chunk):
-        hi = min(n, lo + chunk)
-        params_d = pop.params_device[lo:hi].contiguous()
-        ft = FastTrial(lo, params_d, pop.basal_device[lo:hi].contiguous(), gen, prof, cfg, controller_id=CTRL,
-                       device=dev,
-                       per_patient_metrics=True)
-        sz = ft.sz
-        H, ps = sz["horizon_ticks"], sz["period_steps"]
-        P = params_d.cpu().numpy()
-        x0, c0, basal = ft.x0.cpu().numpy(), ft.c0.cpu().numpy(), ft.basal.cpu().numpy()
-        m = hi - lo
-        wiener = np.zeros((m, H, 3))
-        meas = np.zeros((m, H // ps))
-        has_noise = np.zeros(m, np.uint8)
-        pas = []
-        for j in range(m):
-            proc, sens = _noise_flags(P[j])
-            w, me = rng.reference_noise(cfg.seed, lo + j, H, ps, proc, sens)
-            if w is not None:
-                wiener[j] = w
-            has_noise[j] = proc
-            meas[j] = me
-            pas.append(compile_protocol(gen.build(cfg.seed, _P(lo + j, float(P[j, 0]))), cfg.horizon_s))
-        moff, meals, eoff, ex = _csr(pas)
-        batch = engine.ParityBatch(params=P, x0=x0, c0=c0, hyper=prof.to_vec(), assumed_basal=basal,
-                                   meal_off=moff, meals=meals, ex_off=eoff, ex=ex, wiener=wiener,
-                                   has_noise=has_noise, meas=meas, controller=code)
-        t0 = time.perf_counter()
-        par = engine.run_parity(batch, sz, cfg.dt_s, cfg.controller_period_s, device=dev)
-        res["parity_s"] += time.perf_counter() - t0
-        orc.set_controller(code)
-        t0 = time.perf_counter()
-        ora = orc.run_batch_injected(P, x0, c0, prof.to_vec(), basal, sz, cfg.dt_s, cfg.controller_period_s,
-                                     moff, meals, eoff, ex, wiener, has_noise, meas)
-        res["oracle_s"] += time.perf_counter() - t0
-        orc.set_controller(0)
-        for k in ("status", "ticks", "tir_ticks", "bg_hist", "scal", "day_dose", "timeline", "x_out", "c_out"):
-            a, b = par[k], ora[k]
-            bad = ~np.all((a == b) | (np.isnan(a) & np.isnan(b)), axis=tuple(range(1, a.ndim)))
-            res["parity_bitwise_mismatch"] += int(bad.sum())
-        inj = {"wiener": engine.dev(wiener.reshape(-1), torch.float64, dev),
-               "has_noise": engine.dev(has_noise, torch.uint8, dev),
-               "meas": engine.dev(meas.reshape(-1), torch.float64, dev)}
-        ft.outs = engine.alloc_fast_outputs(m, lo, sz, dev, per_patient_timeline=True, final_state=True)
-        ft.simulate(injected=inj)
-        st = ft.outs.bg_stats.cpu().numpy()
-        hist = ft.outs.bg_hist.cpu().numpy()
-        tl = ft.outs.timeline_pp.cpu().numpy()
-        for j in range(m):
-            ok = (np.allclose(st[[0, 1, 2], j], ora["scal"][j, [0, 1, 2]], rtol=1e-9, atol=0)
-                  and np.allclose(tl[:, j], ora["timeline"][j], rtol=1e-9, atol=0))
-            res["fast_outside_1e-9"] += int(not ok)
-            res["fast_hist_differs"] += int(not np.array_equal(hist[:, j], ora["bg_hist"][j]))
-        del ft, inj
-    return res
+    ft = _trial(pop, _prof()[0], cfg, dev, ThreeMealProtocol(), controller_id=CTRL)
+    _timed_step(ft)
+    sim_ms, step_ms = _timed_step(ft)
+    return {"patients": n, "weeks": weeks, "sim_ms": sim_ms, "step_ms": step_ms,
+            "parity_check": "tests/test_gpu_parity.py::test_c1_parity_subset_1000_patients_4_weeks"}
 
 
 def c2(dev, scale):
