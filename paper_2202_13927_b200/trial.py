@@ -288,3 +288,38 @@ def run_population_arrays(params_host, basal_host, generator, profile, config, *
                    hypo_min_s=hypo_min_s, per_patient_metrics=True)
     ft.step()
     return ft.accumulator(), ft.metrics()
+
+
+def fast_bytes_per_patient(config) -> int:
+    """Device bytes one patient occupies in a FastTrial (outputs, inputs,
+    scratch; the NorthernYear CSR adds ~47 KB per patient on top)."""
+    sz = sizes(config)
+    return int(8 * (30 + 16 + 11 + 4) + 4 * 247 + 8 * 3 + 8 * 3 * sz["n_days"] + 4 * 2 + 8 + 4
+               + 24 * sz["n_grid"] / 32 + 404 + 4 * 5 + 64)
+
+
+def run_population_chunked(n: int, population_seed: int, generator, profile, config, *, pid0: int = 0,
+                           controller_id: str = "dual_hormone", device=None, chunk: int | None = None,
+                           hypo_min_s: float = 900.0, memory_fraction: float = 0.5) -> TrialAccumulator:
+    """Simulate global ids [pid0, pid0 + n) on one device in chunks sized to fit
+    ``memory_fraction`` of its free memory (or ``chunk`` patients), sampling
+    each chunk on the device and merging the exact accumulators.  Results
+    equal a single launch over all ids (pid-keyed streams, exact merge)."""
+    from .analytics import merge
+    from .population import generate_population
+    t = engine.torch()
+    device = engine.require_device(device)
+    if chunk is None:
+        free, _total = t.cuda.mem_get_info(device)
+        chunk = max(1024, int(free * memory_fraction / fast_bytes_per_patient(config)))
+    acc = None
+    for lo in range(pid0, pid0 + n, chunk):
+        m = min(chunk, pid0 + n - lo)
+        pop = generate_population(population_seed, m, pid0=lo, device=device, on_exhausted="redraw_weight")
+        ft = FastTrial(lo, pop.params_device, pop.basal_device, generator, profile, config, controller_id, device,
+                       hypo_min_s=hypo_min_s)
+        ft.step()
+        part = ft.accumulator()
+        acc = part if acc is None else merge(acc, part)
+        del ft, pop
+    return acc

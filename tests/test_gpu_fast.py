@@ -387,3 +387,21 @@ def test_validate_parameter_sets(dev):
     v = validate_parameter_sets(p, ub, device=dev)
     assert any("negative" in s for s in v[0]) and any("standard deviation" in s for s in v[1])
     assert any("below" in s for s in v[2]) and any("does not match" in s for s in v[3])
+
+
+def test_chunked_population_equals_single_launch(dev):
+    """run_population_chunked merges per-chunk exact accumulators: same report
+    as one launch over all ids (chunk boundaries at ragged sizes)."""
+    from paper_2202_13927_b200.config import SimulationConfig
+    from paper_2202_13927_b200.controller import ControllerHyperparameters
+    from paper_2202_13927_b200.population import generate_population
+    from paper_2202_13927_b200.protocol import ThreeMealProtocol
+    from paper_2202_13927_b200.trial import FastTrial, run_population_chunked
+    cfg = SimulationConfig(horizon_s=2 * 86400.0, seed=6, dt_s=60.0)
+    acc = run_population_chunked(700, 13, ThreeMealProtocol(), ControllerHyperparameters(), cfg, device=dev,
+                                 chunk=257)
+    pop = generate_population(13, 700, device=dev, on_exhausted="redraw_weight")
+    ft = FastTrial(0, pop.params_device, pop.basal_device, ThreeMealProtocol(), ControllerHyperparameters(), cfg,
+                   device=dev)
+    ft.step()
+    assert _acc_equal(acc, ft.accumulator())
