@@ -252,3 +252,19 @@ def test_empty_population_rejected():
     with pytest.raises(SimulationError):
         run_trial([], NorthernYearProtocol(), "dual_hormone", ControllerHyperparameters(), "hovorka_ext",
                   SimulationConfig(horizon_s=86400.0, seed=1))
+
+
+def test_merge_monoid_properties():
+    """analytics.merge is a commutative monoid (test_analytics.py:149-191
+    restated with hypothesis): identity, commutativity, associativity."""
+    from hypothesis import given, settings, strategies as st
+
+    @settings(max_examples=40, deadline=None)
+    @given(st.integers(0, 10_000), st.integers(0, 10_000), st.integers(0, 10_000))
+    def laws(sa, sb, sc):
+        a, b, c = _random_acc(sa), _random_acc(sb), _random_acc(sc)
+        empty = TrialAccumulator(60.0, 200, 1, 4, 3000.0)
+        assert _eq(merge(a, empty), a) and _eq(merge(empty, a), a)
+        assert _eq(merge(a, b), merge(b, a))
+        assert _eq(merge(merge(a, b), c), merge(a, merge(b, c)))
+    laws()
