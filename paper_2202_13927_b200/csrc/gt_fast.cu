@@ -1,18 +1,19 @@
 // Fast fused closed-loop integrator (BASELINE north_star subsystem 3).
 //
 // One thread = one virtual patient.  SDE state, Philox counters and per-step
-// accumulators live in registers; the 247-bin BG histogram of each patient
-// lives in shared memory as uint8 counters (a counter that reaches 255 drains
-// into the patient's HBM column; all drain at the end of a slice), and the state that changes only on
-// controller ticks (controller memory, meal window, dose sums, BG extremes)
-// lives in shared memory, so HBM sees parameters in and metrics out only.
+// accumulators live in registers.  The 247-bin BG histogram of each patient
+// lives in shared memory as uint8 counters: a counter that reaches 255
+// drains into the patient's HBM column (predicated RED), and all drain at the
+// end of a slice.  The state that changes only on controller ticks
+// (controller memory, meal window, dose sums, BG extremes) lives in shared
+// memory too, so HBM sees parameters in and metrics out only.
 //
 // Same model (hovorka.py:76-150), controller (controller.py:343-458) and
 // statistics (_kernel.py:137-160) as the parity kernel, re-associated for
 // the FP64 pipe: each linear update x += h*(b*y - x/tau) is evaluated as
 // fma(x, 1-h/tau, h*b*y) with per-patient constants folded at start-up and
-// launch-uniform constants (fixed parameters, Philox round keys) in the
-// kernel-parameter bank.  For every state of that form the reference's
+// launch-uniform constants (fixed parameters) in the kernel-parameter bank;
+// the noise Philox runs under a fixed key whose round keys are immediates.  For every state of that form the reference's
 // projection max(x,0) is a no-op (monotone rounding of a - b with
 // 0 <= b <= a), so it is applied only to Q1 and Q2 (and D1/D2 when arbitrary
 // noise is injected: device Philox normals are bounded by 6.7 sigma, far
