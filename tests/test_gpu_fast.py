@@ -405,3 +405,51 @@ def test_chunked_population_equals_single_launch(dev):
                    device=dev)
     ft.step()
     assert _acc_equal(acc, ft.accumulator())
+
+
+@pytest.mark.parametrize("horizon_h,dt_s,grid_s,slices", [(36, 30.0, 1800.0, 1), (36, 30.0, 1800.0, 3),
+                                                          (50, 20.0, 3600.0, 2), (25, 60.0, 7200.0, 0)])
+def test_fused_equals_parity_on_odd_horizons(dev, oracle, horizon_h, dt_s, grid_s, slices):
+    """Partial last day, non-hourly grid, other dt, sliced schedules: the fused
+    kernel (reference noise injected, CSR schedules) agrees with the parity
+    kernel -- itself bitwise equal to the reference -- to 1e-9, with identical
+    histograms apart from threshold ties."""
+    import torch
+    from paper_2202_13927_b200 import engine, rng
+    from paper_2202_13927_b200.config import SimulationConfig
+    from paper_2202_13927_b200.controller import ControllerHyperparameters
+    from paper_2202_13927_b200.population import generate_population
+    from paper_2202_13927_b200.protocol import ThreeMealProtocol, compile_protocol, compile_ticks
+    from paper_2202_13927_b200.simulation import _csr
+    from paper_2202_13927_b200.trial import FastTrial
+    cfg = SimulationConfig(horizon_s=horizon_h * 3600.0, seed=7, dt_s=dt_s, grid_step_s=grid_s)
+    n = 70
+    pop = generate_population(21, n, device=dev, on_exhausted="redraw_weight")
+    prof, gen = ControllerHyperparameters(), ThreeMealProtocol()
+    ft = FastTrial(0, pop.params_device, pop.basal_device, gen, prof, cfg, device=dev, n_slices=slices)
+    sz = ft.sz
+    H, ps = sz["horizon_ticks"], sz["period_steps"]
+    params, x0, c0, ub = (t.cpu().numpy() for t in (ft.params, ft.x0, ft.c0, ft.basal))
+    pas = [compile_protocol(gen.build(cfg.seed, type("P", (), {"id": i, "body_weight_kg": params[i, 0]})()),
+                            cfg.horizon_s) for i in range(n)]
+    moff, meals, eoff, ex = _csr(pas)
+    W = np.zeros((n, H, 3)); M = np.zeros((n, H // ps))
+    for i in range(n):
+        W[i], M[i] = rng.reference_noise(cfg.seed, i, H, ps, True, True)
+    hn = np.ones(n, np.uint8)
+    par = engine.run_parity(engine.ParityBatch(params, x0, c0, prof.to_vec(), ub, moff, meals, eoff, ex, W, hn, M),
+                            sz, cfg.dt_s, cfg.controller_period_s, device=dev)
+    ft.outs = engine.alloc_fast_outputs(n, 0, sz, dev, per_patient_timeline=True)
+    ft.simulate(injected={"wiener": engine.dev(W.reshape(-1), torch.float64, dev),
+                          "has_noise": engine.dev(hn, torch.uint8, dev),
+                          "meas": engine.dev(M.reshape(-1), torch.float64, dev)})
+    st, hist, tl, dd = (t.cpu().numpy() for t in (ft.outs.bg_stats, ft.outs.bg_hist, ft.outs.timeline_pp,
+                                                  ft.outs.day_dose))
+    assert tl.shape[0] == sz["n_grid"] and dd.shape[0] == sz["n_days"]
+    ties = 0
+    for j in range(n):
+        close = (np.allclose(st[:, j], par["scal"][j, :3], rtol=1e-9, atol=0)
+                 and np.allclose(tl[:, j], par["timeline"][j], rtol=1e-9, atol=0)
+                 and np.allclose(dd[:, :, j], par["day_dose"][j], rtol=1e-9, atol=1e-12))
+        ties += not (close and np.array_equal(hist[:, j], par["bg_hist"][j]))
+    assert ties <= 2
