@@ -19,7 +19,7 @@
 extern "C" {
 #endif
 
-#define GT_ABI_VERSION 1
+#define GT_ABI_VERSION 2  /* 2: gt_fast_args.hyper by value */
 
 /* layouts — hovorka.py:38-55, controller.py:32-41, analytics.py:21-37 */
 #define GT_N_STATES 16
@@ -169,7 +169,10 @@ typedef struct gt_fast_args {
     const double *params;        /* [n][30] */
     const double *x0;            /* [n][16] */
     const double *c0;            /* [n][11] */
-    const double *hyper;         /* [30] */
+    /* controller hyperparameters [30] (controller.py:100-132 packing), by
+     * VALUE: the fused kernel reads them from its parameter bank (the parity
+     * path's gt_parity_args.hyper is a device pointer) */
+    double hyper[30];
     const double *assumed_basal; /* [n] */
     const int32_t *active;       /* [n] or NULL */
     gt_meal_gen meal_gen;        /* GT_PROTO_THREE_MEAL */

@@ -65,7 +65,7 @@ class FastArgs(C.Structure):
         ("period_steps", I64), ("horizon_ticks", I64), ("grid_step_ticks", I64),
         ("n_days", I64), ("n_grid", I64), ("hypo_min_ticks", I64),
         ("noise_role", U32), ("rerun_diverged", I32), ("fixed", D * 30),
-        ("params", P), ("x0", P), ("c0", P), ("hyper", P), ("assumed_basal", P), ("active", P),
+        ("params", P), ("x0", P), ("c0", P), ("hyper", D * 30), ("assumed_basal", P), ("active", P),
         ("meal_gen", MealGen),
         ("meal_off", P), ("meal_ks", P), ("meal_ke", P), ("meal_kp", P),
         ("meal_rate", P), ("meal_ann", P),
@@ -159,7 +159,7 @@ def load(path: str | None = None):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.gt_abi_version() != 1:
+    if lib.gt_abi_version() != 2:   # include/glucosim.h GT_ABI_VERSION
         raise GlucosimError("libglucosim ABI version mismatch")
     if path is None:
         _lib = lib

@@ -144,7 +144,7 @@ int gt_simulate_fast(const gt_fast_args* a, void* stream) {
   REQUIRE(a->n_days == (int64_t)std::ceil((double)a->horizon_ticks * a->dt_s / 86400.0) ||
               a->n_days == 1,
           "gt_simulate_fast: n_days inconsistent with the horizon");
-  REQUIRE(a->params && a->x0 && a->c0 && a->hyper && a->assumed_basal && a->status && a->ticks &&
+  REQUIRE(a->params && a->x0 && a->c0 && a->assumed_basal && a->status && a->ticks &&
               a->bg_hist && a->bg_stats && a->day_dose && a->hypo_events && a->timeline_warp,
           "gt_simulate_fast: null required pointer");
   REQUIRE(a->controller == GT_CTRL_DUAL_HORMONE || a->controller == GT_CTRL_PID_PUMP,

@@ -69,6 +69,8 @@ struct Uni {
   double dt, period, horizon_s, meal_dur_min, rs_agg, pid_ph;
   int32_t ps, n_ctl, ctl_per_day, grid_ctl, hypoL, agg;
   uint32_t nz_c2, nz_c3;  // noise counter words 2-3: seed_lo, seed_hi ^ role << 24
+  double hyper[GT_N_HYPER];  // controller hyperparameters (parameter bank: direct operands)
+  double hc[6];              // hyper-derived controller constants (same IEEE values)
 };
 
 // Persistent work distribution (see the header comment).
@@ -274,8 +276,6 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
   constexpr bool CLAMP_GUT = (NOISE == GT_NOISE_INJECTED);
   // s_thr[k+1] = bits of THRESHOLDS[k]; s_thr[0] = -inf, s_thr[247] = +inf
   __shared__ long long s_thr[GT_N_THRESHOLDS + 2];
-  __shared__ double s_hyper[GT_N_HYPER];
-  __shared__ double s_hc[6];  // hyper-derived controller constants (same IEEE values)
   constexpr int kPulseTab = 64;
   __shared__ double s_prate[kPulseTab];  // PID: basal rate of p whole pulses, (p * q) / P_h
   extern __shared__ uint32_t s_hist[];  // [kHistWords * kFastBS], dynamic (> 48 KB total)
@@ -288,20 +288,11 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
   for (int q = tid; q < GT_N_THRESHOLDS + 2; q += kFastBS)
     s_thr[q] = q == 0 ? LLONG_MIN : (q == GT_N_THRESHOLDS + 1 ? LLONG_MAX
                                                                : __double_as_longlong((double)(4 + q) / 10.0));
-  for (int q = tid; q < GT_N_HYPER; q += kFastBS) s_hyper[q] = a.hyper[q];
   for (int q = tid; q < kHistWords * kFastBS; q += kFastBS) s_hist[q] = 0u;
   if (tid == 0) s_gen = a.meal_gen;
   __syncthreads();
-  if (tid == 0) {
-    s_hc[0] = D_(M_(s_hyper[HPREDHOR], 60.0), u.period);  // prediction factor (controller.py:393)
-    s_hc[1] = S_(1.0, s_hyper[HFILTER]);
-    s_hc[2] = M_(s_hyper[HLOCKMIN], 60.0);
-    s_hc[3] = A_(s_hyper[HGLUCTHR], s_hyper[HHYST]);
-    s_hc[4] = A_(s_hyper[HEXGLUCTHR], s_hyper[HHYST]);
-    s_hc[5] = CTRL == GT_CTRL_PID_PUMP ? D_(1.0, s_hyper[7]) : 0.0;  // PID: RN(1 / pulse size)
-  }
   if (CTRL == GT_CTRL_PID_PUMP)
-    for (int q = tid; q < kPulseTab; q += kFastBS) s_prate[q] = D_(M_((double)q, s_hyper[7]), u.pid_ph);
+    for (int q = tid; q < kPulseTab; q += kFastBS) s_prate[q] = D_(M_((double)q, u.hyper[7]), u.pid_ph);
   __syncthreads();  // no block-wide barrier after this point: warps run independently
 
   const int lane = tid & 31;
@@ -313,7 +304,6 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
   int32_t* const sil = s_i + tid_o;
   const int64_t n = a.n;
   const int64_t n_warps = sch.n_warps;
-  const double* __restrict__ H = s_hyper;
   // shared address of this lane's bin-0 byte, opaque to the compiler so it
   // stays in one register instead of being rebuilt every step
   uint32_t hist_lane;
@@ -674,51 +664,51 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         int flags = sil[(SI_FLAGS) * kFastBS];
         double filt = sdl[(SC_FILT) * kFastBS], prev;
         if (!(flags & 4)) { filt = y; prev = y; flags |= 4; }
-        else { prev = filt; filt = A_(M_(s_hc[1], filt), M_(H[HFILTER], y)); }
+        else { prev = filt; filt = A_(M_(u.hc[1], filt), M_(u.hyper[HFILTER], y)); }
         sdl[(SC_FILT) * kFastBS] = filt;
         const double trend = S_(filt, prev);
         double b_basal = 0.0, b_bolus = 0.0, b_gluc = 0.0;
         if (CTRL == GT_CTRL_PID_PUMP) {   // the controller is a template parameter: one per kernel
           // ---- PID + pump quantisation (pid.py pid_step_vec), same filter;
           // slots: SC_WEND = integral, SC_SUSP = pump carry
-          const double e = S_(filt, H[1]);
+          const double e = S_(filt, u.hyper[1]);
           const double ph = u.pid_ph;   // period / 3600, folded on the host (same IEEE quotient)
           double integ = A_(sdl[(SC_WEND) * kFastBS], M_(e, ph));
-          if (integ > H[6]) integ = H[6];
-          if (integ < -H[6]) integ = -H[6];
+          if (integ > u.hyper[6]) integ = u.hyper[6];
+          if (integ < -u.hyper[6]) integ = -u.hyper[6];
           sdl[(SC_WEND) * kFastBS] = integ;
-          double factor = A_(A_(A_(1.0, M_(H[2], e)), M_(H[3], integ)), M_(H[4], trend));
+          double factor = A_(A_(A_(1.0, M_(u.hyper[2], e)), M_(u.hyper[3], integ)), M_(u.hyper[4], trend));
           if (factor < 0.0) factor = 0.0;
-          if (factor > H[5]) factor = H[5];
+          if (factor > u.hyper[5]) factor = u.hyper[5];
           const double vol = A_(M_(M_(sdl[(SC_ASSUMED) * kFastBS], factor), ph), sdl[(SC_SUSP) * kFastBS]);
           // floor(vol / q) of the IEEE quotient: vol * RN(1/q) is within 1e-13
           // of it, so its floor is exact unless it lies within 1e-9 of an
           // integer (then the division is done)
-          const double qf = M_(vol, s_hc[5]);
+          const double qf = M_(vol, u.hc[5]);
           double pulses = floor(qf);
           const double fr = S_(qf, pulses);
-          if (!(fr > 1e-9 && fr < 1.0 - 1e-9 && qf < 1e6)) pulses = floor(D_(vol, H[7]));
+          if (!(fr > 1e-9 && fr < 1.0 - 1e-9 && qf < 1e6)) pulses = floor(D_(vol, u.hyper[7]));
           if (pulses < 0.0) pulses = 0.0;
-          const double delivered = M_(pulses, H[7]);
+          const double delivered = M_(pulses, u.hyper[7]);
           sdl[(SC_SUSP) * kFastBS] = S_(vol, delivered);
           // (p * q) / P_h from the table (same operations), else computed
           b_basal = pulses < (double)kPulseTab ? s_prate[(int)pulses] : D_(delivered, ph);
           if (announced > 0.0) {
             double bb = D_(announced, sdl[(SC_ICR) * kFastBS]);
-            if (bb > H[9]) bb = H[9];
-            b_bolus = M_(floor(D_(bb, H[8])), H[8]);
+            if (bb > u.hyper[9]) bb = u.hyper[9];
+            b_bolus = M_(floor(D_(bb, u.hyper[8])), u.hyper[8]);
           }
         } else {
         const bool exercising = HAS_EX && phase >= 0.0;
-        const double setpoint = exercising ? H[HEXSETPOINT] : H[HSETPOINT];
-        const double gluc_thr = exercising ? H[HEXGLUCTHR] : H[HGLUCTHR];
-        double micro = exercising ? H[HEXMICROUG] : H[HMICROUG];
+        const double setpoint = exercising ? u.hyper[HEXSETPOINT] : u.hyper[HSETPOINT];
+        const double gluc_thr = exercising ? u.hyper[HEXGLUCTHR] : u.hyper[HGLUCTHR];
+        double micro = exercising ? u.hyper[HEXMICROUG] : u.hyper[HMICROUG];
         bool done = false;
         if (exercising) {
           if (!(flags & 2)) {
             flags |= 2;
-            if (filt < H[HEXBOLUSBG]) {
-              b_gluc = fmin(H[HEXBOLUS], H[HMAXGLUC]);
+            if (filt < u.hyper[HEXBOLUSBG]) {
+              b_gluc = fmin(u.hyper[HEXBOLUS], u.hyper[HMAXGLUC]);
               sdl[(SC_LASTG) * kFastBS] = t_s;
               done = true;
             }
@@ -727,11 +717,11 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           flags &= ~2;
         }
         if (!done) {
-          const double pred = A_(filt, M_(trend, s_hc[0]));
+          const double pred = A_(filt, M_(trend, u.hc[0]));
           if (!(flags & 1)) {
             if (filt < gluc_thr || pred < gluc_thr) flags |= 1;
           } else {
-            if (filt >= (exercising ? s_hc[4] : s_hc[3]) && pred >= gluc_thr) flags &= ~1;
+            if (filt >= (exercising ? u.hc[4] : u.hc[3]) && pred >= gluc_thr) flags &= ~1;
           }
           const double wend = sdl[(SC_WEND) * kFastBS];
           if (wend > 0.0) {
@@ -740,17 +730,17 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
             sdl[(SC_WPEAK) * kFastBS] = wpeak; sdl[(SC_WMIN) * kFastBS] = wmin;
             if (t_s >= wend) {
               double icr = sdl[(SC_ICR) * kFastBS];
-              if (wmin < H[HUNDERBG]) icr = M_(icr, A_(1.0, H[HICRSTEPUP]));
-              else if (S_(wpeak, H[HSETPOINT]) > H[HEXCHI]) icr = M_(icr, S_(1.0, H[HICRSTEP]));
-              if (icr < H[HICRMIN]) icr = H[HICRMIN];
-              if (icr > H[HICRMAX]) icr = H[HICRMAX];
+              if (wmin < u.hyper[HUNDERBG]) icr = M_(icr, A_(1.0, u.hyper[HICRSTEPUP]));
+              else if (S_(wpeak, u.hyper[HSETPOINT]) > u.hyper[HEXCHI]) icr = M_(icr, S_(1.0, u.hyper[HICRSTEP]));
+              if (icr < u.hyper[HICRMIN]) icr = u.hyper[HICRMIN];
+              if (icr > u.hyper[HICRMAX]) icr = u.hyper[HICRMAX];
               sdl[(SC_ICR) * kFastBS] = icr;
               sdl[(SC_WEND) * kFastBS] = 0.0;
             }
           }
           if (flags & 1) {
-            if (filt < gluc_thr && trend < -H[HMICROTREND] && S_(t_s, sdl[(SC_LASTG) * kFastBS]) >= s_hc[2]) {
-              if (micro > H[HMAXGLUC]) micro = H[HMAXGLUC];
+            if (filt < gluc_thr && trend < -u.hyper[HMICROTREND] && S_(t_s, sdl[(SC_LASTG) * kFastBS]) >= u.hc[2]) {
+              if (micro > u.hyper[HMAXGLUC]) micro = u.hyper[HMAXGLUC];
               b_gluc = micro;
               sdl[(SC_LASTG) * kFastBS] = t_s;
             }
@@ -758,22 +748,22 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
             const double assumed = sdl[(SC_ASSUMED) * kFastBS];
             if (announced > 0.0) {
               const double icr = sdl[(SC_ICR) * kFastBS];
-              double b = A_(D_(announced, icr), D_(S_(filt, setpoint), M_(H[HCFICR], icr)));
-              if (filt > H[HSUPBG]) b = A_(b, D_(M_(M_(H[HSUPFRAC], assumed), H[HSUSPMIN]), 60.0));
+              double b = A_(D_(announced, icr), D_(S_(filt, setpoint), M_(u.hyper[HCFICR], icr)));
+              if (filt > u.hyper[HSUPBG]) b = A_(b, D_(M_(M_(u.hyper[HSUPFRAC], assumed), u.hyper[HSUSPMIN]), 60.0));
               if (b < 0.0) b = 0.0;
-              if (b > H[HMAXBOLUS]) b = H[HMAXBOLUS];
+              if (b > u.hyper[HMAXBOLUS]) b = u.hyper[HMAXBOLUS];
               b_bolus = b;
-              sdl[(SC_SUSP) * kFastBS] = A_(t_s, M_(H[HSUSPMIN], 60.0));
-              sdl[(SC_WEND) * kFastBS] = A_(t_s, M_(H[HMEALWIN], 60.0));
+              sdl[(SC_SUSP) * kFastBS] = A_(t_s, M_(u.hyper[HSUSPMIN], 60.0));
+              sdl[(SC_WEND) * kFastBS] = A_(t_s, M_(u.hyper[HMEALWIN], 60.0));
               sdl[(SC_WPEAK) * kFastBS] = filt;
               sdl[(SC_WMIN) * kFastBS] = filt;
             }
             if (!(t_s < sdl[(SC_SUSP) * kFastBS])) {
-              double factor = A_(A_(1.0, M_(H[HBKP], S_(filt, setpoint))), M_(H[HBKD], trend));
+              double factor = A_(A_(1.0, M_(u.hyper[HBKP], S_(filt, setpoint))), M_(u.hyper[HBKD], trend));
               if (factor < 0.0) factor = 0.0;
-              if (factor > H[HBFMAX]) factor = H[HBFMAX];
+              if (factor > u.hyper[HBFMAX]) factor = u.hyper[HBFMAX];
               double b = M_(assumed, factor);
-              if (exercising) b = M_(b, H[HEXBFACTOR]);
+              if (exercising) b = M_(b, u.hyper[HEXBFACTOR]);
               b_basal = b;
             }
           }
@@ -1045,6 +1035,16 @@ static Uni make_uni(const gt_fast_args& a) {
   u.agg = a.noise_agg < 1 ? 1 : a.noise_agg;
   u.rs_agg = 1.0 / std::sqrt((double)u.agg);
   u.pid_ph = a.period_s / 3600.0;
+  // controller constants: single IEEE operations, identical on host and device
+  // (controller.py:393 prediction factor, filter complement, lock-out, hysteresis)
+  for (int k = 0; k < GT_N_HYPER; ++k) u.hyper[k] = a.hyper[k];
+  const double* hy = a.hyper;
+  u.hc[0] = (hy[HPREDHOR] * 60.0) / a.period_s;
+  u.hc[1] = 1.0 - hy[HFILTER];
+  u.hc[2] = hy[HLOCKMIN] * 60.0;
+  u.hc[3] = hy[HGLUCTHR] + hy[HHYST];
+  u.hc[4] = hy[HEXGLUCTHR] + hy[HHYST];
+  u.hc[5] = a.controller == GT_CTRL_PID_PUMP ? 1.0 / hy[7] : 0.0;   // PID: RN(1 / pulse size)
   u.nz_c2 = (uint32_t)a.seed;
   u.nz_c3 = (uint32_t)(a.seed >> 32) ^ (a.noise_role << 24);
   return u;

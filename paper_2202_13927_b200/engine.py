@@ -224,8 +224,16 @@ def launch_fast(inputs: dict, outs: FastOutputs, sz: dict, dt_s: float, period_s
     a.n_days, a.n_grid, a.hypo_min_ticks = sz["n_days"], sz["n_grid"], int(hypo_min_ticks)
     a.noise_role = noise_role
     a.rerun_diverged = int(bool(rerun_diverged))
-    for k in ("params", "x0", "c0", "hyper", "assumed_basal", "active"):
+    for k in ("params", "x0", "c0", "assumed_basal", "active"):
         setattr(a, k, ptr(inputs.get(k)))
+    # hyperparameters by value (the kernel's parameter bank): the host copy
+    # when the caller has one, else read back once from the device tensor
+    hy = inputs.get("hyper_host")
+    if hy is None:
+        hy = inputs["hyper"]
+        hy = hy.detach().cpu().numpy() if hasattr(hy, "detach") else np.asarray(hy)
+    for k in range(len(a.hyper)):
+        a.hyper[k] = float(hy[k])
     a.meal_gen = meal_gen_struct(meal_spec)
     if csr is not None:
         for k in ("meal_off", "meal_ks", "meal_ke", "meal_kp", "meal_rate", "meal_ann", "ex_off",

@@ -86,6 +86,7 @@ class FastTrial:
             self.outs = engine.alloc_fast_outputs(self.n, self.pid0, self.sz, self.device)
             self.red = engine.alloc_reduce_outputs(self.n, self.sz, self.device, per_patient_metrics)
         self._inputs = {"params": self.params, "x0": self.x0, "c0": self.c0, "hyper": self.hyper_d,
+                        "hyper_host": np.asarray(self.hyper, np.float64),
                         "assumed_basal": self.basal, "active": self.active}
 
     def _build_csr(self, generator):
