@@ -51,6 +51,9 @@ namespace gt {
 #ifndef GT_LASTCHECK
 #define GT_LASTCHECK 1   // the state check at the horizon's last tick only (see the tick)
 #endif
+#ifndef GT_DAY_VOTE
+#define GT_DAY_VOTE 1
+#endif
 #ifndef GT_NOISE_PIPE
 #define GT_NOISE_PIPE 1  // draw tick k + 1's normals during step k
 #endif
@@ -511,8 +514,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
     // warp-uniform cursors derived from the slice start
     int next_grid_ctl = ((ctl_lo + u.grid_ctl - 1) / u.grid_ctl) * u.grid_ctl;
     int g_idx = next_grid_ctl / u.grid_ctl;
-    int next_day_ctl = max(cpd, ((ctl_lo + cpd - 1) / cpd) * cpd);  // day flush (ctl > 0)
-    int next_gen_ctl = ((ctl_lo + cpd - 1) / cpd) * cpd;             // day window generation
+    int next_day_ctl = ((ctl_lo + cpd - 1) / cpd) * cpd;  // day start: flush (ctl > 0), day window
 
     // software-pipelined noise: the normals of tick k + 1 are drawn during
     // step k, next to its Euler update, so no step waits on its own Philox
@@ -918,20 +920,25 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       // day boundary: flush the finished day's dose sums (_kernel.py:133-149)
       if (ctl == next_day_ctl) {
         next_day_ctl += cpd;
-        const int64_t day = ctl / cpd - 1;
-        GT_CHECK(day >= 0 && day < a.n_days, "day flush");
-        if (inrange) {
-          double* dd = a.day_dose + (day * 3) * n + i;
-          dd[0] = day_basal; dd[n] = sdl[(SC_DBOLUS) * kFastBS]; dd[2 * n] = sdl[(SC_DGLUC) * kFastBS];
+        // flush the finished day's dose sums (_kernel.py:133-149)
+        if (ctl > 0) {
+          const int64_t day = ctl / cpd - 1;
+          GT_CHECK(day >= 0 && day < a.n_days, "day flush");
+          if (inrange) {
+            double* dd = a.day_dose + (day * 3) * n + i;
+            dd[0] = day_basal; dd[n] = sdl[(SC_DBOLUS) * kFastBS]; dd[2 * n] = sdl[(SC_DGLUC) * kFastBS];
+          }
+          day_basal = 0.0; sdl[(SC_DBOLUS) * kFastBS] = 0.0; sdl[(SC_DGLUC) * kFastBS] = 0.0;
         }
-        day_basal = 0.0; sdl[(SC_DBOLUS) * kFastBS] = 0.0; sdl[(SC_DGLUC) * kFastBS] = 0.0;
+        if (PROTO == GT_PROTO_THREE_MEAL) {
+          day_ctl0 = ctl; day_k0 = ctl * ps;
+          gen_day(ctl / cpd);
+        }
+        // lanes die only at the horizon's last tick: an all-dead warp is one
+        // masked from the start (excluded / re-run lanes); checked per day
+        if (GT_DAY_VOTE && __all_sync(0xffffffffu, !alive)) break;
       }
-      if (PROTO == GT_PROTO_THREE_MEAL && ctl == next_gen_ctl) {
-        next_gen_ctl += cpd;
-        day_ctl0 = ctl; day_k0 = ctl * ps;
-        gen_day(ctl / cpd);
-      }
-      if (__all_sync(0xffffffffu, !alive)) break;   // (a per-slice vote spills: kept per period)
+      if (!GT_DAY_VOTE && __all_sync(0xffffffffu, !alive)) break;
       const int32_t kb0 = ctl * ps;
       step(kb0, true, ctl, 0);
       for (int s = 1; s < ps; ++s) step(kb0 + s, false, ctl, s);
