@@ -453,3 +453,36 @@ def test_fused_equals_parity_on_odd_horizons(dev, oracle, horizon_h, dt_s, grid_
                  and np.allclose(dd[:, :, j], par["day_dose"][j], rtol=1e-9, atol=1e-12))
         ties += not (close and np.array_equal(hist[:, j], par["bg_hist"][j]))
     assert ties <= 2
+
+
+@pytest.mark.parametrize("controller", ["dual_hormone", "pid_pump"])
+def test_nonfinite_non_glucose_state_aborts(dev, controller):
+    """A non-finite state other than glucose (the sensor Gsc at t = 0) aborts
+    the patient, as the reference's per-tick state check does
+    (_kernel.py:98-103): the fused kernel checks the state at the horizon's
+    last tick (non-finiteness is absorbing) and the BG sum after the last
+    step.  The other patients' statistics exclude it exactly."""
+    from paper_2202_13927_b200.config import SimulationConfig
+    from paper_2202_13927_b200.controller import ControllerHyperparameters
+    from paper_2202_13927_b200.layout import IGSC
+    from paper_2202_13927_b200.pid import PIDProfile
+    from paper_2202_13927_b200.population import generate_population
+    from paper_2202_13927_b200.protocol import ThreeMealProtocol
+    from paper_2202_13927_b200.trial import FastTrial
+    cfg = SimulationConfig(horizon_s=86400.0, seed=4, dt_s=60.0)
+    pop = generate_population(3, 64, device=dev, on_exhausted="redraw_weight")
+    prof = PIDProfile() if controller == "pid_pump" else ControllerHyperparameters()
+    ft = FastTrial(0, pop.params_device, pop.basal_device, ThreeMealProtocol(), prof, cfg, controller, dev,
+                   per_patient_metrics=True)
+    x0 = ft._inputs["x0"].clone()
+    x0[7, IGSC] = float("nan")
+    ft._inputs["x0"] = x0
+    ft.step()
+    acc = ft.accumulator()
+    assert acc.aborted_ids == (7,)
+    assert acc.n_patients == 63
+    clean = FastTrial(0, pop.params_device, pop.basal_device, ThreeMealProtocol(), prof, cfg, controller, dev,
+                      per_patient_metrics=True)
+    clean.step()
+    keep = np.arange(64) != 7
+    assert np.array_equal(ft.metrics()["tir"][keep], clean.metrics()["tir"][keep])
