@@ -1059,12 +1059,21 @@ static Uni make_uni(const gt_fast_args& a) {
 
 }  // namespace gt
 
-// Number of horizon slices: the smallest c in 1..8 minimising
-// ceil(c * warps / slots) / c (the makespan in units of one full horizon).
+// Number of horizon slices.  Per-warp cost varies with the patients'
+// trajectories (hypo runs, meals), so the persistent schedule balances better
+// with several units per resident warp slot: aim for >= 6 rounds of units,
+// then take the count in that range with the least wave quantisation
+// ceil(c * warps / slots) / c (ties: fewer slices).  A slice keeps >= 48
+// controller periods so save / restore stays negligible.  Measured on
+// 100k x 4 weeks: 3 slices 41.3 ms, 6-32 slices 39.2-40.1 ms.
 static int choose_chunks(int64_t warps, int64_t slots, int n_ctl) {
-  int best = 1;
+  const int c_max = std::max(1, std::min(32, n_ctl / 48));
+  // (fewer warps than slots: one slice; a warp's slices run in sequence anyway)
+  const int c_min = warps < slots ? 1
+                                  : (int)std::max<int64_t>(1, std::min<int64_t>(c_max, (6 * slots + warps - 1) / warps));
+  int best = c_min;
   double best_t = 1e300;
-  for (int c = 1; c <= 8 && c <= n_ctl; ++c) {
+  for (int c = c_min; c <= c_max; ++c) {
     const double rounds = (double)((c * warps + slots - 1) / slots);
     const double t = rounds / c;
     if (t < best_t - 1e-9) { best_t = t; best = c; }

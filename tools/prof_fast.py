@@ -1,6 +1,6 @@
 """Profiling driver: stage a FastTrial and run simulate+reduce a few times.
 
-    python tools/prof_fast.py [n_patients] [weeks] [reps] [three_meal|northern] [dual_hormone|pid_pump]
+    python tools/prof_fast.py [n_patients] [weeks] [reps] [three_meal|northern] [dual_hormone|pid_pump] [dt_s] [n_slices]
 """
 import os
 import sys
@@ -23,6 +23,7 @@ reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 proto = sys.argv[4] if len(sys.argv) > 4 else "three_meal"
 ctrl = sys.argv[5] if len(sys.argv) > 5 else "dual_hormone"
 dt_s = float(sys.argv[6]) if len(sys.argv) > 6 else 60.0
+n_slices = int(sys.argv[7]) if len(sys.argv) > 7 else 0
 dev = torch.device("cuda", 0)
 cfg = SimulationConfig(horizon_s=weeks * 7 * 86400.0, seed=1, dt_s=dt_s)
 pop = generate_population(1, n, device=dev, on_exhausted="redraw_weight")
@@ -36,7 +37,8 @@ if ctrl == "pid_pump":
     prof = PIDProfile()
 else:
     prof = ControllerHyperparameters()
-ft = FastTrial(0, pop.params_device, pop.basal_device, gen, prof, cfg, controller_id=ctrl, device=dev)
+ft = FastTrial(0, pop.params_device, pop.basal_device, gen, prof, cfg, controller_id=ctrl, device=dev,
+               n_slices=n_slices)
 for r in range(reps):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
