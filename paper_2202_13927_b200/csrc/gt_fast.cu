@@ -180,13 +180,13 @@ __device__ __forceinline__ U4 philox_fast(uint32_t c0, uint32_t c1, uint32_t c2,
   return U4{c0, c1, c2, c3};
 }
 
-// Raw SFU approximations (MUFU.LG2 / RSQ / SIN / COS), no denormal or
+// Raw SFU approximations (MUFU.LG2 / SQRT / SIN / COS), no denormal or
 // special-value paths: every argument below is a normal, finite float.
 __device__ __forceinline__ float lg2_approx(float x) {
   float r; asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x)); return r;
 }
-__device__ __forceinline__ float rsqrt_approx(float x) {
-  float r; asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x)); return r;
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r; asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x)); return r;
 }
 __device__ __forceinline__ float sin_approx(float x) {
   float r; asm("sin.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x)); return r;
@@ -195,13 +195,14 @@ __device__ __forceinline__ float cos_approx(float x) {
   float r; asm("cos.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x)); return r;
 }
 
-// Box-Muller in FP32 on the SFU: u1 in [2^-33, 1 - 2^-24] (never 0 or 1),
-// radius sqrt(-2 ln u1) = t * rsqrt(t), angle 2*pi*u2 in [0, 2*pi).
+// Box-Muller in FP32 on the SFU: u1 in [2^-33, 1] (never 0), radius
+// sqrt(-2 ln u1) by MUFU.SQRT (u1 = 1 gives radius 0, as it should), angle
+// 2*pi*u2 in [0, 2*pi).
 __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float& z0, float& z1) {
-  const float u1 = fminf(fmaf((float)a, 2.3283064365386963e-10f, 1.1641532182693481e-10f), 0.99999994f);
+  const float u1 = fmaf((float)a, 2.3283064365386963e-10f, 1.1641532182693481e-10f);
   const float ang = (float)b * 1.4629180792671596e-09f;  // 2*pi * 2^-32
   const float t = lg2_approx(u1) * -1.3862943611198906f;  // -2 ln 2 * log2(u1) > 0
-  const float rad = t * rsqrt_approx(t);
+  const float rad = sqrt_approx(t);
   z0 = rad * cos_approx(ang);
   z1 = rad * sin_approx(ang);
 }
