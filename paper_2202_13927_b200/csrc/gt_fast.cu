@@ -60,7 +60,10 @@ namespace gt {
 #ifndef GT_FAST_MINB
 #define GT_FAST_MINB 4  // resident 128-thread blocks per SM (register budget 128)
 #endif
-constexpr int kFastBS = 128;
+#ifndef GT_FAST_BS
+#define GT_FAST_BS 128  // threads per block (lanes sharing the block's shared-memory slots)
+#endif
+constexpr int kFastBS = GT_FAST_BS;
 constexpr int kHistWords = (GT_N_BG_BINS + 3) / 4;  // 62 packed uint8x4 words per lane
 
 // Launch-uniform constants derived from the fixed parameters (host-computed,
@@ -811,7 +814,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         kb = alive ? kb : GT_N_BG_BINS;  // dead lanes count into the padding bin 247
         {  // byte ((kb >> 2) * kFastBS + tid) * 4 + (kb & 3)
           GT_CHECK(kb >= 0 && kb <= GT_N_BG_BINS, "histogram bin");
-          const uint32_t ha = hist_lane + ((uint32_t)(kb & ~3) << 7) + (uint32_t)(kb & 3);
+          const uint32_t ha = hist_lane + (uint32_t)(kb & ~3) * (uint32_t)kFastBS + (uint32_t)(kb & 3);
           uint32_t c;
           asm volatile("{\n\t.reg .u32 t;\n\tld.shared.u8 t, [%1];\n\tadd.u32 %0, t, 1;\n\t"
                        "st.shared.u8 [%1], %0;\n\t}" : "=r"(c) : "r"(ha));
@@ -1132,7 +1135,7 @@ static int launch_sched(const gt_fast_args* a, const gt::Uni& u, cudaStream_t st
     s.sd = reinterpret_cast<double*>(base);
     s.si = reinterpret_cast<int*>(base + n_pad * gt::SD_N * sizeof(double));
   }
-  const int64_t blocks_needed = (warps + 3) / 4;
+  const int64_t blocks_needed = (warps + gt::kFastBS / 32 - 1) / (gt::kFastBS / 32);
   const unsigned grid = (unsigned)std::min<int64_t>((int64_t)sms * per_sm, blocks_needed);
   kern<<<grid, gt::kFastBS, kDyn, st>>>(*a, u, s);
   const int e = gt_check_launch("fast_kernel");
