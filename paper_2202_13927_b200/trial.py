@@ -183,54 +183,68 @@ class FastTrial:
         self.simulate(rerun_diverged=True)
 
     # ----------------------------------------------------------- readback
-    def accumulator(self) -> TrialAccumulator:
+    def _fetch(self, *xs):
+        """D2H of several device tensors: pinned, stream-ordered copies and one
+        synchronisation (instead of one per tensor)."""
         t = engine.torch()
+        hosts = []
+        for x in xs:
+            if x.device.type == "cpu":
+                hosts.append(x)
+                continue
+            h = t.empty(x.shape, dtype=x.dtype, pin_memory=True)
+            h.copy_(x, non_blocking=True)
+            hosts.append(h)
+        if any(x.device.type != "cpu" for x in xs):
+            t.cuda.current_stream(self.device).synchronize()
+        return [h.numpy() for h in hosts]
+
+    def accumulator(self) -> TrialAccumulator:
         cfg, sz, red = self.config, self.sz, self.red
         acc = TrialAccumulator(dt_s=cfg.dt_s, horizon_ticks=sz["horizon_ticks"], n_days=sz["n_days"],
                                n_grid=sz["n_grid"], grid_step_s=cfg.grid_step_s)
-        h = lambda x: x.cpu().numpy()
-        counts = h(red.counts)
+        (counts, status, ss, tir_total, tir_hist, bg_total, below_min, below_max, mm, tl, dh, dsum, mhist,
+         w) = self._fetch(red.counts, self.outs.status, self.ss_status, red.tir_ticks_total, red.tir_hist,
+                          red.bg_hist_total, red.below_min, red.below_max, red.minmax_bg_bits, red.timeline,
+                          red.dose_hist, red.dose_sum_fp, red.metric_hist, red.worst)
         acc.n_patients = int(counts[0])
-        status = h(self.outs.status)
-        ss = h(self.ss_status)
         aborted = np.nonzero((status == GT_STATUS_NONFINITE) | (ss == GT_STATUS_NO_STEADY_STATE))[0]
         acc.n_aborted = int(aborted.size)
         acc.aborted_ids = tuple(int(self.pid0 + i) for i in aborted)
         acc.sum_bg_fp = (int(counts[4]) << 64) + (int(counts[2]) & 0xFFFFFFFFFFFFFFFF)
         acc.n_patient_days = int(counts[3])
-        acc.tir_ticks_total = h(red.tir_ticks_total).astype(np.int64)
-        acc.tir_hist = h(red.tir_hist).astype(np.int64)
-        acc.bg_hist_total = h(red.bg_hist_total).astype(np.int64)
-        acc.below_min = h(red.below_min).astype(np.int64)
-        acc.below_max = h(red.below_max).astype(np.int64)
-        mm = h(red.minmax_bg_bits)
+        acc.tir_ticks_total = tir_total.astype(np.int64)
+        acc.tir_hist = tir_hist.astype(np.int64)
+        acc.bg_hist_total = bg_total.astype(np.int64)
+        acc.below_min = below_min.astype(np.int64)
+        acc.below_max = below_max.astype(np.int64)
         acc.min_bg = engine.ordered_bits_to_double(mm[0]) if acc.n_patients else np.inf
         acc.max_bg = engine.ordered_bits_to_double(mm[1]) if acc.n_patients else -np.inf
-        tl = h(red.timeline)
         acc.timeline_sum_fp, acc.timeline_min_fp, acc.timeline_max_fp = (tl[0].copy(), tl[1].copy(), tl[2].copy())
-        dh = h(red.dose_hist)
         acc.dose_hist = {s: dh[k].astype(np.int64) for k, s in enumerate(DOSE_SIGNALS)}
-        acc.dose_sum_fp = [int(v) for v in h(red.dose_sum_fp)]
-        acc.metric_hist = h(red.metric_hist).astype(np.int64)
-        w = h(red.worst)
+        acc.dose_sum_fp = [int(v) for v in dsum]
+        acc.metric_hist = mhist.astype(np.int64)
         if int(w[3]):
             i = int(w[2]) - self.pid0
-            hist = h(self.outs.bg_hist[:, i]).astype(np.int64)
+            hist, wmax, wticks = self._fetch(self.outs.bg_hist[:, i].contiguous(), self.outs.bg_stats[1, i:i + 1],
+                                             self.outs.ticks[i:i + 1])
+            hist = hist.astype(np.int64)
             cum = np.cumsum(hist)
             tir = np.array([cum[25], cum[34] - cum[25], cum[95] - cum[34], cum[134] - cum[95],
                             cum[-1] - cum[134]], dtype=np.int64)
             acc.worst = WorstCase(patient_id=int(w[2]), min_bg=engine.ordered_bits_to_double(w[0]),
-                                  max_bg=float(h(self.outs.bg_stats[1, i])), ticks_below_3=int(w[1]),
-                                  ticks=int(h(self.outs.ticks[i])), tir_ticks=tir, bg_hist=hist)
+                                  max_bg=float(wmax[0]), ticks_below_3=int(w[1]),
+                                  ticks=int(wticks[0]), tir_ticks=tir, bg_hist=hist)
         return acc
 
     def metrics(self) -> dict | None:
         if self.red.metrics is None:
             return None
-        out = {k: v.cpu().numpy() for k, v in self.red.metrics.items()}
-        out["hypo_events_lt70"] = self.outs.hypo_events[0].cpu().numpy()
-        out["hypo_events_lt54"] = self.outs.hypo_events[1].cpu().numpy()
-        out["status"] = self.outs.status.cpu().numpy()
+        keys = list(self.red.metrics)
+        vals = self._fetch(*[self.red.metrics[k] for k in keys], self.outs.hypo_events[0], self.outs.hypo_events[1],
+                           self.outs.status)
+        out = dict(zip(keys, vals[:len(keys)]))
+        out["hypo_events_lt70"], out["hypo_events_lt54"], out["status"] = vals[len(keys):]
         return out
 
 
