@@ -3,8 +3,8 @@
 // One thread = one virtual patient.  SDE state, Philox counters and per-step
 // accumulators live in registers.  The 247-bin BG histogram of each patient
 // lives in shared memory as uint8 counters: a counter that reaches 255
-// drains into the patient's HBM column (predicated RED), and all drain at the
-// end of a slice.  The state that changes only on controller ticks
+// drains into the patient's HBM column (a RED on that rare path only), and
+// all drain at the end of a slice.  The state that changes only on controller ticks
 // (controller memory, meal window, dose sums, BG extremes) lives in shared
 // memory too, so HBM sees parameters in and metrics out only.
 //
@@ -12,8 +12,9 @@
 // statistics (_kernel.py:137-160) as the parity kernel, re-associated for
 // the FP64 pipe: each linear update x += h*(b*y - x/tau) is evaluated as
 // fma(x, 1-h/tau, h*b*y) with per-patient constants folded at start-up and
-// launch-uniform constants (fixed parameters) in the kernel-parameter bank;
-// the noise Philox runs under a fixed key whose round keys are immediates.  For every state of that form the reference's
+// launch-uniform constants (fixed parameters, controller hyperparameters) in
+// the kernel-parameter bank; the noise Philox runs under a fixed key whose
+// round keys are immediates.  For every state of that form the reference's
 // projection max(x,0) is a no-op (monotone rounding of a - b with
 // 0 <= b <= a), so it is applied only to Q1 and Q2 (and D1/D2 when arbitrary
 // noise is injected: device Philox normals are bounded by 6.7 sigma, far
@@ -25,8 +26,9 @@
 // chunk-major order, from a global counter; a unit with c > 0 waits until
 // unit (c-1, w) has released its saved state.  Slicing the horizon removes
 // the wave quantisation of one-thread-per-patient launches (100k patients =
-// 3125 warps on 2368 resident warp slots = 1.32 waves): the host picks the
-// slice count that makes the unit count divide the slots best.
+// 3125 warps on 2368 resident warp slots = 1.32 waves) and, with several
+// units per slot, lets the schedule balance the warps' unequal costs
+// (choose_chunks).
 //
 // Loop structure is warp-uniform: outer loop over controller periods, inner
 // loop over the period's integration steps; all lanes of a warp hit
@@ -858,8 +860,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         }
         if (lane == 0) {
           GT_CHECK(g_idx >= 0 && g_idx < a.n_grid, "timeline");
-          GT_CHECK(g_idx >= 0 && g_idx < a.n_grid, "timeline tail");
-        long long* dst = (long long*)a.timeline_warp + ((int64_t)g_idx * n_warps + warp_global) * 3;
+          long long* dst = (long long*)a.timeline_warp + ((int64_t)g_idx * n_warps + warp_global) * 3;
           dst[0] = ssum; dst[1] = smin; dst[2] = smax;
         }
         if (a.timeline_pp && inrange) a.timeline_pp[(int64_t)g_idx * n + i] = alive ? bg : 0.0;
