@@ -56,9 +56,6 @@ namespace gt {
 #ifndef GT_DAY_VOTE
 #define GT_DAY_VOTE 1
 #endif
-#ifndef GT_HIST_LATE
-#define GT_HIST_LATE 1   // bin step k's BG after its Euler update (latency overlap)
-#endif
 #ifndef GT_NOISE_PIPE
 #define GT_NOISE_PIPE 1  // draw tick k + 1's normals during step k
 #endif
@@ -797,54 +794,6 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         // SURVEY.md §7): use the reference's exact division for that tick
         bg = Q1 / (a.params[ii * NP + PVG] * a.params[ii * NP + PW]);
       }
-      if (!GT_HIST_LATE) {
-      // A non-finite bg (_kernel.py:139-141) is caught lazily: bg_sum absorbs
-      // Inf/NaN and is checked after the last step.  Until then the lane's
-      // statistics are garbage but in range; an aborted patient's are
-      // discarded and its warp re-run with it masked.
-      {
-        // searchsorted(THRESHOLDS, bg, 'right') for bg >= 0.  THRESHOLDS[i] =
-        // RN((5+i)/10), so away from a threshold the bin is floor(10 bg) - 4
-        // (clamped to [0, 246]); the FP32 estimate decides whenever 10 bg is
-        // more than 1e-4 from an integer (its error is < 4e-5 up to bg = 25.6)
-        // and the exact int64 compare against the table settles the rest.
-        const float t10 = __double2float_rz(bg) * 10.0f;
-        const float fl = floorf(t10);
-        int kb = min(max((int)fl - 4, 0), GT_N_THRESHOLDS);
-        const float fr = t10 - fl;
-        if (__builtin_expect(!(fr > 1e-4f && fr < 0.9999f), 0)) {
-          const long long bb = __double_as_longlong(bg);
-          kb = min(max(kb, 0), GT_N_THRESHOLDS);
-          kb += (s_thr[kb + 1] <= bb) - (s_thr[kb] > bb);
-        }
-        kb = alive ? kb : GT_N_BG_BINS;  // dead lanes count into the padding bin 247
-        {  // byte ((kb >> 2) * kFastBS + tid) * 4 + (kb & 3)
-          GT_CHECK(kb >= 0 && kb <= GT_N_BG_BINS, "histogram bin");
-          const uint32_t ha = hist_lane + (uint32_t)(kb & ~3) * (uint32_t)kFastBS + (uint32_t)(kb & 3);
-          uint32_t c;
-          asm volatile("{\n\t.reg .u32 t;\n\tld.shared.u8 t, [%1];\n\tadd.u32 %0, t, 1;\n\t"
-                       "st.shared.u8 [%1], %0;\n\t}" : "=r"(c) : "r"(ha));
-          // a full counter drains into the HBM column (1 tick in 255): the
-          // column address is formed only on that path
-          if (__builtin_expect(c == 255u, 0)) {
-            asm volatile("st.shared.u8 [%0], 0;" :: "r"(ha) : "memory");
-            if (kb < GT_N_BG_BINS && inrange) atomicAdd(a.bg_hist + ((int64_t)kb * n + i), 255);
-          }
-        }
-        bg_sum += bg;
-        // extremes: only a tick in the lowest/highest bin so far can move them;
-        // hypo runs: only ticks below 3.9 mmol/L (or ending such a run) matter
-        if (__builtin_expect(kb <= trig_lo || kb >= kb_max, 0) && alive) {
-          if (kb <= kb_min) { const double o = sdl[(SC_BGMIN) * kFastBS]; sdl[(SC_BGMIN) * kFastBS] = bg < o ? bg : o; kb_min = kb; }
-          if (kb >= kb_max) { const double o = sdl[(SC_BGMAX) * kFastBS]; sdl[(SC_BGMAX) * kFastBS] = bg > o ? bg : o; kb_max = kb; }
-          run39 = kb <= 34 ? run39 + 1 : 0;  // bg < 3.9 (THRESHOLDS[34])
-          run30 = kb <= 25 ? run30 + 1 : 0;  // bg < 3.0 (THRESHOLDS[25])
-          ev39 += run39 == u.hypoL;
-          ev30 += run30 == u.hypoL;
-          trig_lo = run39 > 0 ? INT_MAX : max(kb_min, 34);
-        }
-      }
-      }
       if (tick && ctl == next_grid_ctl) {  // timeline point (warp-uniform)
         next_grid_ctl += u.grid_ctl;
         const long long v = __double2ll_rn(bg * kFpScale);
@@ -922,11 +871,11 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       }
       G = FMR(G, (R)u.aS, bgR * (R)u.hS);
       Q1 = nQ1; Q2 = nQ2; D1 = nD1; D2 = nD2;
-      if (GT_HIST_LATE) {
-      // A non-finite bg (_kernel.py:139-141) is caught lazily: bg_sum absorbs
-      // Inf/NaN and is checked after the last step.  Until then the lane's
-      // statistics are garbage but in range; an aborted patient's are
-      // discarded and its warp re-run with it masked.
+      // Statistics of tick k's BG, binned after the update so the bin chain
+      // overlaps the model's FP64 chain.  A non-finite bg (_kernel.py:139-141)
+      // is caught lazily: bg_sum absorbs Inf/NaN and is checked after the last
+      // step.  Until then the lane's statistics are garbage but in range; an
+      // aborted patient's are discarded and its warp re-run with it masked.
       {
         // searchsorted(THRESHOLDS, bg, 'right') for bg >= 0.  THRESHOLDS[i] =
         // RN((5+i)/10), so away from a threshold the bin is floor(10 bg) - 4
@@ -968,7 +917,6 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           ev30 += run30 == u.hypoL;
           trig_lo = run39 > 0 ? INT_MAX : max(kb_min, 34);
         }
-      }
       }
     };
 
