@@ -213,11 +213,11 @@ int oracle_run_batch_philox(
             uint32_t pid = (uint32_t)(pid0 + i);
             /* noise: one Philox call per tick -> 4 normals: 3 Wiener + 1 sensor
                (the sensor one is used on controller ticks only).  The device
-               layout (csrc/gt_fast.cu philox_fast): fixed key, counter
-               (tick, pid, seed_lo, seed_hi ^ role << 24). */
+               layout (csrc/gt_fast.cu philox_fast / philox_lane): fixed key,
+               counter (pid, tick, seed_lo, seed_hi ^ role << 24). */
             int64_t ci = 0;
             for (int64_t k = 0; k < horizon_ticks; ++k) {
-                uint32_t ctr[4] = {(uint32_t)k, pid, (uint32_t)seed,
+                uint32_t ctr[4] = {pid, (uint32_t)k, (uint32_t)seed,
                                    (uint32_t)(seed >> 32) ^ (noise_role << 24)};
                 uint32_t r[4];
                 philox4x32_10(ctr, 0xA4093822u, 0x299F31D0u, r);

@@ -77,6 +77,7 @@ struct Uni {
   double dt, period, horizon_s, meal_dur_min, rs_agg, pid_ph;
   int32_t ps, n_ctl, ctl_per_day, grid_ctl, hypoL, agg;
   uint32_t nz_c2, nz_c3;  // noise counter words 2-3: seed_lo, seed_hi ^ role << 24
+  uint32_t nz_a;          // hi(nz_c2 * M1) ^ K0(0): round 1's launch word (philox_lane)
   double hyper[GT_N_HYPER];  // controller hyperparameters (parameter bank: direct operands)
   double hc[6];              // hyper-derived controller constants (same IEEE values)
 };
@@ -168,8 +169,8 @@ __device__ __forceinline__ void mulwide(uint32_t a, uint32_t b, uint32_t& lo, ui
 // Noise stream: Philox4x32-10 under a FIXED key, so the 20 round keys are
 // compile-time immediates of the LOP3s (no uniform registers, no constant
 // loads); the trial seed enters the counter instead:
-//   counter = (index, pid, seed_lo, seed_hi ^ role << 24)
-// which is injective in (index, pid, seed) for the one role the kernel draws.
+//   counter = (pid, index, seed_lo, seed_hi ^ role << 24)
+// which is injective in (pid, index, seed) for the one role the kernel draws.
 // Per round: 2 IMAD.WIDE.U32 + 2 LOP3.
 constexpr uint32_t kNoiseKey0 = 0xA4093822u, kNoiseKey1 = 0x299F31D0u;  // digits of pi
 __device__ __forceinline__ U4 philox_fast(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3) {
@@ -181,6 +182,48 @@ __device__ __forceinline__ U4 philox_fast(uint32_t c0, uint32_t c1, uint32_t c2,
     const uint32_t n0 = hi1 ^ c1 ^ (kNoiseKey0 + (uint32_t)r * 0x9E3779B9u);
     const uint32_t n2 = hi0 ^ c3 ^ (kNoiseKey1 + (uint32_t)r * 0xBB67AE85u);
     c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+  }
+  return U4{c0, c1, c2, c3};
+}
+
+// The integrator's draws: Philox4x32-10 with the counter (pid, index, seed_lo,
+// seed_hi ^ role << 24).  With the index in word 1 (xored, never multiplied in
+// round 1), rounds 1-3 reduce to 2 multiplies and 4 xors per draw given four
+// per-patient words (NoiseLane) and one launch word (Uni::nz_a):
+//   round 1: (index ^ A, lo(s2*M1), B, lo(pid*M0))        B = hi(pid*M0) ^ s3 ^ K1(0)
+//   round 2: (C, lo(B*M1), hi0 ^ D, lo0)  (lo0, hi0) = (index ^ A) * M0,
+//            C = hi(B*M1) ^ lo(s2*M1) ^ K0(1), D = lo(pid*M0) ^ K1(1)
+//   round 3: (hi1 ^ E, lo1, lo0 ^ F, lo(C*M0))  (lo1, hi1) = (hi0 ^ D) * M1,
+//            E = lo(B*M1) ^ K0(2), F = hi(C*M0) ^ K1(2)
+// then rounds 4-10 as usual: the same outputs as philox_fast(pid, index, s2, s3).
+struct NoiseLane { uint32_t d, e, f, loc; };
+__device__ __forceinline__ uint32_t noise_k0(int r) { return kNoiseKey0 + (uint32_t)r * 0x9E3779B9u; }
+__device__ __forceinline__ uint32_t noise_k1(int r) { return kNoiseKey1 + (uint32_t)r * 0xBB67AE85u; }
+__device__ __forceinline__ NoiseLane noise_lane(uint32_t pid, uint32_t s2, uint32_t s3) {
+  uint32_t lo0p, hi0p, lo1u, hi1u, loB, hiB, loC, hiC;
+  mulwide(pid, 0xD2511F53u, lo0p, hi0p);
+  mulwide(s2, 0xCD9E8D57u, lo1u, hi1u);
+  const uint32_t B = hi0p ^ s3 ^ noise_k1(0);
+  mulwide(B, 0xCD9E8D57u, loB, hiB);
+  const uint32_t C = hiB ^ lo1u ^ noise_k0(1);
+  mulwide(C, 0xD2511F53u, loC, hiC);
+  NoiseLane L;
+  L.d = lo0p ^ noise_k1(1); L.e = loB ^ noise_k0(2); L.f = hiC ^ noise_k1(2); L.loc = loC;
+  return L;
+}
+__device__ __forceinline__ U4 philox_lane(uint32_t index, const NoiseLane& L, uint32_t nz_a) {
+  uint32_t lo0, hi0, lo1, hi1;
+  mulwide(index ^ nz_a, 0xD2511F53u, lo0, hi0);       // round 2, word 0 product
+  mulwide(hi0 ^ L.d, 0xCD9E8D57u, lo1, hi1);         // round 3, word 2 product
+  uint32_t c0 = hi1 ^ L.e, c1 = lo1, c2 = lo0 ^ L.f, c3 = L.loc;
+#pragma unroll
+  for (int r = 3; r < 10; ++r) {
+    uint32_t a0, b0, a1, b1;
+    mulwide(c0, 0xD2511F53u, a0, b0);
+    mulwide(c2, 0xCD9E8D57u, a1, b1);
+    const uint32_t n0 = b1 ^ c1 ^ noise_k0(r);
+    const uint32_t n2 = b0 ^ c3 ^ noise_k1(r);
+    c0 = n0; c1 = a1; c2 = n2; c3 = a0;
   }
   return U4{c0, c1, c2, c3};
 }
@@ -336,6 +379,10 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
     const bool inrange = i < n;
     const int64_t ii = inrange ? i : 0;
     const uint32_t pid = (uint32_t)(a.pid0 + i);
+    const NoiseLane nlane = noise_lane(pid, u.nz_c2, u.nz_c3);
+    auto philox_draw = [&](uint32_t index) -> U4 {
+      return philox_lane(index, nlane, u.nz_a);
+    };
 
     // rerun mode: only warps holding a diverged lane re-simulate (lanes masked)
     const bool was_bad = a.rerun_diverged && inrange && a.status[i] == GT_STATUS_NONFINITE;
@@ -527,7 +574,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
     constexpr bool PIPE = GT_NOISE_PIPE && NOISE == GT_NOISE_PHILOX && !AGG;
     float pz0 = 0.f, pz1 = 0.f, pz2 = 0.f, pz3 = 0.f;
     auto draw_pipe = [&](int32_t kk) {
-      const U4 r = philox_fast((uint32_t)kk, pid, u.nz_c2, u.nz_c3);
+      const U4 r = philox_draw((uint32_t)kk);
       box_muller(r.x, r.y, pz0, pz1);
       box_muller(r.z, r.w, pz2, pz3);
     };
@@ -548,7 +595,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           if (tick) zm = pz3;
         } else if (NOISE == GT_NOISE_PHILOX) {
           if (!AGG) {
-            const U4 r = philox_fast((uint32_t)k, pid, u.nz_c2, u.nz_c3);
+            const U4 r = philox_draw((uint32_t)k);
             float f0, f1, f2, f3;
             box_muller(r.x, r.y, f0, f1);
             box_muller(r.z, r.w, f2, f3);
@@ -561,7 +608,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
             R s0 = 0, s1 = 0, s2 = 0;
             const uint32_t kf = (uint32_t)k * (uint32_t)u.agg;
             for (int j = 0; j < u.agg; ++j) {
-              const U4 r = philox_fast(kf + (uint32_t)j, pid, u.nz_c2, u.nz_c3);
+              const U4 r = philox_draw(kf + (uint32_t)j);
               float f0, f1, f2, f3;
               box_muller(r.x, r.y, f0, f1);
               box_muller(r.z, r.w, f2, f3);
@@ -1060,6 +1107,7 @@ static Uni make_uni(const gt_fast_args& a) {
   u.hc[5] = a.controller == GT_CTRL_PID_PUMP ? 1.0 / hy[7] : 0.0;   // PID: RN(1 / pulse size)
   u.nz_c2 = (uint32_t)a.seed;
   u.nz_c3 = (uint32_t)(a.seed >> 32) ^ (a.noise_role << 24);
+  u.nz_a = (uint32_t)(((uint64_t)u.nz_c2 * 0xCD9E8D57u) >> 32) ^ kNoiseKey0;
   return u;
 }
 
@@ -1157,14 +1205,14 @@ static int launch_one(const gt_fast_args* a, const gt::Uni& u, cudaStream_t st) 
 
 // The fused kernel's noise stream, materialised: out[(i * n_ticks + j) * 4 + l]
 // = normal l of tick k0 + j of patient pid0 + i, drawn exactly as the kernel
-// draws it (philox_fast + FP32 SFU Box-Muller; lanes 0-2 = Wiener, 3 = CGM).
+// draws it (philox_lane + FP32 SFU Box-Muller; lanes 0-2 = Wiener, 3 = CGM).
 namespace gt {
 __global__ void noise_normals_kernel(int64_t n, int64_t pid0, int64_t k0, int64_t n_ticks, const Uni u,
                                      float* out) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= n * n_ticks) return;
   const int64_t i = idx / n_ticks, j = idx - i * n_ticks;
-  const U4 r = philox_fast((uint32_t)(k0 + j), (uint32_t)(pid0 + i), u.nz_c2, u.nz_c3);
+  const U4 r = philox_lane((uint32_t)(k0 + j), noise_lane((uint32_t)(pid0 + i), u.nz_c2, u.nz_c3), u.nz_a);
   float f0, f1, f2, f3;
   box_muller(r.x, r.y, f0, f1);
   box_muller(r.z, r.w, f2, f3);
@@ -1179,6 +1227,7 @@ int gt_launch_noise_normals(int64_t n, int64_t pid0, uint64_t seed, uint32_t rol
   gt::Uni u{};
   u.nz_c2 = (uint32_t)seed;
   u.nz_c3 = (uint32_t)(seed >> 32) ^ (role << 24);
+  u.nz_a = (uint32_t)(((uint64_t)u.nz_c2 * 0xCD9E8D57u) >> 32) ^ gt::kNoiseKey0;
   const int64_t total = n * n_ticks;
   gt::noise_normals_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(n, pid0, k0, n_ticks, u, out);
   return gt_check_launch("noise_normals_kernel");

@@ -486,3 +486,16 @@ def test_nonfinite_non_glucose_state_aborts(dev, controller):
     clean.step()
     keep = np.arange(64) != 7
     assert np.array_equal(ft.metrics()["tir"][keep], clean.metrics()["tir"][keep])
+
+
+def test_philox_forms_agree_generator_vs_csr(dev):
+    """Under device Philox noise (the per-patient philox_lane form, pinned to
+    the plain rounds in test_host.py) the 3-meal generator run and the CSR
+    run of its host twin draw the same stream: bit-identical results."""
+    from paper_2202_13927_b200.protocol import ThreeMealProtocol
+    case = SimCase("sim_threemeal_dt60.npz")
+    sub = case.subset(case.valid())
+    a = _run_fast(case, sub, dev, csr=_csr_ticks(case, sub, dev), injected=None)
+    b = _run_fast(case, sub, dev, meal_spec=ThreeMealProtocol().device_spec(), injected=None)
+    for k in ("status", "ticks", "bg_hist", "bg_stats", "day_dose", "hypo_events", "timeline_pp", "x_out"):
+        assert np.array_equal(_h(getattr(a, k)), _h(getattr(b, k))), k
