@@ -39,6 +39,12 @@ extern "C" {
 #define GT_STATUS_NONFINITE 1
 #define GT_STATUS_NO_STEADY_STATE 2
 #define GT_STATUS_EXCLUDED 3 /* masked out by the caller (e.g. padding) */
+/* fused kernel, pid_pump: x0's glucagon states Z1/Z2 are not 0.  That
+ * controller never doses glucagon, so from the fasting steady state (which
+ * simulation.py:317-319 always starts from, Z1 = Z2 = 0) the glucagon chain
+ * stays exactly 0 and the kernel drops it; any other x0 is refused per
+ * patient (counted as aborted), never integrated wrongly. */
+#define GT_STATUS_BAD_INITIAL_STATE 4
 
 /* error codes */
 #define GT_OK 0

@@ -18,6 +18,7 @@ GT_STATUS_OK = 0
 GT_STATUS_NONFINITE = 1
 GT_STATUS_NO_STEADY_STATE = 2
 GT_STATUS_EXCLUDED = 3
+GT_STATUS_BAD_INITIAL_STATE = 4
 
 GT_PROTO_CSR = 0
 GT_PROTO_THREE_MEAL = 1

@@ -95,7 +95,7 @@ struct Sched {
 template <typename R>
 struct PC {
   R invVGw, aG, hTG, aI, hTI, cI, dI, ax1, bx1, ax2, bx2, ax3, bx3;
-  R hF01w, hk12, aK12, hE, rK0, sqE;
+  R hF01w45, hk12, aK12, hE, rK0, sqE;
 };
 
 template <typename R>
@@ -110,7 +110,7 @@ __device__ __forceinline__ void make_pc(const double* __restrict__ p, const Uni&
   c.ax1 = (R)(1.0 - h * p[PKA1]); c.bx1 = (R)(h * p[PKA1] * p[PSIT]);
   c.ax2 = (R)(1.0 - h * p[PKA2]); c.bx2 = (R)(h * p[PKA2] * p[PSID]);
   c.ax3 = (R)(1.0 - h * p[PKA3]); c.bx3 = (R)(h * p[PKA3] * p[PSIE]);
-  c.hF01w = (R)(h * p[PF01] * w);
+  c.hF01w45 = (R)(h * p[PF01] * w / 4.5);
   c.hk12 = (R)hk12; c.aK12 = (R)(1.0 - hk12);
   c.hE = (R)(h * p[PEGP0] * w);
   c.rK0 = (R)(h * 0.003 * 9.0 * p[PVG] * w);
@@ -444,6 +444,10 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       Q1 = (R)x0[IQ1]; Q2 = (R)x0[IQ2]; S1 = (R)x0[IS1]; S2 = (R)x0[IS2]; I = (R)x0[II];
       X1 = (R)x0[IX1]; X2 = (R)x0[IX2]; X3 = (R)x0[IX3]; D1 = (R)x0[ID1]; D2 = (R)x0[ID2];
       G = (R)x0[IGSC]; Z1 = (R)x0[IZ1]; Z2 = (R)x0[IZ2];
+      if (CTRL == GT_CTRL_PID_PUMP) {  // no glucagon: Z1 = Z2 = 0 throughout (GT_STATUS_BAD_INITIAL_STATE)
+        if (alive && (x0[IZ1] != 0.0 || x0[IZ2] != 0.0)) { alive = false; status = GT_STATUS_BAD_INITIAL_STATE; }
+        Z1 = 0; Z2 = 0;
+      }
       if (HAS_EX) { E1 = (R)x0[IE1]; E2 = (R)x0[IE2]; E3 = (R)x0[IE3]; }
       const double* c0 = a.c0 + ii * NC;
       sdl[(SC_FILT) * kFastBS] = c0[CFILT]; sdl[(SC_ICR) * kFastBS] = c0[CICR];
@@ -481,6 +485,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       Q1 = (R)LDD(SD_Q1); Q2 = (R)LDD(SD_Q2); S1 = (R)LDD(SD_S1); S2 = (R)LDD(SD_S2); I = (R)LDD(SD_I);
       X1 = (R)LDD(SD_X1); X2 = (R)LDD(SD_X2); X3 = (R)LDD(SD_X3); D1 = (R)LDD(SD_D1); D2 = (R)LDD(SD_D2);
       G = (R)LDD(SD_G); Z1 = (R)LDD(SD_Z1); Z2 = (R)LDD(SD_Z2);
+      if (CTRL == GT_CTRL_PID_PUMP) { Z1 = 0; Z2 = 0; }
       if (HAS_EX) { E1 = (R)LDD(SD_E1); E2 = (R)LDD(SD_E2); E3 = (R)LDD(SD_E3); }
       bg_sum = LDD(SD_BGSUM); day_basal = LDD(SD_DAYBASAL);
       hu_ins = (R)LDD(SD_HUINS); hu2 = (R)LDD(SD_HU2); gin = (R)LDD(SD_GIN);
@@ -880,20 +885,22 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       const R ab = HAS_EX ? FMR((R)u.sex, E3, one) : one;
       const R ub = HAS_EX ? FMR((R)u.qex, E2, one) : one;
       const R x1e = X1 * ab, x2e = X2 * ab;
-      const R t1 = x1e * Q1;
-      const R bg45 = bgR * (R)(1.0 / 4.5);
-      const R hf01 = MR_(pc.hF01w, lt_or(bg45, one));  // explicit: fixed rounding
-      const R ren = FMR(Q1, (R)u.rK1, -pc.rK0);
-      const R hren = pos_or_zero(ren);
+      // Q1's loop-carried chain is kept short: the Q1-independent terms
+      // (gut, Q2 exchange, EGP, noise) are summed first, off the chain, and
+      // the Q1 terms enter as one FMA plus the two clamped fluxes
       const R egp = FMR(-pc.hE, X3, pc.hE);
-      const R hegp = FMR((R)u.cG, Z2, pos_or_zero(egp));
-      R dq = FMR(pc.hk12, Q2, D2 * pc.hTG);
-      dq = FMR(-hf01, ub, dq);
-      dq = FMR(-(R)u.h, t1, dq);
-      dq = (dq - hren) + hegp;
+      // pid_pump doses no glucagon: Z2 = 0 exactly and cG * 0 + e == e
+      const R hegp = CTRL == GT_CTRL_PID_PUMP ? pos_or_zero(egp) : FMR((R)u.cG, Z2, pos_or_zero(egp));
+      R pq = FMR(pc.hk12, Q2, D2 * pc.hTG) + hegp;
+      pq = FMR(sqE, z0, pq);
+      const R a1 = FMR(-(R)u.h, x1e, one);                       // 1 - h x1e
+      const R hf01 = MR_(pc.hF01w45, lt_or(bgR, (R)4.5));        // h F01 w min(bg/4.5, 1)
+      const R hren = pos_or_zero(FMR(Q1, (R)u.rK1, -pc.rK0));
+      R q1n = FMR(Q1, a1, pq);
+      q1n = FMR(-hf01, ub, q1n);
+      q1n = q1n - hren;
       // projection max(x, 0) (_kernel.py:175-177): keeps NaN like `if x < 0: x = 0`
-      const R q1n = FMR(sqE, z0, Q1 + dq);
-      const R q2n = FMR(Q2, pc.aK12, (R)u.h * FMR(-x2e, Q2, t1));
+      const R q2n = FMR(Q2, FMR(-(R)u.h, x2e, pc.aK12), ((R)u.h * x1e) * Q1);
       const R nQ1 = zero_if_neg(q1n);
       const R nQ2 = zero_if_neg(q2n);
       R nD1 = FMR(D1, FMR(sqG, z1, pc.aG), gin_k);
@@ -907,9 +914,11 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       X2 = FMR(X2, pc.ax2, I * pc.bx2);
       X3 = FMR(X3, pc.ax3, I * pc.bx3);
       I = nI;
-      const R nZ2 = FMR(Z2, (R)u.aZ2, Z1 * (R)u.hTg);
-      Z1 = FMR(Z1, (R)u.aZ1, hu2);
-      Z2 = nZ2;
+      if (CTRL != GT_CTRL_PID_PUMP) {  // (pid_pump: the chain stays at 0)
+        const R nZ2 = FMR(Z2, (R)u.aZ2, Z1 * (R)u.hTg);
+        Z1 = FMR(Z1, (R)u.aZ1, hu2);
+        Z2 = nZ2;
+      }
       if (HAS_EX) {
         const R nE2 = FMR(E2, (R)u.aE2, E1 * (R)u.bE2);
         const R nE3 = FMR(E3, (R)u.aE3, E1 * (R)u.bE3);

@@ -142,7 +142,8 @@ __global__ void __launch_bounds__(kRedBS) reduce_patients_kernel(gt_reduce_args 
     const int stv = inr ? a.status[i] : GT_STATUS_EXCLUDED;
     const bool ok = inr && stv == GT_STATUS_OK;
     n_ok += ok;
-    n_ab += inr && (stv == GT_STATUS_NONFINITE || stv == GT_STATUS_NO_STEADY_STATE);
+    n_ab += inr && (stv == GT_STATUS_NONFINITE || stv == GT_STATUS_NO_STEADY_STATE ||
+                    stv == GT_STATUS_BAD_INITIAL_STATE);
     // ---- histogram, below-threshold envelope, TIR ticks
     int cum = 0, c25 = 0, c34 = 0, c95 = 0, c134 = 0;
     for (int b = 0; b < GT_N_BG_BINS; ++b) {

@@ -17,7 +17,8 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import analytics, engine, rng
-from ._lib import GT_STATUS_EXCLUDED, GT_STATUS_NO_STEADY_STATE, GT_STATUS_NONFINITE, GT_STATUS_OK
+from ._lib import (GT_STATUS_BAD_INITIAL_STATE, GT_STATUS_EXCLUDED, GT_STATUS_NO_STEADY_STATE, GT_STATUS_NONFINITE,
+                   GT_STATUS_OK)
 from .analytics import TrialAccumulator, WorstCase
 from .config import SimulationError, sizes
 from .controller import device_code, hyper_vector, icr_initial_factor
@@ -208,7 +209,8 @@ class FastTrial:
                           red.bg_hist_total, red.below_min, red.below_max, red.minmax_bg_bits, red.timeline,
                           red.dose_hist, red.dose_sum_fp, red.metric_hist, red.worst)
         acc.n_patients = int(counts[0])
-        aborted = np.nonzero((status == GT_STATUS_NONFINITE) | (ss == GT_STATUS_NO_STEADY_STATE))[0]
+        aborted = np.nonzero((status == GT_STATUS_NONFINITE) | (status == GT_STATUS_BAD_INITIAL_STATE)
+                             | (ss == GT_STATUS_NO_STEADY_STATE))[0]
         acc.n_aborted = int(aborted.size)
         acc.aborted_ids = tuple(int(self.pid0 + i) for i in aborted)
         acc.sum_bg_fp = (int(counts[4]) << 64) + (int(counts[2]) & 0xFFFFFFFFFFFFFFFF)

@@ -51,14 +51,11 @@ def test_pid_parity_kernel_bitwise_vs_oracle(dev, oracle, name):
     assert np.allclose(basal_vol / 0.05, np.round(basal_vol / 0.05), atol=1e-9)
 
 
-@pytest.mark.parametrize("name", PID_SIMS)
-def test_pid_fused_kernel_matches_to_rounding(dev, name):
+def _pid_fused(case, sub, dev, x0=None):
+    """The fused pid_pump kernel on a golden case's injected noise (CSR protocol)."""
     import torch
     from paper_2202_13927_b200 import engine, rng
     from paper_2202_13927_b200.protocol import ProtocolArrays, compile_ticks
-    case = SimCase(name)
-    g = case.g
-    sub = case.subset(case.valid())
     n = sub["params"].shape[0]
     D = lambda a, t=torch.float64: engine.dev(a, t, dev)
     tas = []
@@ -79,11 +76,21 @@ def test_pid_fused_kernel_matches_to_rounding(dev, name):
     csr["ex_start_s"] = D(nz(cat("ex_start", np.float64)))
     inj = {"wiener": D(sub["wiener"].reshape(-1)), "has_noise": D(sub["has_noise"], torch.uint8),
            "meas": D(sub["meas"].reshape(-1))}
-    ins = {"params": D(sub["params"]), "x0": D(sub["x0"]), "c0": D(sub["c0"]), "hyper": D(case.hyper),
-           "assumed_basal": D(sub["basal"])}
+    ins = {"params": D(sub["params"]), "x0": D(sub["x0"] if x0 is None else x0), "c0": D(sub["c0"]),
+           "hyper": D(case.hyper), "assumed_basal": D(sub["basal"])}
     outs = engine.alloc_fast_outputs(n, int(case.ids[sub["idx"][0]]), case.sz, dev, per_patient_timeline=True)
     engine.launch_fast(ins, outs, case.sz, case.config.dt_s, case.config.controller_period_s, case.config.seed,
                        rng.ROLE_DEVICE_NOISE, 15, dev, csr=csr, injected=inj, controller_code=1)
+    return outs
+
+
+@pytest.mark.parametrize("name", PID_SIMS)
+def test_pid_fused_kernel_matches_to_rounding(dev, name):
+    case = SimCase(name)
+    g = case.g
+    sub = case.subset(case.valid())
+    n = sub["params"].shape[0]
+    outs = _pid_fused(case, sub, dev)
     st, hist, tl = outs.bg_stats.cpu().numpy(), outs.bg_hist.cpu().numpy(), outs.timeline_pp.cpu().numpy()
     ties = 0
     for j, i in enumerate(sub["idx"]):
@@ -139,3 +146,25 @@ def test_simulate_closed_loop_with_pid_object(dev):
     assert r.status == "ok" and r.trace.shape == (1440, 8)
     vol = r.trace[::5, 5] * 300.0 / 3600.0
     assert np.allclose(vol / 0.05, np.round(vol / 0.05), atol=1e-9)
+
+
+def test_pid_fused_refuses_nonzero_glucagon_state(dev):
+    """pid_pump never doses glucagon, so the fused kernel drops the glucagon
+    chain (Z1 = Z2 = 0 from the fasting steady state).  A patient whose x0
+    has a glucagon state is refused (GT_STATUS_BAD_INITIAL_STATE, counted as
+    aborted), never integrated wrongly; the other patients are unaffected."""
+    from paper_2202_13927_b200._lib import GT_STATUS_BAD_INITIAL_STATE
+    from paper_2202_13927_b200.layout import IZ1, IZ2
+    case = SimCase("sim_pid_threemeal_dt60.npz")
+    sub = case.subset(case.valid())
+    assert not sub["x0"][:, [IZ1, IZ2]].any()
+    ref = _pid_fused(case, sub, dev)
+    x0 = sub["x0"].copy()
+    x0[0, IZ1] = 1e-3
+    x0[1, IZ2] = 1e-3
+    out = _pid_fused(case, sub, dev, x0=x0)
+    st = out.status.cpu().numpy()
+    assert list(st[:2]) == [GT_STATUS_BAD_INITIAL_STATE] * 2
+    assert np.array_equal(st[2:], ref.status.cpu().numpy()[2:])
+    assert np.array_equal(out.bg_hist.cpu().numpy()[:, 2:], ref.bg_hist.cpu().numpy()[:, 2:])
+    assert np.array_equal(out.bg_stats.cpu().numpy()[:, 2:], ref.bg_stats.cpu().numpy()[:, 2:])
