@@ -309,6 +309,24 @@ __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
 
+// Saved slice state is written with an L2 evict_last policy so it stays in
+// L2 until the next slice of the same warp reads it, and the read lines are
+// then discarded (no write-back): the state round trip does not reach HBM.
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void st_keep(double* a, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" :: "l"(a), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_keep(int* a, int v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" :: "l"(a), "r"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void l2_discard_line(const void* a) {  // a: 128-byte aligned
+  asm volatile("discard.global.L2 [%0], 128;" :: "l"(a) : "memory");
+}
+
 // Shared-memory per-lane slots (SoA, [slot][tid]).
 enum { SC_FILT, SC_ICR, SC_SUSP, SC_LASTG, SC_WEND, SC_WPEAK, SC_WMIN,
        SC_BGMIN, SC_BGMAX, SC_DBOLUS, SC_DGLUC, SC_ANNCARBS, SC_ASSUMED, N_SC };
@@ -319,7 +337,8 @@ enum { SD_Q1, SD_Q2, SD_S1, SD_S2, SD_I, SD_X1, SD_X2, SD_X3, SD_D1, SD_D2, SD_G
        SD_E1, SD_E2, SD_E3, SD_BGSUM, SD_DAYBASAL, SD_HUINS, SD_HU2, SD_GIN, SD_MC0, SD_MC1,
        SD_MC2, SD_SC0, SD_N = SD_SC0 + N_SC };
 enum { SV_MKS, SV_MKE, SV_KBMIN, SV_KBMAX, SV_RUN39, SV_RUN30, SV_EV39,
-       SV_EV30, SV_ALIVE, SV_STATUS, SV_DEATH, SV_MK0, SV_SI0 = SV_MK0 + 9, SV_N = SV_SI0 + N_SI };
+       SV_EV30, SV_ALIVE, SV_STATUS, SV_DEATH, SV_MK0, SV_SI0 = SV_MK0 + 9, SV_H0 = SV_SI0 + N_SI,
+       SV_N = SV_H0 + kHistWords };  // SV_H0: the packed uint8 histogram counters
 
 template <int PROTO, int NOISE, typename R, bool AGG, bool TRACE, int CTRL>
 __global__ void __launch_bounds__(kFastBS, GT_FAST_MINB)
@@ -491,6 +510,9 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       hu_ins = (R)LDD(SD_HUINS); hu2 = (R)LDD(SD_HU2); gin = (R)LDD(SD_GIN);
       for (int q = 0; q < N_SC; ++q) sdl[(q) * kFastBS] = LDD(SD_SC0 + q);
       for (int q = 0; q < N_SI; ++q) sil[(q) * kFastBS] = LDI(SV_SI0 + q);
+      // the histogram counters carried over from the previous slice
+      for (int w = 0; w < kHistWords; ++w) s_hist[w * kFastBS + tid] = (uint32_t)LDI(SV_H0 + w);
+      asm volatile("" ::: "memory");  // before the asm increments
       if (PROTO == GT_PROTO_THREE_MEAL) {
         for (int j = 0; j < 3; ++j) {
           s_mc[j][tid] = LDD(SD_MC0 + j);
@@ -508,6 +530,15 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       status = LDI(SV_STATUS); death_tick = LDI(SV_DEATH);
 #undef LDD
 #undef LDI
+      // every lane of the warp has read its slots: drop this warp's slot
+      // lines (2 x 128 B per FP64 field, 128 B per int field) from L2
+      __syncwarp();
+      for (int r = lane; r < 2 * SD_N + SV_N; r += 32) {
+        const char* line = r < 2 * SD_N
+            ? reinterpret_cast<const char*>(sch.sd + (int64_t)(r >> 1) * npad + warp_global * 32) + (r & 1) * 128
+            : reinterpret_cast<const char*>(sch.si + (int64_t)(r - 2 * SD_N) * npad + warp_global * 32);
+        l2_discard_line(line);
+      }
       alive = alive && inrange && !was_bad;  // padding lanes read patient 0's slot
     }
 
@@ -1012,7 +1043,10 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         long long* dst = (long long*)a.timeline_warp + ((int64_t)g_idx * n_warps + warp_global) * 3;
         dst[0] = 0; dst[1] = LLONG_MAX; dst[2] = LLONG_MIN;
       }
-    flush_hist();  // empties this thread's shared histogram for its next unit
+    // the last slice drains the counters into the HBM columns; earlier ones
+    // carry them in the saved lane state (no read-modify-write of the
+    // [247][n] columns per slice).  Either way the shared counters end empty.
+    if (last) flush_hist();
 
     if (last && alive && !(fabs(bg_sum) < INFINITY)) {  // the lazy bg check (see the step)
       alive = false; status = GT_STATUS_NONFINITE; death_tick = (int)a.horizon_ticks;
@@ -1023,8 +1057,9 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         const int64_t npad = (int64_t)sch.n_warps * 32;
         double* sd = sch.sd + i;
         int* si = sch.si + i;
-#define STD(f, v) sd[(int64_t)(f) * npad] = (v)
-#define STI(f, v) si[(int64_t)(f) * npad] = (v)
+        const uint64_t keep = l2_evict_last_policy();
+#define STD(f, v) st_keep(sd + (int64_t)(f) * npad, (double)(v), keep)
+#define STI(f, v) st_keep(si + (int64_t)(f) * npad, (int)(v), keep)
         STD(SD_Q1, Q1); STD(SD_Q2, Q2); STD(SD_S1, S1); STD(SD_S2, S2); STD(SD_I, I);
         STD(SD_X1, X1); STD(SD_X2, X2); STD(SD_X3, X3); STD(SD_D1, D1); STD(SD_D2, D2);
         STD(SD_G, G); STD(SD_Z1, Z1); STD(SD_Z2, Z2);
@@ -1033,6 +1068,11 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         STD(SD_HU2, hu2); STD(SD_GIN, gin);
         for (int q = 0; q < N_SC; ++q) STD(SD_SC0 + q, sdl[(q) * kFastBS]);
         for (int q = 0; q < N_SI; ++q) STI(SV_SI0 + q, sil[(q) * kFastBS]);
+        asm volatile("" ::: "memory");  // after the asm increments
+        for (int w = 0; w < kHistWords; ++w) {
+          STI(SV_H0 + w, (int)s_hist[w * kFastBS + tid]);
+          s_hist[w * kFastBS + tid] = 0u;
+        }
         if (PROTO == GT_PROTO_THREE_MEAL) {
           for (int j = 0; j < 3; ++j) {
             STD(SD_MC0 + j, s_mc[j][tid]);
@@ -1125,23 +1165,23 @@ static Uni make_uni(const gt_fast_args& a) {
 // Number of horizon slices.  Per-warp cost varies with the patients'
 // trajectories (hypo runs, meals), so the persistent schedule balances better
 // with several units per resident warp slot: aim for >= 6 rounds of units,
-// then take the count in that range with the least wave quantisation
-// ceil(c * warps / slots) / c (ties: fewer slices).  A slice keeps >= 48
-// controller periods so save / restore stays negligible.  Measured on
-// 100k x 4 weeks: 3 slices 41.3 ms, 6-32 slices 39.2-40.1 ms.
+// then take the fewest slices whose wave quantisation ceil(c * warps / slots)
+// / c is within 1 % of the least in that range.  A slice keeps >= 48
+// controller periods; each boundary moves ~0.65 KB per lane through L2.
+// Measured on 100k x 4 weeks (PID): 5 slices 38.0 ms, 9-25 slices 35.9-36.6 ms.
 static int choose_chunks(int64_t warps, int64_t slots, int n_ctl) {
   const int c_max = std::max(1, std::min(32, n_ctl / 48));
   // (fewer warps than slots: one slice; a warp's slices run in sequence anyway)
   const int c_min = warps < slots ? 1
                                   : (int)std::max<int64_t>(1, std::min<int64_t>(c_max, (6 * slots + warps - 1) / warps));
-  int best = c_min;
+  // the fewest slices whose quantised rounds come within 1 % of the best:
+  // every slice boundary saves and restores ~0.65 KB per lane
+  auto t_of = [&](int c) { return (double)((c * warps + slots - 1) / slots) / c; };
   double best_t = 1e300;
-  for (int c = c_min; c <= c_max; ++c) {
-    const double rounds = (double)((c * warps + slots - 1) / slots);
-    const double t = rounds / c;
-    if (t < best_t - 1e-9) { best_t = t; best = c; }
-  }
-  return best;
+  for (int c = c_min; c <= c_max; ++c) best_t = std::min(best_t, t_of(c));
+  for (int c = c_min; c <= c_max; ++c)
+    if (t_of(c) <= best_t * 1.01) return c;
+  return c_min;
 }
 
 template <int PROTO, int NOISE, typename R, bool AGG, bool TRACE, int CTRL>
@@ -1173,7 +1213,7 @@ static int launch_sched(const gt_fast_args* a, const gt::Uni& u, cudaStream_t st
   const size_t bytes_i = sizeof(int) * (1 + (size_t)warps);
   const size_t n_pad = (size_t)warps * 32;   // every lane of a warp owns a saved-state slot
   const size_t bytes_state = s.n_chunks > 1 ? n_pad * (gt::SD_N * sizeof(double) + gt::SV_N * sizeof(int)) : 0;
-  const size_t need = ((bytes_i + 15) & ~size_t(15)) + bytes_state;
+  const size_t need = bytes_i + 256 + bytes_state;  // state rows 256-byte aligned (L2 line discards)
   char* scratch = static_cast<char*>(a->scratch);
   const bool own = scratch == nullptr;
   if (own) {
@@ -1190,7 +1230,7 @@ static int launch_sched(const gt_fast_args* a, const gt::Uni& u, cudaStream_t st
   s.counter = reinterpret_cast<int*>(scratch);
   s.done = s.counter + 1;
   if (bytes_state) {
-    char* base = scratch + ((bytes_i + 15) & ~size_t(15));
+    char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(scratch) + bytes_i + 255) & ~uintptr_t(255));
     s.sd = reinterpret_cast<double*>(base);
     s.si = reinterpret_cast<int*>(base + n_pad * gt::SD_N * sizeof(double));
   }
@@ -1246,7 +1286,7 @@ int gt_launch_noise_normals(int64_t n, int64_t pid0, uint64_t seed, uint32_t rol
 int64_t gt_fast_scratch_need(int64_t n) {
   const int64_t warps = (n + 31) / 32;
   const int64_t bytes_i = (int64_t)sizeof(int) * (1 + warps);
-  return ((bytes_i + 15) & ~int64_t(15)) + warps * 32 * (int64_t)(gt::SD_N * sizeof(double) + gt::SV_N * sizeof(int));
+  return bytes_i + 256 + warps * 32 * (int64_t)(gt::SD_N * sizeof(double) + gt::SV_N * sizeof(int));
 }
 
 int gt_launch_fast(const gt_fast_args* a, cudaStream_t st) {
