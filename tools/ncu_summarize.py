@@ -75,5 +75,18 @@ lines.append(f"  total warp-instructions {tot}" + (f"  = {tot / warp_steps:.1f} 
 for op, c in ops.most_common(30):
     per = f"{c / warp_steps:7.2f}/step" if warp_steps else ""
     lines.append(f"  {op:<10s} {100 * c / tot:6.2f} %  {per}")
+# warp-state sampling: where the warps wait (latency vs issue)
+stalls = []
+for k, x in zip(h, v):
+    if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("_not_issued"):
+        try:
+            stalls.append((float(x.replace(",", "")), k[len("smsp__pcsamp_warps_issue_stalled_"):]))
+        except ValueError:
+            pass
+tot_s = sum(c for c, _ in stalls) or 1.0
+lines.append("\n[warp-state samples (smsp__pcsamp_warps_issue_stalled_*)]")
+for c, k in sorted(stalls, reverse=True):
+    if c > 0:
+        lines.append(f"  {k:<28s} {100 * c / tot_s:5.1f} %")
 open(f"{prefix}_ncu.txt", "w").write("\n".join(lines) + "\n")
 print(f"wrote {prefix}_ncu.txt, {prefix}_traffic.json; {tot / warp_steps if warp_steps else tot:.1f}")
