@@ -695,9 +695,13 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         ex_active = k >= ex_ks_c;   // (k < ex_ke_c here)
         hrr = ex_active ? ex_hrr_c : 0.0;
       }
-      // controller tick (_kernel.py:98-135)
+      // controller tick (_kernel.py:98-135): the check, the announcement and
+      // the reading here.  Under kLateControl the controller itself runs
+      // after the Euler update of the other states (only S1 / Z1 take its
+      // output), so its serial FP64 chain overlaps the model's
+      double t_s = 0.0, announced = 0.0, phase = -1.0, y = 0.0;
       if (tick) {
-        const double t_s = (double)k * u.dt;
+        t_s = (double)k * u.dt;
         // The reference checks every state at every tick (_kernel.py:98-103).
         // Non-finiteness is absorbing here: a linear update a*x + b (a > 0)
         // keeps Inf/NaN, a projected Q1/Q2 at +Inf turns NaN the next step
@@ -718,7 +722,6 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           if (acc != acc) { alive = false; status = GT_STATUS_NONFINITE; death_tick = k; }
         }
         // announced carbs starting within [t, t+P)
-        double announced = 0.0;
         if (PROTO == GT_PROTO_THREE_MEAL) {
           // meals are >= 1 h apart, so at most one starts in a period: the
           // day's next announcement is a cursor (0 + carbs = the reference's sum)
@@ -742,13 +745,14 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           }
           sil[(SI_ANNM) * kFastBS] = am; sil[(SI_ANNKP) * kFastBS] = akp; sdl[(SC_ANNCARBS) * kFastBS] = carbs;
         }
-        double phase = -1.0;
         if (HAS_EX && ex_active) {
           const int p = sil[(SI_EXPTR) * kFastBS];
           if (a.ex_announced[ex_lo + p] != 0.0) phase = t_s - a.ex_start_s[ex_lo + p];
         }
-        const double y = A_((double)G, M_(u.sqrtR, zm));
+        y = A_((double)G, M_(u.sqrtR, zm));
         if (TRACE) tr_y = y;
+      }
+      auto control = [&]() {
         // ---- controller_step_vec (controller.py:343-458); state in shared
         // memory.  Explicit IEEE operations in the reference's order: the
         // controller is bit-identical to the reference's for identical readings.
@@ -869,7 +873,11 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           sdl[(SC_DBOLUS) * kFastBS] += b_bolus;
           sdl[(SC_DGLUC) * kFastBS] += b_gluc;
         }
-      }
+      };
+      // late control measured -1.2 % under pid_pump and +3.8 % under
+      // dual_hormone (whose larger controller then spills): pid_pump only
+      constexpr bool kLateControl = !TRACE && CTRL == GT_CTRL_PID_PUMP;
+      if (tick && !kLateControl) control();
       // statistics at tick k (_kernel.py:137-160)
       double bg = (double)MR_(Q1, pc.invVGw);  // explicit: never fused into the sums below
       if (tick && ctl == 0) {
@@ -938,7 +946,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       R nD2 = FMR(D2, FMR(sqG, z2, pc.aG), D1 * pc.hTG);
       if (CLAMP_GUT) { nD1 = zero_if_neg(nD1); nD2 = zero_if_neg(nD2); }
       const R nS2 = FMR(S2, pc.aI, S1 * pc.hTI);
-      S1 = FMR(S1, pc.aI, hu_ins);
+      if (!tick || !kLateControl) S1 = FMR(S1, pc.aI, hu_ins);
       const R nI = FMR(I, pc.cI, S2 * pc.dI);
       S2 = nS2;
       X1 = FMR(X1, pc.ax1, I * pc.bx1);
@@ -947,7 +955,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       I = nI;
       if (CTRL != GT_CTRL_PID_PUMP) {  // (pid_pump: the chain stays at 0)
         const R nZ2 = FMR(Z2, (R)u.aZ2, Z1 * (R)u.hTg);
-        Z1 = FMR(Z1, (R)u.aZ1, hu2);
+        if (!tick || !kLateControl) Z1 = FMR(Z1, (R)u.aZ1, hu2);
         Z2 = nZ2;
       }
       if (HAS_EX) {
@@ -958,6 +966,11 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       }
       G = FMR(G, (R)u.aS, bgR * (R)u.hS);
       Q1 = nQ1; Q2 = nQ2; D1 = nD1; D2 = nD2;
+      if (tick && kLateControl) {  // the controller, then the two states that take its output
+        control();
+        S1 = FMR(S1, pc.aI, hu_ins);
+        if (CTRL != GT_CTRL_PID_PUMP) Z1 = FMR(Z1, (R)u.aZ1, hu2);
+      }
       // Statistics of tick k's BG, binned after the update so the bin chain
       // overlaps the model's FP64 chain.  A non-finite bg (_kernel.py:139-141)
       // is caught lazily: bg_sum absorbs Inf/NaN and is checked after the last
