@@ -55,7 +55,7 @@ def fp64_peak():
         37.2, "nominal 148 SM x 64 DFMA x 2 x 1.965 GHz (fallback)")
 
 
-TRAFFIC_FILES = {"pid_pump": "r01e_fast_kernel_pid_traffic.json", "dual_hormone": "r01e_fast_kernel_dual_traffic.json"}
+TRAFFIC_FILES = {"pid_pump": "r01f_fast_kernel_pid_traffic.json", "dual_hormone": "r01f_fast_kernel_dual_traffic.json"}
 
 
 def measured_traffic(n_patients, controller="pid_pump"):

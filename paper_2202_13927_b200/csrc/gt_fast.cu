@@ -875,8 +875,9 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         }
       };
       // late control measured -1.2 % under pid_pump and +3.8 % under
-      // dual_hormone (whose larger controller then spills): pid_pump only
-      constexpr bool kLateControl = !TRACE && CTRL == GT_CTRL_PID_PUMP;
+      // dual_hormone (whose larger controller then spills), and +2 % on the
+      // CSR (NorthernYear) path: pid_pump with the generated meals only
+      constexpr bool kLateControl = !TRACE && CTRL == GT_CTRL_PID_PUMP && PROTO == GT_PROTO_THREE_MEAL;
       if (tick && !kLateControl) control();
       // statistics at tick k (_kernel.py:137-160)
       double bg = (double)MR_(Q1, pc.invVGw);  // explicit: never fused into the sums below
