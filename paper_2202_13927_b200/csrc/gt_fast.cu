@@ -1066,7 +1066,10 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       alive = false; status = GT_STATUS_NONFINITE; death_tick = (int)a.horizon_ticks;
     }
     if (!last) {
-      // ---- save the lane state for the next slice (padding lanes too)
+      // ---- save the lane state for the next slice (padding lanes too); the
+      // warp barrier orders these stores after the other lanes' discards of
+      // the same lines at this unit's restore
+      __syncwarp();
       {
         const int64_t npad = (int64_t)sch.n_warps * 32;
         double* sd = sch.sd + i;
