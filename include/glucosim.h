@@ -19,7 +19,7 @@
 extern "C" {
 #endif
 
-#define GT_ABI_VERSION 2  /* 2: gt_fast_args.hyper by value */
+#define GT_ABI_VERSION 3  /* 2: gt_fast_args.hyper by value; 3: dose_sum_fp [6] (128-bit) */
 
 /* layouts — hovorka.py:38-55, controller.py:32-41, analytics.py:21-37 */
 #define GT_N_STATES 16
@@ -257,7 +257,8 @@ typedef struct gt_reduce_args {
     int64_t *minmax_bg_bits;  /* [2] order-preserving int64 of min_bg / max_bg */
     int64_t *timeline;        /* [3][n_grid] sum, min, max */
     int64_t *dose_hist;       /* [3][201] */
-    int64_t *dose_sum_fp;     /* [3] */
+    int64_t *dose_sum_fp;     /* [6] low 64 bits (unsigned) of the 3 fixed-point dose
+                                 sums, then their 3 carry words (high 64 bits) */
     int64_t *worst;           /* [4] key_bits(min_bg), ticks_below_3, pid, found */
     /* per-patient metric arrays (optional, NULL to skip): [n] each */
     float *metric_tir;        /* fraction 3.9-10 */

@@ -160,7 +160,7 @@ def load(path: str | None = None):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.gt_abi_version() != 2:   # include/glucosim.h GT_ABI_VERSION
+    if lib.gt_abi_version() != 3:   # include/glucosim.h GT_ABI_VERSION
         raise GlucosimError("libglucosim ABI version mismatch")
     if path is None:
         _lib = lib

@@ -102,7 +102,11 @@ static int check_config(const char* who, double dt_s, double period_s, int64_t p
   REQUIRE(grid_step_ticks > 0, "%s: grid_step_ticks must be positive", who);
   REQUIRE(n_grid == (horizon_ticks + grid_step_ticks - 1) / grid_step_ticks,
           "%s: n_grid inconsistent with horizon/grid step", who);
-  REQUIRE(n_days >= 1, "%s: n_days must be >= 1", who);
+  // the kernels index day_dose by t // 86400 without a bound: the buffer
+  // must hold every day of the horizon (advisor finding r01)
+  const double days = std::ceil((double)horizon_ticks * dt_s / 86400.0);
+  REQUIRE(n_days == (days < 1.0 ? 1 : (int64_t)days),
+          "%s: n_days must be max(1, ceil(horizon_ticks * dt_s / 86400))", who);
   return GT_OK;
 }
 
@@ -141,9 +145,6 @@ int gt_simulate_fast(const gt_fast_args* a, void* stream) {
           "gt_simulate_fast: the controller period must divide one day");
   REQUIRE((double)a->horizon_ticks * a->dt_s < 2147483647.0,
           "gt_simulate_fast: horizon too long for int32 tick arithmetic");
-  REQUIRE(a->n_days == (int64_t)std::ceil((double)a->horizon_ticks * a->dt_s / 86400.0) ||
-              a->n_days == 1,
-          "gt_simulate_fast: n_days inconsistent with the horizon");
   REQUIRE(a->params && a->x0 && a->c0 && a->assumed_basal && a->status && a->ticks &&
               a->bg_hist && a->bg_stats && a->day_dose && a->hypo_events && a->timeline_warp,
           "gt_simulate_fast: null required pointer");
@@ -157,6 +158,7 @@ int gt_simulate_fast(const gt_fast_args* a, void* stream) {
   if (a->noise_kind == GT_NOISE_INJECTED)
     REQUIRE(a->wiener && a->has_noise && a->meas, "gt_simulate_fast: injected noise arrays required");
   REQUIRE(a->hypo_min_ticks > 0, "gt_simulate_fast: hypo_min_ticks must be positive");
+  REQUIRE(a->n_slices >= 0, "gt_simulate_fast: n_slices must be >= 0 (0 = automatic)");
   return gt_launch_fast(a, S(stream));
 }
 

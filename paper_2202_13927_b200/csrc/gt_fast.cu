@@ -1205,13 +1205,14 @@ template <int PROTO, int NOISE, typename R, bool AGG, bool TRACE, int CTRL>
 static int launch_sched(const gt_fast_args* a, const gt::Uni& u, cudaStream_t st) {
   constexpr int kDyn = gt::kHistWords * gt::kFastBS * 4;
   auto kern = gt::fast_kernel<PROTO, NOISE, R, AGG, TRACE, CTRL>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
-    attr = true;
-  }
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
+  // the > 48 KB dynamic shared-memory opt-in is a per-device attribute: set
+  // it on every launch (cheap) rather than once per process
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn) != cudaSuccess) {
+    gt_set_error("gt_simulate_fast: cudaFuncSetAttribute(MaxDynamicSharedMemorySize) failed");
+    return GT_ECUDA;
+  }
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, gt::kFastBS, kDyn);
   if (per_sm < 1) per_sm = 1;
@@ -1219,7 +1220,10 @@ static int launch_sched(const gt_fast_args* a, const gt::Uni& u, cudaStream_t st
   const int64_t slots = (int64_t)sms * per_sm * (gt::kFastBS / 32);
   const int n_ctl = u.n_ctl;
   // a traced launch runs unsliced (the held trace columns are not saved between slices)
-  const int chunks = TRACE ? 1 : a->n_slices > 0 ? std::min(a->n_slices, n_ctl) : choose_chunks(warps, slots, n_ctl);
+  // an explicit slice count is clamped to the horizon's periods and to the
+  // 32-bit unit counter (warps * slices < 2^31; advisor finding r01)
+  const int max_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(n_ctl, INT32_MAX / std::max<int64_t>(warps, 1)));
+  const int chunks = TRACE ? 1 : a->n_slices > 0 ? std::min(a->n_slices, max_chunks) : std::min(choose_chunks(warps, slots, n_ctl), max_chunks);
   gt::Sched s{};
   s.n_warps = (int)warps;
   s.n_chunks = chunks;

@@ -89,6 +89,14 @@ __device__ __forceinline__ long long wmax64(long long v) {
   return v;
 }
 
+// Unsigned 128-bit accumulation as a low word + carry word (the reference's
+// fixed-point sums are Python ints): every partial is >= 0, so a wrapped low
+// word (old + v < old) carries exactly one into the high word.
+__device__ __forceinline__ void add_u128(unsigned long long* lo, unsigned long long* hi, unsigned long long v) {
+  const unsigned long long old = atomicAdd(lo, v);
+  if (old + v < old) atomicAdd(hi, 1ull);
+}
+
 struct Worst { long long kb; long long neg_t3; long long pid; };
 __device__ __forceinline__ bool worst_less(const Worst& a, const Worst& b) {
   // analytics.py:150-153: (min_bg, -ticks_below_3, patient_id)
@@ -106,7 +114,7 @@ __global__ void reduce_init_kernel(gt_reduce_args a, Worst* wblk, int nblk) {
   if (t < GT_N_THRESHOLDS) { a.below_min[t] = LLONG_MAX; a.below_max[t] = 0; }
   if (t == 0) { a.minmax_bg_bits[0] = LLONG_MAX; a.minmax_bg_bits[1] = LLONG_MIN; }
   if (t < 3 * kDoseBins) a.dose_hist[t] = 0;
-  if (t < 3) a.dose_sum_fp[t] = 0;
+  if (t < 6) a.dose_sum_fp[t] = 0;  // low words [0..2], carry words [3..5]
   if (a.metric_hist && t < 7 * kTirBins) a.metric_hist[t] = 0;
   if (t < nblk) wblk[t] = Worst{LLONG_MAX, LLONG_MAX, LLONG_MAX};
 }
@@ -120,6 +128,7 @@ __global__ void __launch_bounds__(kRedBS) reduce_patients_kernel(gt_reduce_args 
   __shared__ unsigned long long s_mr[3 * kTirBins];  // tbr70, tar180 combined-range hists
   __shared__ unsigned long long s_tir[GT_N_RANGES];
   __shared__ long long s_misc[8];  // n_ok, n_abort, sum_fp, d0, d1, d2, minb, maxb
+  __shared__ unsigned long long s_carry[4];  // carry words of sum_fp, d0, d1, d2
   __shared__ Worst s_w[kRedBS / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int k = tid; k < GT_N_BG_BINS; k += kRedBS) s_bg[k] = 0;
@@ -130,6 +139,7 @@ __global__ void __launch_bounds__(kRedBS) reduce_patients_kernel(gt_reduce_args 
   for (int k = tid; k < 3 * kTirBins; k += kRedBS) s_mr[k] = 0;
   if (tid < GT_N_RANGES) s_tir[tid] = 0;
   if (tid < 8) s_misc[tid] = (tid == 6) ? LLONG_MAX : (tid == 7 ? LLONG_MIN : 0);
+  if (tid < 4) s_carry[tid] = 0;
   __syncthreads();
 
   const int64_t n = a.n;
@@ -207,7 +217,7 @@ __global__ void __launch_bounds__(kRedBS) reduce_patients_kernel(gt_reduce_args 
     const long long wmn = wmin64(ok ? ordered_bits(mnb) : LLONG_MAX);
     const long long wmx = wmax64(ok ? ordered_bits(mxb) : LLONG_MIN);
     if (lane == 0) {
-      atomicAdd((unsigned long long*)&s_misc[2], (unsigned long long)ws);
+      add_u128((unsigned long long*)&s_misc[2], &s_carry[0], (unsigned long long)ws);
       atomicMin(&s_misc[6], wmn);
       atomicMax(&s_misc[7], wmx);
     }
@@ -233,7 +243,7 @@ __global__ void __launch_bounds__(kRedBS) reduce_patients_kernel(gt_reduce_args 
       }
       const long long fp = ok ? __double2ll_rn(psum * kFpScale) : 0;
       const long long wsf = wsum64(fp);
-      if (lane == 0) atomicAdd((unsigned long long*)&s_misc[3 + k], (unsigned long long)wsf);
+      if (lane == 0) add_u128((unsigned long long*)&s_misc[3 + k], &s_carry[1 + k], (unsigned long long)wsf);
     }
     // ---- worst case candidate (analytics.py:150-153, 260-265)
     if (ok) {
@@ -287,15 +297,17 @@ __global__ void __launch_bounds__(kRedBS) reduce_patients_kernel(gt_reduce_args 
   if (tid == 0) {
     atomicAdd((unsigned long long*)&a.counts[0], (unsigned long long)s_misc[0]);
     atomicAdd((unsigned long long*)&a.counts[1], (unsigned long long)s_misc[1]);
-    {
-      // sum_bg_fp can exceed int64 for 1M x 52-week trials (the reference
-      // uses Python ints): 128-bit accumulation, low word + carry word.
-      const unsigned long long v = (unsigned long long)s_misc[2];
-      const unsigned long long old = atomicAdd((unsigned long long*)&a.counts[2], v);
-      if (old + v < old) atomicAdd((unsigned long long*)&a.counts[4], 1ull);
-    }
+    // sum_bg_fp and the dose sums can exceed int64 (1M x 52-week trials; the
+    // reference uses Python ints): 128-bit accumulation, low word + carry
+    // word, per warp into the block partial and per block into the output
+    add_u128((unsigned long long*)&a.counts[2], (unsigned long long*)&a.counts[4], (unsigned long long)s_misc[2]);
+    if (s_carry[0]) atomicAdd((unsigned long long*)&a.counts[4], s_carry[0]);
     atomicAdd((unsigned long long*)&a.counts[3], (unsigned long long)(s_misc[0] * a.n_days));
-    for (int k = 0; k < 3; ++k) atomicAdd((unsigned long long*)&a.dose_sum_fp[k], (unsigned long long)s_misc[3 + k]);
+    for (int k = 0; k < 3; ++k) {
+      add_u128((unsigned long long*)&a.dose_sum_fp[k], (unsigned long long*)&a.dose_sum_fp[3 + k],
+               (unsigned long long)s_misc[3 + k]);
+      if (s_carry[1 + k]) atomicAdd((unsigned long long*)&a.dose_sum_fp[3 + k], s_carry[1 + k]);
+    }
     atomicMin((long long*)&a.minmax_bg_bits[0], s_misc[6]);
     atomicMax((long long*)&a.minmax_bg_bits[1], s_misc[7]);
   }

@@ -336,7 +336,7 @@ def alloc_reduce_outputs(n: int, sz: dict, device, per_patient_metrics=False) ->
         tir_hist=empty((5, TIR_BINS + 1), i64, device), bg_hist_total=empty((N_BG_BINS,), i64, device),
         below_min=empty((N_THRESHOLDS,), i64, device), below_max=empty((N_THRESHOLDS,), i64, device),
         minmax_bg_bits=empty((2,), i64, device), timeline=empty((3, sz["n_grid"]), i64, device),
-        dose_hist=empty((3, 201), i64, device), dose_sum_fp=empty((3,), i64, device),
+        dose_hist=empty((3, 201), i64, device), dose_sum_fp=empty((6,), i64, device),
         worst=empty((4,), i64, device), metric_hist=empty((7, TIR_BINS + 1), i64, device),
         metrics={k: empty((n,), t.float32, device) for k in ("tir", "tbr70", "tbr54", "tar180", "tar250")}
         if per_patient_metrics else None,

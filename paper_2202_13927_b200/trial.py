@@ -224,7 +224,7 @@ class FastTrial:
         acc.max_bg = engine.ordered_bits_to_double(mm[1]) if acc.n_patients else -np.inf
         acc.timeline_sum_fp, acc.timeline_min_fp, acc.timeline_max_fp = (tl[0].copy(), tl[1].copy(), tl[2].copy())
         acc.dose_hist = {s: dh[k].astype(np.int64) for k, s in enumerate(DOSE_SIGNALS)}
-        acc.dose_sum_fp = [int(v) for v in dsum]
+        acc.dose_sum_fp = [(int(dsum[3 + k]) << 64) + (int(dsum[k]) & 0xFFFFFFFFFFFFFFFF) for k in range(3)]
         acc.metric_hist = mhist.astype(np.int64)
         if int(w[3]):
             i = int(w[2]) - self.pid0

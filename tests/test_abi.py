@@ -40,14 +40,14 @@ def test_exports_every_declared_symbol(lib):
 
 def test_abi_version(lib):
     lib.gt_abi_version.restype = C.c_int
-    assert lib.gt_abi_version() == 2
+    assert lib.gt_abi_version() == 3
 
 
 def test_struct_layouts_match_c():
     from paper_2202_13927_b200 import _lib
     structs = {"gt_parity_args": _lib.ParityArgs, "gt_fast_args": _lib.FastArgs,
                "gt_reduce_args": _lib.ReduceArgs, "gt_sampler_args": _lib.SamplerArgs,
-               "gt_meal_gen": _lib.MealGen}
+               "gt_meal_gen": _lib.MealGen, "gt_northern_args": _lib.NorthernArgs}
     lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', "int main(void){"]
     for cname, py in structs.items():
         lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
