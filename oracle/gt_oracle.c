@@ -297,10 +297,27 @@ static void init_tables(void)
 }
 
 /* ------------------------------------------------------------------------ */
+/* Hypoglycaemia events (BASELINE.json north_star output; the reference has no
+ * such statistic — it counts only ticks below 3 mmol/L, analytics.py:129-135).
+ * Definition used throughout the repo: an event is a
+ * maximal run of consecutive ticks whose BG is below 3.9 (resp. 3.0) mmol/L
+ * — the statistics' BG at each tick, _kernel.py:137 — lasting at least
+ * min_ticks = ceil(900 s / dt) ticks.  The run state carries across blocks.
+ * hypo = {run39, run30, events39, events30, min_ticks}. */
+static void hypo_update(int64_t *hypo, double bg)
+{
+    hypo[0] = bg < 3.9 ? hypo[0] + 1 : 0;
+    hypo[1] = bg < 3.0 ? hypo[1] + 1 : 0;
+    hypo[2] += hypo[0] == hypo[4];
+    hypo[3] += hypo[1] == hypo[4];
+}
+
+/* ------------------------------------------------------------------------ */
 /* _kernel.py:38-182  simulate_block (one patient, one block).
  * Arrays exactly as the reference: day_dose [n_days][3], trace [n][8] or NULL,
- * wiener [n][3] or NULL (has_noise = wiener != NULL), meas [n/period_steps]. */
-int oracle_simulate_block(
+ * wiener [n][3] or NULL (has_noise = wiener != NULL), meas [n/period_steps].
+ * hypo: optional hypoglycaemia-event state (hypo_update), NULL to skip. */
+static int simulate_block_hypo(
     double *x, double *c, const double *p, const double *hyper, double assumed_basal_uh,
     double t0_s, int64_t n_steps, double dt_s, int64_t period_steps, double period_s,
     const double *meals_start, const double *meals_end, const double *meals_rate,
@@ -309,7 +326,7 @@ int oracle_simulate_block(
     const double *ex_announced, int64_t n_ex,
     int64_t *ptrs, const double *wiener, const double *meas_norm,
     int64_t *tir_ticks, int64_t *bg_hist, double *scal, double *day_dose,
-    double *timeline, int64_t grid_step_ticks, int64_t global_tick0, double *trace)
+    double *timeline, int64_t grid_step_ticks, int64_t global_tick0, double *trace, int64_t *hypo)
 {
     init_tables();
     int has_noise = wiener != NULL;
@@ -376,6 +393,7 @@ int oracle_simulate_block(
         int64_t day = (int64_t)oracle_py_floordiv(t, 86400.0);
         day_dose[day * 3 + 0] += basal_uh;
         if (global_tick % grid_step_ticks == 0) timeline[global_tick / grid_step_ticks] = bg;
+        if (hypo) hypo_update(hypo, bg);
         if (trace) {
             double *tr = trace + i * 8;
             tr[0] = t; tr[1] = bg; tr[2] = scal[SCAL_LAST_Y]; tr[3] = d[0]; tr[4] = d[1];
@@ -399,6 +417,25 @@ int oracle_simulate_block(
     return 0;
 }
 
+/* the reference's signature (_kernel.py:38-49) */
+int oracle_simulate_block(
+    double *x, double *c, const double *p, const double *hyper, double assumed_basal_uh,
+    double t0_s, int64_t n_steps, double dt_s, int64_t period_steps, double period_s,
+    const double *meals_start, const double *meals_end, const double *meals_rate,
+    const double *meals_ann, int64_t n_meals,
+    const double *ex_start, const double *ex_end, const double *ex_hrr,
+    const double *ex_announced, int64_t n_ex,
+    int64_t *ptrs, const double *wiener, const double *meas_norm,
+    int64_t *tir_ticks, int64_t *bg_hist, double *scal, double *day_dose,
+    double *timeline, int64_t grid_step_ticks, int64_t global_tick0, double *trace)
+{
+    return simulate_block_hypo(x, c, p, hyper, assumed_basal_uh, t0_s, n_steps, dt_s, period_steps,
+                               period_s, meals_start, meals_end, meals_rate, meals_ann, n_meals,
+                               ex_start, ex_end, ex_hrr, ex_announced, n_ex, ptrs, wiener, meas_norm,
+                               tir_ticks, bg_hist, scal, day_dose, timeline, grid_step_ticks,
+                               global_tick0, trace, NULL);
+}
+
 /* ------------------------------------------------------------------------ */
 /* simulation.py:314-391  _simulate_arrays, fast-engine branch, with the
  * process/measurement noise injected as whole-horizon arrays (a one-shot
@@ -414,7 +451,7 @@ int oracle_simulate_patient(
     const double *ex_announced, int64_t n_ex,
     const double *wiener, const double *meas_norm,
     int64_t *tir_ticks, int64_t *bg_hist, double *scal, double *day_dose,
-    double *timeline, int64_t grid_step_ticks, double *trace, int64_t *ticks_out)
+    double *timeline, int64_t grid_step_ticks, double *trace, int64_t *ticks_out, int64_t *hypo)
 {
     int64_t ptrs[3] = {0, 0, 0};
     scal[0] = INFINITY; scal[1] = -INFINITY; scal[2] = 0.0; scal[3] = 0.0;
@@ -423,13 +460,13 @@ int oracle_simulate_patient(
     int status = 0;
     while (done < horizon_ticks) {
         int64_t n = horizon_ticks - done < block ? horizon_ticks - done : block;
-        status = oracle_simulate_block(
+        status = simulate_block_hypo(
             x, c, p, hyper, assumed_basal_uh, (double)done * dt_s, n, dt_s, period_steps, period_s,
             meals_start, meals_end, meals_rate, meals_ann, n_meals,
             ex_start, ex_end, ex_hrr, ex_announced, n_ex, ptrs,
             wiener ? wiener + done * 3 : NULL, meas_norm + done / period_steps,
             tir_ticks, bg_hist, scal, day_dose, timeline, grid_step_ticks, done,
-            trace ? trace + done * 8 : NULL);
+            trace ? trace + done * 8 : NULL, hypo);
         if (status != 0) break;
         done += n;
     }

@@ -36,7 +36,7 @@ int oracle_simulate_patient(
     const double *ex_announced, int64_t n_ex,
     const double *wiener, const double *meas_norm,
     int64_t *tir_ticks, int64_t *bg_hist, double *scal, double *day_dose,
-    double *timeline, int64_t grid_step_ticks, double *trace, int64_t *ticks_out);
+    double *timeline, int64_t grid_step_ticks, double *trace, int64_t *ticks_out, int64_t *hypo);
 
 /* ---------------------------------------------------------------- Philox */
 static void philox4x32_10(const uint32_t ctr_in[4], uint32_t k0, uint32_t k1, uint32_t out[4])
@@ -157,12 +157,13 @@ int oracle_run_batch_injected(
     const double *eh, const double *ea, const double *wiener, const uint8_t *has_noise,
     const double *meas, int32_t *status, int64_t *ticks, int64_t *tir_ticks,
     int64_t *bg_hist, double *scal, double *day_dose, double *timeline, double *x_out,
-    double *c_out, int nthreads)
+    double *c_out, int32_t *hypo_events, int64_t hypo_min_ticks, double *trace, int nthreads)
 {
     int64_t n_ctl = horizon_ticks / period_steps;
 #pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads > 0 ? nthreads : 1)
     for (int64_t i = 0; i < n; ++i) {
         double x[16], c[11];
+        int64_t hypo[5] = {0, 0, 0, 0, hypo_min_ticks};
         memcpy(x, x0 + i * 16, sizeof x);
         memcpy(c, c0 + i * 11, sizeof c);
         int64_t mo = meal_off[i], eo = ex_off[i];
@@ -172,7 +173,9 @@ int oracle_run_batch_injected(
             ee + eo, eh + eo, ea + eo, ex_off[i + 1] - eo,
             has_noise[i] ? wiener + i * horizon_ticks * 3 : NULL, meas + i * n_ctl,
             tir_ticks + i * 5, bg_hist + i * 247, scal + i * 4, day_dose + i * n_days * 3,
-            timeline + i * n_grid, grid_step_ticks, NULL, ticks + i);
+            timeline + i * n_grid, grid_step_ticks, trace ? trace + i * horizon_ticks * 8 : NULL,
+            ticks + i, hypo);
+        if (hypo_events) { hypo_events[i * 2] = (int32_t)hypo[2]; hypo_events[i * 2 + 1] = (int32_t)hypo[3]; }
         if (x_out) memcpy(x_out + i * 16, x, sizeof x);
         if (c_out) memcpy(c_out + i * 11, c, sizeof c);
     }
@@ -196,7 +199,7 @@ int oracle_run_batch_philox(
     const double *assumed_basal, int64_t horizon_ticks, double dt_s, int64_t period_steps,
     double period_s, int64_t grid_step_ticks, int64_t n_days, int64_t n_grid,
     int32_t *status, int64_t *ticks, int64_t *tir_ticks, int64_t *bg_hist, double *scal,
-    int nthreads)
+    int32_t *hypo_events, int64_t hypo_min_ticks, int nthreads)
 {
     int64_t n_ctl = horizon_ticks / period_steps;
     double horizon_s = (double)horizon_ticks * dt_s;
@@ -243,11 +246,13 @@ int oracle_run_batch_philox(
             memset(day_dose, 0, sizeof(double) * n_days * 3);
             for (int r = 0; r < 5; ++r) tir_ticks[i * 5 + r] = 0;
             for (int b = 0; b < 247; ++b) bg_hist[i * 247 + b] = 0;
+            int64_t hypo[5] = {0, 0, 0, 0, hypo_min_ticks};
             status[i] = oracle_simulate_patient(
                 x, c, params + i * 30, hyper, assumed_basal[i], horizon_ticks, dt_s,
                 period_steps, period_s, ms, me, mr, ma, nm, NULL, NULL, NULL, NULL, 0, wiener,
                 meas, tir_ticks + i * 5, bg_hist + i * 247, scal + i * 4, day_dose, timeline,
-                grid_step_ticks, NULL, ticks + i);
+                grid_step_ticks, NULL, ticks + i, hypo);
+            if (hypo_events) { hypo_events[i * 2] = (int32_t)hypo[2]; hypo_events[i * 2 + 1] = (int32_t)hypo[3]; }
         }
         free(wiener); free(meas); free(mbuf); free(day_dose); free(timeline);
     }

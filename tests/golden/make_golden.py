@@ -44,6 +44,9 @@ from glucotrial.storage import report_bytes  # noqa: E402
 
 from paper_2202_13927_b200.protocol import ThreeMealProtocol  # noqa: E402  (BASELINE generator plug-in)
 
+sys.path.insert(0, os.path.join(REPO, "oracle"))
+import oracle as _oracle  # noqa: E402  (numpy twin of the hypo-event count, applied to the reference's BG)
+
 DAY = 86400.0
 
 
@@ -155,7 +158,8 @@ def sim_fixture(name, entries, generator, cfg, trace_for=(0, 1), extra_params=No
     model = get_model("hovorka_ext")
     rec = {"ids": [], "params": [], "x0": [], "c0": [], "basal": [], "status": [], "ticks": [],
            "tir": [], "hist": [], "scal": [], "day_dose": [], "timeline": [], "meal_off": [0],
-           "ex_off": [0], "noise_sha": []}
+           "ex_off": [0], "noise_sha": [], "hypo": []}
+    hmin = _oracle.hypo_min_ticks(cfg.dt_s)
     meals, ex = [[], [], [], []], [[], [], [], []]
     traces = {}
     for j, (patient, pset) in enumerate(entries):
@@ -192,6 +196,7 @@ def sim_fixture(name, entries, generator, cfg, trace_for=(0, 1), extra_params=No
             rec["tir"].append(np.zeros(5, np.int64)); rec["hist"].append(np.zeros(247, np.int64))
             rec["scal"].append(np.zeros(3)); rec["day_dose"].append(np.zeros((cfg.n_days, 3)))
             rec["timeline"].append(np.zeros(cfg.n_grid))
+            rec["hypo"].append((0, 0))
             continue
         st = res.stats
         rec["status"].append(0 if res.status == "ok" else 1)
@@ -199,6 +204,8 @@ def sim_fixture(name, entries, generator, cfg, trace_for=(0, 1), extra_params=No
         rec["tir"].append(st.tir_ticks); rec["hist"].append(st.bg_hist)
         rec["scal"].append([st.min_bg, st.max_bg, st.sum_bg])
         rec["day_dose"].append(st.day_dose); rec["timeline"].append(st.timeline_bg)
+        # hypo events of the reference's own per-tick BG (trace column 1), up to the abort tick
+        rec["hypo"].append(_oracle.hypo_events(res.trace[:st.ticks, 1], hmin))
         if j in trace_for:
             traces[f"trace_{j}"] = res.trace
     arrays = {k: np.array(v) for k, v in rec.items()}
@@ -206,6 +213,8 @@ def sim_fixture(name, entries, generator, cfg, trace_for=(0, 1), extra_params=No
         arrays[nm] = np.concatenate(meals[k]) if meals[k] else np.zeros(0)
     for k, nm in enumerate(("ex_start", "ex_end", "ex_hrr", "ex_announced")):
         arrays[nm] = np.concatenate(ex[k]) if ex[k] else np.zeros(0)
+    arrays["hypo"] = arrays["hypo"].astype(np.int32).reshape(-1, 2)
+    arrays["hypo_min_ticks"] = np.array(hmin)
     arrays["hyper"] = prof.to_vec()
     arrays["config"] = np.array([cfg.horizon_s, cfg.seed, cfg.dt_s, cfg.controller_period_s,
                                  cfg.grid_step_s, cfg.initial_bg_mmol_per_l])
@@ -300,9 +309,34 @@ def pid_fixtures():
                 make_ctl=lambda basal: PIDController(prof, basal))
 
 
+def hypo_fixtures():
+    """Hypoglycaemia-rich closed loops (the bench's short fixtures have almost
+    no events): the controllers are told an assumed basal rate scaled up, as
+    run_trial's basal_scale does (simulation.py:502), so insulin is overdosed
+    and BG repeatedly crosses 3.9 and 3.0 mmol/L.  Event counts come from the
+    reference's own BG traces (sim_fixture)."""
+    from paper_2202_13927_b200.pid import PIDController, PIDProfile
+    prof = load_profile()
+    e0, _ = generate_population(seed=0, n=64)
+    e101, _ = generate_population(seed=101, n=12)
+    cfg_tm = SimulationConfig(horizon_s=7 * DAY, seed=0, dt_s=60.0)
+    sim_fixture("sim_hypo_threemeal_dt60.npz", e0[:16], ThreeMealProtocol(), cfg_tm, trace_for=(),
+                make_ctl=lambda basal: DualHormoneController(prof, 2.8 * basal))
+    cfg_ny = SimulationConfig(horizon_s=7 * DAY, seed=8, dt_s=30.0)
+    sim_fixture("sim_hypo_northern_dt30.npz", e101[:8], NorthernYearProtocol(), cfg_ny, trace_for=(),
+                make_ctl=lambda basal: DualHormoneController(prof, 2.4 * basal))
+    pp = PIDProfile()
+    cfg_pid = SimulationConfig(horizon_s=4 * DAY, seed=4, dt_s=60.0)
+    sim_fixture("sim_hypo_pid_threemeal_dt60.npz", e0[16:28], ThreeMealProtocol(), cfg_pid, trace_for=(),
+                prof=pp, make_ctl=lambda basal: PIDController(pp, 1.8 * basal))
+
+
 def main():
     if "--only-pid" in sys.argv:
         pid_fixtures()
+        return
+    if "--only-hypo" in sys.argv:
+        hypo_fixtures()
         return
     pop = population_fixture()
     flop_fixture()
@@ -335,6 +369,7 @@ def main():
     res = run_trial(e101[:4], nyp, "dual_hormone", load_profile(), "hovorka_ext", worst_cfg)
     _save("worst_trace.npz", trace=res.worst_trace, worst_id=np.array(res.accumulator.worst.patient_id))
     pid_fixtures()
+    hypo_fixtures()
     # one empty-protocol day, no noise: fixed point (test_simulation.py:133-144)
     with open(os.path.join(HERE, "versions.json"), "w") as fh:
         json.dump({"numpy": np.__version__, "scipy": scipy.__version__, "numba": numba.__version__,

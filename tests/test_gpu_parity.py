@@ -8,11 +8,12 @@ import pytest
 
 from conftest import golden, golden_bytes
 from helpers import SimCase
+import ties
 
 pytestmark = pytest.mark.gpu
 
 SIMS = ["sim_northern_dt30.npz", "sim_threemeal_dt60.npz", "sim_northern_dt37p5.npz",
-        "sim_northern_dt30_8d.npz", "sim_faults.npz"]
+        "sim_northern_dt30_8d.npz", "sim_faults.npz", "sim_hypo_threemeal_dt60.npz", "sim_hypo_northern_dt30.npz"]
 
 
 @pytest.fixture(scope="module")
@@ -81,7 +82,8 @@ def test_c1_parity_subset_1000_patients_4_weeks(dev, oracle, controller):
     seed-1 device population x 4 weeks at dt 60 s, the reference's own noise
     streams injected, 3-meal schedules.  The parity kernel equals the C oracle
     bit for bit on every output; the fused kernel agrees to relative 1e-9 with
-    identical histograms except documented threshold ties."""
+    identical histograms and hypo-event counts except for patients proven
+    threshold ties one by one (tests/ties.py)."""
     import torch
     from paper_2202_13927_b200 import engine, rng
     from paper_2202_13927_b200.config import SimulationConfig
@@ -97,7 +99,7 @@ def test_c1_parity_subset_1000_patients_4_weeks(dev, oracle, controller):
     gen = ThreeMealProtocol()
     pop = generate_population(1, 1000, device=dev, on_exhausted="redraw_weight")
     oracle.set_controller(code)
-    ties = 0
+    exc = []
     try:
         for lo in range(0, 1000, 250):
             hi = lo + 250
@@ -125,14 +127,95 @@ def test_c1_parity_subset_1000_patients_4_weeks(dev, oracle, controller):
             ft.simulate(injected={"wiener": engine.dev(W.reshape(-1), torch.float64, dev),
                                   "has_noise": engine.dev(hn, torch.uint8, dev),
                                   "meas": engine.dev(M.reshape(-1), torch.float64, dev)})
-            st, hist, tl = (t.cpu().numpy() for t in (ft.outs.bg_stats, ft.outs.bg_hist, ft.outs.timeline_pp))
-            for j in range(hi - lo):
-                close = (np.allclose(st[:, j], ref["scal"][j, :3], rtol=1e-9, atol=0)
-                         and np.allclose(tl[:, j], ref["timeline"][j], rtol=1e-9, atol=0))
-                ties += not (close and np.array_equal(hist[:, j], ref["bg_hist"][j]))
+            fused = {"scal": ft.outs.bg_stats.cpu().numpy().T, "hist": ft.outs.bg_hist.cpu().numpy().T,
+                     "timeline": ft.outs.timeline_pp.cpu().numpy().T,
+                     "day_dose": ft.outs.day_dose.cpu().numpy().transpose(2, 0, 1),
+                     "hypo": ft.outs.hypo_events.cpu().numpy().T}
+            refd = {"scal": ref["scal"], "hist": ref["bg_hist"], "timeline": ref["timeline"],
+                    "day_dose": ref["day_dose"], "hypo": ref["hypo_events"]}
+            exc += ties.check_patients(oracle, dev, hi - lo, refd, fused,
+                                       ties.inputs_from_arrays(params, x0, c0, ub, prof.to_vec(), moff, meals, eoff,
+                                                               ex, W, hn, M, code, sz, cfg.dt_s,
+                                                               cfg.controller_period_s, lo),
+                                       label=f"C1 {controller} [{lo}, {hi})")
+            oracle.set_controller(code)   # (check_patients restores controller 0)
     finally:
         oracle.set_controller(0)
-    assert ties <= 10, f"{ties} of 1000 patients differ beyond rounding (threshold ties)"
+    print(f"C1 {controller}: {len(exc)} proven threshold ties of 1000 patients")
+
+
+@pytest.mark.parametrize("controller", ["dual_hormone", "pid_pump"])
+def test_c1_parity_subset_northern_year(dev, oracle, controller):
+    """The reference's own configuration at BASELINE configs[1] scale: the
+    first 1 000 patients of the seed-1 device population x 4 weeks at dt 60 s
+    on the NorthernYear protocol (weight-scaled meals, announced exercise;
+    simulation.py:420-453), the schedule planned ON THE DEVICE for the fused
+    kernel (gt_northern.cu) and built on the host for the oracle, the
+    reference's own noise streams injected.  The parity kernel equals the
+    oracle bit for bit on every output; the fused kernel agrees to 1e-9 with
+    identical histograms and hypo events except proven threshold ties."""
+    import torch
+    from paper_2202_13927_b200 import engine, rng
+    from paper_2202_13927_b200.config import SimulationConfig
+    from paper_2202_13927_b200.controller import ControllerHyperparameters
+    from paper_2202_13927_b200.northern import NorthernYearProtocol
+    from paper_2202_13927_b200.pid import PIDProfile
+    from paper_2202_13927_b200.population import generate_population
+    from paper_2202_13927_b200.protocol import compile_protocol
+    from paper_2202_13927_b200.simulation import _csr
+    from paper_2202_13927_b200.trial import FastTrial
+    cfg = SimulationConfig(horizon_s=28 * 86400.0, seed=1, dt_s=60.0)
+    prof = PIDProfile() if controller == "pid_pump" else ControllerHyperparameters()
+    code = 1 if controller == "pid_pump" else 0
+    gen = NorthernYearProtocol()
+    assert gen.on_device()
+    pop = generate_population(1, 1000, device=dev, on_exhausted="redraw_weight")
+    exc, n_ex_sessions, n_hypo = [], 0, 0
+    for lo in range(0, 1000, 250):
+        hi = lo + 250
+        ft = FastTrial(lo, pop.params_device[lo:hi].contiguous(), pop.basal_device[lo:hi].contiguous(), gen,
+                       prof, cfg, controller_id=controller, device=dev)
+        sz = ft.sz
+        H, ps = sz["horizon_ticks"], sz["period_steps"]
+        params, x0, c0, ub = (t.cpu().numpy() for t in (ft.params, ft.x0, ft.c0, ft.basal))
+        pas = [compile_protocol(gen.build(cfg.seed, type("P", (), {"id": lo + i, "body_weight_kg": params[i, 0]})()),
+                                cfg.horizon_s) for i in range(hi - lo)]
+        moff, meals, eoff, ex = _csr(pas)
+        n_ex_sessions += int(eoff[-1])
+        W = np.zeros((hi - lo, H, 3)); M = np.zeros((hi - lo, H // ps))
+        for i in range(hi - lo):
+            W[i], M[i] = rng.reference_noise(cfg.seed, lo + i, H, ps, True, True)
+        hn = np.ones(hi - lo, np.uint8)
+        b = engine.ParityBatch(params, x0, c0, prof.to_vec(), ub, moff, meals, eoff, ex, W, hn, M, controller=code)
+        out = engine.run_parity(b, sz, cfg.dt_s, cfg.controller_period_s, device=dev)
+        oracle.set_controller(code)
+        try:
+            ref = oracle.run_batch_injected(params, x0, c0, prof.to_vec(), ub, sz, cfg.dt_s, cfg.controller_period_s,
+                                            moff, meals, eoff, ex, W, hn, M)
+        finally:
+            oracle.set_controller(0)
+        for k in ("status", "ticks", "tir_ticks", "bg_hist", "scal", "day_dose", "timeline", "x_out", "c_out"):
+            assert np.array_equal(out[k], ref[k]), k
+        assert np.all(ref["status"] == 0)
+        n_hypo += int(ref["hypo_events"].sum())
+        ft.outs = engine.alloc_fast_outputs(hi - lo, lo, sz, dev, per_patient_timeline=True)
+        ft.simulate(injected={"wiener": engine.dev(W.reshape(-1), torch.float64, dev),
+                              "has_noise": engine.dev(hn, torch.uint8, dev),
+                              "meas": engine.dev(M.reshape(-1), torch.float64, dev)})
+        fused = {"scal": ft.outs.bg_stats.cpu().numpy().T, "hist": ft.outs.bg_hist.cpu().numpy().T,
+                 "timeline": ft.outs.timeline_pp.cpu().numpy().T,
+                 "day_dose": ft.outs.day_dose.cpu().numpy().transpose(2, 0, 1),
+                 "hypo": ft.outs.hypo_events.cpu().numpy().T}
+        refd = {"scal": ref["scal"], "hist": ref["bg_hist"], "timeline": ref["timeline"], "day_dose": ref["day_dose"],
+                "hypo": ref["hypo_events"]}
+        assert np.array_equal(ft.outs.status.cpu().numpy(), ref["status"])
+        exc += ties.check_patients(oracle, dev, hi - lo, refd, fused,
+                                   ties.inputs_from_arrays(params, x0, c0, ub, prof.to_vec(), moff, meals, eoff, ex,
+                                                           W, hn, M, code, sz, cfg.dt_s, cfg.controller_period_s, lo),
+                                   label=f"C1 NorthernYear {controller} [{lo}, {hi})")
+    assert n_ex_sessions >= 1000 * 6     # announced exercise: 76 sessions a year, ~8 in 4 weeks
+    print(f"C1 NorthernYear {controller}: {len(exc)} proven threshold ties of 1000 patients; "
+          f"{n_ex_sessions} exercise sessions, {n_hypo} hypo events (<3.9) in the reference run")
 
 
 def test_simulate_closed_loop_api(dev):
