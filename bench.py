@@ -15,6 +15,10 @@ own 100k-patient shard (global patient ids rank*n ...), exact accumulators
 are combined with NCCL all-reduce (sum/min/max) — the only collective.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+With --gpus N > 1 and no torchrun environment, bench.py re-launches itself
+under ``python -m torch.distributed.run --nproc-per-node N`` (127.0.0.1
+rendezvous), one rank per GPU; rank 0 prints the one JSON line.
 """
 
 from __future__ import annotations
@@ -75,6 +79,37 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
+
+
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(args, argv) -> int | None:
+    """--gpus N > 1 outside torchrun: re-launch this script as N ranks (one
+    process per GPU) and return their exit status; None when no spawn is
+    needed (already a rank, or N = 1).  NCCL's INFO log (communicator set-up,
+    transports) goes to per-rank files so stdout keeps the one JSON line."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    if not args.dry_run and args.impl == "ours":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            raise SystemExit(f"bench.py --gpus {args.gpus}: only {have} CUDA device(s) visible")
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT,COLL")
+    env.setdefault("NCCL_DEBUG_FILE", os.path.join(REPO, "gpurun_out" if os.path.isdir(os.path.join(REPO, "gpurun_out"))
+                                                   else "/tmp", "nccl_bench.%h.%p.log"))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + list(argv)
+    return subprocess.run(cmd, env=env).returncode
 
 
 class ClockSampler:
@@ -397,7 +432,7 @@ def run_trial1m(args):
         dist.init_process_group("nccl", device_id=device)
     from paper_2202_13927_b200 import analytics
     from paper_2202_13927_b200.config import SimulationConfig
-    from paper_2202_13927_b200.parallel import allreduce_accumulator, shard_range
+    from paper_2202_13927_b200.parallel import allreduce_accumulator, gather_per_patient, shard_range
     from paper_2202_13927_b200.population import generate_population
     from paper_2202_13927_b200.protocol import ThreeMealProtocol
     from paper_2202_13927_b200.trial import FastTrial
@@ -418,6 +453,10 @@ def run_trial1m(args):
         acc = ft.accumulator()
         if ws > 1:
             acc = allreduce_accumulator(acc, device)
+            # the per-patient metric arrays, gathered over NCCL in global-id order
+            metrics = gather_per_patient(ft.metrics_device(), lo, n_total, device)
+        else:
+            metrics = ft.metrics()
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
         if ws > 1:
@@ -429,16 +468,69 @@ def run_trial1m(args):
         del ft, pop
     if rank == 0:
         w = float(np.median(walls))
+        ok = metrics["status"] == 0
+        assert metrics["tir"].shape[0] == n_total and int(ok.sum()) == acc.n_patients
+        # exact per-patient quantiles of the gathered arrays next to the
+        # histogram (0.5 % bin) quantiles of the accumulator
+        exact = {k: {str(q): float(np.quantile(metrics[k][ok].astype(np.float64), q, method="inverted_cdf"))
+                     for q in (0.05, 0.25, 0.5, 0.75, 0.95)}
+                 for k in ("tir", "tbr70", "tbr54", "tar180", "tar250", "hypo_events_lt70", "hypo_events_lt54")}
         print(json.dumps({
             "metric": "1M-patient x 52-week trial wall-clock", "value": w, "unit": "s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": False, "scaling": "strong",
             "patient_weeks_per_s": n_total * weeks / w, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"BASELINE configs[2]: {n_total} patients x {weeks} weeks, seed 2, dt 60 s",
                        "controller": ctl_label, "protocol": "three_meal",
-                       "timed": "sampler + staging + fused kernel + reduction + NCCL combine (host wall, max over ranks)"},
-            "quantiles": analytics.metric_quantiles(acc)}), flush=True)
+                       "timed": "sampler + staging + fused kernel + reduction + NCCL all-reduce of the exact "
+                                "accumulators + NCCL all-gather of the per-patient metric arrays (host wall, "
+                                "max over ranks)"},
+            "gathered_patients": int(metrics["tir"].shape[0]),
+            "quantiles": analytics.metric_quantiles(acc), "quantiles_exact_per_patient": exact}), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
+    return 0
+
+
+def run_dry(args):
+    """--dry-run: the multi-rank plumbing without a GPU (gloo): the spawn, the
+    per-rank shard ids, barrier-bracketed timing with the max over ranks and
+    the whole-job aggregation of the JSON line.  The per-rank 'step' is a
+    fixed host wait, so the value is NOT a measurement (tests only)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2202_13927_b200.parallel import shard_range
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("gloo")
+    n = args.patients
+    lo, hi = rank * n, (rank + 1) * n
+    for _ in range(args.warmup):
+        time.sleep(0.002)
+    if ws > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        time.sleep(0.005)
+    ms = 1000.0 * (time.perf_counter() - t0)
+    ids = torch.tensor([lo, hi], dtype=torch.int64)
+    parts = [torch.zeros(2, dtype=torch.int64) for _ in range(ws)]
+    if ws > 1:
+        dist.barrier()
+        t = torch.tensor([ms])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.all_gather(parts, ids)
+    else:
+        parts = [ids]
+    if rank == 0:
+        shards = [tuple(int(v) for v in p) for p in parts]
+        print(json.dumps({"metric": METRIC + " (dry run: no GPU work)", "value": n * WEEKS * ws / (ms / args.steps / 1000.0),
+                          "unit": "patient-weeks/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": ms / args.steps, "dry_run": True, "scaling": "weak",
+                          "shards": shards, "trial1m_shards": [shard_range(1_000_000, r, ws) for r in range(ws)]}),
+              flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
     return 0
 
 
@@ -453,7 +545,15 @@ def main():
     ap.add_argument("--controller", default="pid_pump", choices=["pid_pump", "dual_hormone"])
     ap.add_argument("--workload", default="c1", choices=["c1", "trial1m"],
                     help="c1: BASELINE configs[1] throughput (default); trial1m: the 1M x 52 w trial wall-clock")
-    args = ap.parse_args()
+    ap.add_argument("--dry-run", action="store_true",
+                    help="multi-rank plumbing check on CPU (gloo, no GPU work; tests only)")
+    argv = sys.argv[1:]
+    args = ap.parse_args(argv)
+    rc = spawn_ranks(args, argv)
+    if rc is not None:
+        return rc
+    if args.dry_run:
+        return run_dry(args)
     if args.workload == "trial1m" and args.impl == "ours":
         return run_trial1m(args)
     if args.impl == "reference":

@@ -98,7 +98,8 @@ def gather_per_patient(arrays: dict, lo: int, n_total: int, device=None, group=N
     contiguous slice starting at global id ``lo``) into global-id order.
     Shards differ in size by at most one patient, so every rank pads to the
     largest shard (one collective per array, NCCL all-gather over NVLink on
-    GPUs, gloo on CPU)."""
+    GPUs, gloo on CPU).  Device tensors stay on the device (no host round
+    trip before the collective); the result is numpy."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
@@ -107,13 +108,15 @@ def gather_per_patient(arrays: dict, lo: int, n_total: int, device=None, group=N
     width = max(hi - l for l, hi in sizes)
     out = {}
     for k in sorted(arrays):
-        a = np.ascontiguousarray(arrays[k])
-        buf = np.zeros((width,) + a.shape[1:], dtype=a.dtype)
-        buf[: a.shape[0]] = a
-        t = torch.as_tensor(buf, device=dev)
+        a = arrays[k]
+        if not isinstance(a, torch.Tensor):
+            a = torch.as_tensor(np.ascontiguousarray(a))
+        a = a.to(dev)
+        t = torch.zeros((width,) + tuple(a.shape[1:]), dtype=a.dtype, device=dev)
+        t[: a.shape[0]] = a
         parts = [torch.empty_like(t) for _ in range(world)]
         dist.all_gather(parts, t, group=group)
-        out[k] = np.concatenate([p.cpu().numpy()[: hi - l] for p, (l, hi) in zip(parts, sizes)])
+        out[k] = torch.cat([p[: hi - l] for p, (l, hi) in zip(parts, sizes)]).cpu().numpy()
     return out
 
 

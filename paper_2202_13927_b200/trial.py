@@ -239,6 +239,16 @@ class FastTrial:
                                   ticks=int(wticks[0]), tir_ticks=tir, bg_hist=hist)
         return acc
 
+    def metrics_device(self) -> dict | None:
+        """Per-patient metric arrays as device tensors (shard order): the five
+        range fractions, the two hypo-event counts and the status."""
+        if self.red.metrics is None:
+            return None
+        out = dict(self.red.metrics)
+        out["hypo_events_lt70"], out["hypo_events_lt54"] = self.outs.hypo_events[0], self.outs.hypo_events[1]
+        out["status"] = self.outs.status
+        return out
+
     def metrics(self) -> dict | None:
         if self.red.metrics is None:
             return None

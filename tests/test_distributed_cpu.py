@@ -110,3 +110,30 @@ def test_gather_per_patient_world3():
         assert p.exitcode == 0
     for _, tir, st in res:
         assert tir == [i * 0.5 for i in range(11)] and st == [i % 3 for i in range(11)]
+
+
+def _bench_line(*extra):
+    import json
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(repo, "bench.py"), "--dry-run", "--steps", "4", "--warmup", "1",
+                          *extra], capture_output=True, text=True, timeout=300, env=env, cwd=repo)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout       # rank 0 alone prints
+    return json.loads(lines[0])
+
+
+def test_bench_spawns_ranks_for_gpus_n():
+    """bench.py --gpus 2 outside torchrun re-launches itself as 2 ranks
+    (torch.distributed.run, 127.0.0.1 rendezvous); the plumbing runs on CPU
+    with gloo under --dry-run: one JSON line, n_gpus 2, global-id shards
+    tiling the population, whole-job value (2 shards over the max rank time)."""
+    one = _bench_line()
+    two = _bench_line("--gpus", "2")
+    assert one["n_gpus"] == 1 and two["n_gpus"] == 2
+    assert two["shards"] == [[0, 100000], [100000, 200000]]
+    assert two["trial1m_shards"] == [[0, 500000], [500000, 1000000]]
+    assert two["value"] > 1.5 * one["value"]

@@ -213,7 +213,7 @@ def test_c1_parity_subset_northern_year(dev, oracle, controller):
                                    ties.inputs_from_arrays(params, x0, c0, ub, prof.to_vec(), moff, meals, eoff, ex,
                                                            W, hn, M, code, sz, cfg.dt_s, cfg.controller_period_s, lo),
                                    label=f"C1 NorthernYear {controller} [{lo}, {hi})")
-    assert n_ex_sessions >= 1000 * 6     # announced exercise: 76 sessions a year, ~8 in 4 weeks
+    assert n_ex_sessions >= 1000 * 4     # announced exercise: 76 sessions a year, ~5.5 in 4 weeks
     print(f"C1 NorthernYear {controller}: {len(exc)} proven threshold ties of 1000 patients; "
           f"{n_ex_sessions} exercise sessions, {n_hypo} hypo events (<3.9) in the reference run")
 

@@ -6,7 +6,8 @@
       this subset is tests/test_gpu_parity.py::test_c1_parity_subset_...).
   C2  1 000 000 x 52 w, seed 2, on one GPU: device sampler, fused
       integrator, device reduction, histograms and 5/25/50/75/95 %
-      quantiles.  On N GPUs each rank runs 1/N of the ids (bench.py --gpus).
+      quantiles.  On N GPUs each rank runs 1/N of the ids
+      (bench.py --workload trial1m --gpus N spawns the N ranks).
   C3  4 controller arms x 250 000 shared patients x 12 w under common random
       numbers; paired differences (studies.treatment_comparison).
   C4  precision / step study, 250 000 x 12 w (studies.precision_study).
