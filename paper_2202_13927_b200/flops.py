@@ -23,6 +23,31 @@ PID_CONTROLLER_TYPICAL = 22
 PID_TICK = PID_CONTROLLER_TYPICAL + 2 + 7 + 1   # 32
 
 
+# Structurally-zero work, counted (not hand-typed) by a known-value float over
+# the reference's drift_vec (tests/golden/flop_counts.json, make_golden.py
+# _structural_counts): an op whose result a known 0 / 1 operand fixes is
+# trivial.  A workload without exercise sessions (the 3-meal generator) keeps
+# E1..E3 = 0 and HRR = 0 for the whole horizon; the pid_pump controller never
+# doses glucagon, so Z1 = Z2 = 0 and u[2] = 0.  The fused kernel compiles those
+# terms out (gt_fast.cu: HAS_EX, CTRL == GT_CTRL_PID_PUMP), so the roofline
+# also reports the fraction on the work that remains ("nontrivial").
+DRIFT_NOEX, DRIFT_NOGLUC, DRIFT_NOEX_NOGLUC = 54, 60, 46
+ZERO_STATES_NOEX, ZERO_STATES_NOGLUC, ZERO_STATES_NOEX_NOGLUC = 3, 2, 5
+TICK_TRIVIAL_NOGLUC = 1      # glucagon_ug / (period / 60) with glucagon 0 (_kernel.py:129)
+
+
+def flops_per_step_nontrivial(period_steps: int, controller: str = "dual_hormone",
+                              exercise: bool = False) -> float:
+    """flops_per_step minus the structurally-zero terms of the workload."""
+    gluc = controller != "pid_pump"
+    drift, zs = {(True, True): (DRIFT_TYPICAL, 0), (False, True): (DRIFT_NOEX, ZERO_STATES_NOEX),
+                 (True, False): (DRIFT_NOGLUC, ZERO_STATES_NOGLUC),
+                 (False, False): (DRIFT_NOEX_NOGLUC, ZERO_STATES_NOEX_NOGLUC)}[(bool(exercise), gluc)]
+    step = STEP_OTHER + drift - 2 * zs
+    tick = TICK if gluc else PID_TICK - TICK_TRIVIAL_NOGLUC
+    return step + tick / period_steps
+
+
 def flops_per_step(period_steps: int, controller: str = "dual_hormone") -> float:
     return STEP + (PID_TICK if controller == "pid_pump" else TICK) / period_steps
 

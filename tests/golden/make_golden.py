@@ -248,6 +248,84 @@ class _CF(float):
         return _CF(-float(self))
 
 
+class _KF(float):
+    """Float that tracks STRUCTURAL zeros / ones (k = 0.0 / 1.0 / None): an
+    op whose result is fixed by a known operand (x + 0, x * 1, x * 0, 0 / x,
+    0 - 0 ...) is trivial -- the fused kernel compiles it out -- every other
+    +, -, *, / is counted.  Used to count the algorithmic work that remains
+    when a workload structurally has no exercise (E = 0, HRR = 0) or no
+    glucagon (Z = 0, u[2] = 0)."""
+    n = 0
+
+    def __new__(cls, v, k=None):
+        o = float.__new__(cls, v)
+        o.k = k
+        return o
+
+    @staticmethod
+    def _k(o):
+        if isinstance(o, _KF):
+            return o.k
+        return float(o) if float(o) in (0.0, 1.0) else None   # literal constants of the source
+
+    def _op(op):
+        def f(self, o):
+            a, b = (self, o) if not op.startswith("__r") else (o, self)
+            ka, kb = _KF._k(a), _KF._k(b)
+            name = op.replace("__r", "__", 1) if op.startswith("__r") else op
+            v = getattr(float, name)(float(a), float(b))
+            k = None
+            trivial = False
+            if name == "__add__":
+                if ka == 0.0 or kb == 0.0:
+                    trivial, k = True, (kb if ka == 0.0 else ka)
+            elif name == "__sub__":
+                if kb == 0.0:
+                    trivial, k = True, ka
+                elif ka == 0.0 and kb is not None:
+                    trivial, k = True, -kb
+            elif name == "__mul__":
+                if ka == 0.0 or kb == 0.0:
+                    trivial, k = True, 0.0
+                elif ka == 1.0 or kb == 1.0:
+                    trivial, k = True, (kb if ka == 1.0 else ka)
+            elif name == "__truediv__":
+                if ka == 0.0:
+                    trivial, k = True, 0.0
+            if not trivial:
+                _KF.n += 1
+            return _KF(v, k)
+        return f
+    __add__, __radd__ = _op("__add__"), _op("__radd__")
+    __sub__, __rsub__ = _op("__sub__"), _op("__rsub__")
+    __mul__, __rmul__ = _op("__mul__"), _op("__rmul__")
+    __truediv__, __rtruediv__ = _op("__truediv__"), _op("__rtruediv__")
+
+    def __neg__(self):
+        return _KF(-float(self), None if self.k is None else -self.k)
+
+
+def _structural_counts(p, x):
+    """Non-trivial drift ops and structurally-zero derivatives with exercise
+    and/or glucagon absent (typical branch state x)."""
+    from glucotrial.hovorka import IE1, IE2, IE3, IZ1, IZ2
+    res = {}
+    for label, zero_x, zero_u, zero_d in (("noex", (IE1, IE2, IE3), (), (1,)),
+                                          ("nogluc", (IZ1, IZ2), (2,), ()),
+                                          ("noex_nogluc", (IE1, IE2, IE3, IZ1, IZ2), (2,), (1,))):
+        xx = np.array([_KF(0.0, 0.0) if k in zero_x else _KF(v) for k, v in enumerate(x)], dtype=object)
+        uu = np.array([_KF(0.0, 0.0) if k in zero_u else _KF(v) for k, v in enumerate([10.0, 0.0, 0.0])],
+                      dtype=object)
+        dd = np.array([_KF(0.0, 0.0) if k in zero_d else _KF(v) for k, v in enumerate([0.0, 0.0])], dtype=object)
+        out = np.empty(16, dtype=object)
+        _KF.n = 0
+        hovorka.drift_vec.py_func(_KF(0.0), xx, uu, dd, np.array([_KF(v) for v in p], dtype=object), out)
+        res[f"drift_typical_{label}"] = _KF.n
+        # Euler updates x += f * dt (2 ops) vanish for states held at a known 0
+        res[f"zero_states_{label}"] = sum(1 for k in range(16) if _KF._k(out[k]) == 0.0 and k in zero_x)
+    return res
+
+
 def flop_fixture():
     """Op counts of drift_vec / diffusion_diag / controller_step_vec over the
     reference's own Python source (.py_func), on golden-like states."""
@@ -283,6 +361,7 @@ def flop_fixture():
     vals, cnt = np.unique(ctrl_counts, return_counts=True)
     counts["controller_typical"] = int(vals[np.argmax(cnt)])
     counts["controller_min"], counts["controller_max"] = int(min(ctrl_counts)), int(max(ctrl_counts))
+    counts.update(_structural_counts(p, x))
     with open(os.path.join(HERE, "flop_counts.json"), "w") as fh:
         json.dump(counts, fh, indent=1, sort_keys=True)
 
@@ -337,6 +416,9 @@ def main():
         return
     if "--only-hypo" in sys.argv:
         hypo_fixtures()
+        return
+    if "--only-flops" in sys.argv:
+        flop_fixture()
         return
     pop = population_fixture()
     flop_fixture()

@@ -16,6 +16,22 @@ def test_flop_constants_pinned_to_reference_counts():
     assert abs(flops.flops_per_patient_week(60.0, 5) - 1.2499e6) < 1e3
 
 
+def test_structural_zero_counts_pinned():
+    """The work left when exercise / glucagon are structurally absent, counted
+    by the known-value float over the reference's drift_vec (make_golden.py)."""
+    c = json.loads(golden_bytes("flop_counts.json"))
+    assert c["drift_typical_noex"] == flops.DRIFT_NOEX
+    assert c["drift_typical_nogluc"] == flops.DRIFT_NOGLUC
+    assert c["drift_typical_noex_nogluc"] == flops.DRIFT_NOEX_NOGLUC
+    assert c["zero_states_noex"] == flops.ZERO_STATES_NOEX
+    assert c["zero_states_nogluc"] == flops.ZERO_STATES_NOGLUC
+    assert c["zero_states_noex_nogluc"] == flops.ZERO_STATES_NOEX_NOGLUC
+    # bench workload: 3-meal generator (no exercise) + pid_pump (no glucagon)
+    assert flops.flops_per_step_nontrivial(5, "pid_pump", exercise=False) == 119 - 23 - 10 + 31 / 5
+    assert flops.flops_per_step_nontrivial(5, "dual_hormone", exercise=True) == flops.flops_per_step(5)
+    assert flops.flops_per_step_nontrivial(5, "dual_hormone", exercise=False) == 119 - 15 - 6 + 25 / 5
+
+
 def test_pid_controller_op_count():
     """PID_CONTROLLER_TYPICAL = FP64 +,-,*,/ of pid_step_vec on its typical
     branch (no meal bolus), counted with an op-counting float."""

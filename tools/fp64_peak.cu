@@ -36,10 +36,35 @@ double run(const char* name, int blocks, int threads, int iters) {
   cudaFree(out);
   return tf;
 }
+// back-to-back launches for ~seconds: the sustained figure (a kernel timed
+// inside a long step runs at the sustained clock)
+template <typename T>
+double sustained(const char* name, int blocks, int threads, int iters, double seconds) {
+  T* out; cudaMalloc(&out, sizeof(T) * blocks * threads);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  fma_loop<T><<<blocks, threads>>>(out, iters, (T)0.999999, (T)1e-7);
+  cudaEventRecord(e0);
+  fma_loop<T><<<blocks, threads>>>(out, iters, (T)0.999999, (T)1e-7);
+  cudaEventRecord(e1); cudaEventSynchronize(e1);
+  float ms1; cudaEventElapsedTime(&ms1, e0, e1);
+  const int reps = (int)(seconds * 1e3 / ms1) + 1;
+  cudaEventRecord(e0);
+  for (int r = 0; r < reps; ++r) fma_loop<T><<<blocks, threads>>>(out, iters, (T)0.999999, (T)1e-7);
+  cudaEventRecord(e1); cudaEventSynchronize(e1);
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  double flops = 2.0 * NCHAIN * (double)iters * blocks * threads * reps;
+  double tf = flops / (ms * 1e-3) / 1e12;
+  printf("{\"kernel\": \"%s_sustained\", \"blocks\": %d, \"threads\": %d, \"reps\": %d, \"ms\": %.3f, \"tflops\": %.3f}\n",
+         name, blocks, threads, reps, ms, tf);
+  cudaFree(out);
+  return tf;
+}
 int main() {
   int sms = 0; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   int clk = 0; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
   printf("{\"sms\": %d, \"clock_khz\": %d}\n", sms, clk);
+  sustained<double>("dfma", sms * 8, 256, 20000, 4.0);
+  sustained<float>("ffma", sms * 8, 256, 40000, 4.0);
   for (int occ = 1; occ <= 8; occ *= 2) run<double>("dfma", sms * occ, 256, 20000);
   run<double>("dfma", sms * 16, 256, 10000);
   for (int occ = 1; occ <= 8; occ *= 2) run<float>("ffma", sms * occ, 256, 40000);

@@ -57,6 +57,40 @@ if traffic["duration_ns"] is not None:
     traffic["duration_ns"] *= {"ns": 1, "usecond": 1e3, "us": 1e3, "msecond": 1e6, "ms": 1e6, "s": 1e9}.get(u, 1)
 json.dump(traffic, open(f"{prefix}_traffic.json", "w"), indent=1)
 
+# pipe utilisation: the counters north_star asks for (FP64 / FP32 pipes, plus
+# the SFU = XU pipe) and the issue rate that bounds an issue-limited kernel
+PIPES = [
+    ("fp64_pipe_cycles_active_pct", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+    ("fp64_inst_executed_pct", "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
+    ("fma_pipe_cycles_active_pct", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+    ("fmaheavy_pipe_cycles_active_pct", "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+    ("fma_inst_executed_pct", "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
+    ("alu_pipe_cycles_active_pct", "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+    ("xu_sfu_inst_executed_pct", "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
+    ("lsu_inst_executed_pct", "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"),
+    ("issue_active_pct", "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+    ("ipc_per_sm", "sm__inst_executed.avg.per_cycle_active"),
+    ("warps_active_pct", "sm__warps_active.avg.pct_of_peak_sustained_active"),
+    ("dram_throughput_pct", "dram__throughput.avg.pct_of_peak_sustained_elapsed"),
+]
+
+
+def _num(name):
+    try:
+        return get(name)
+    except ValueError:
+        return None
+
+
+pipes = {"kernel": kernel, "workload": label, "source": f"ncu --set full ({prefix}_ncu.txt)"}
+for key, name in PIPES:
+    pipes[key] = _num(name)
+json.dump(pipes, open(f"{prefix}_pipes.json", "w"), indent=1)
+lines.insert(3, "\n[pipe utilisation]")
+for i, (key, name) in enumerate(PIPES):
+    val = pipes[key]
+    lines.insert(4 + i, f"  {key:<34s} {'n/a' if val is None else f'{val:.2f}'}   ({name})")
+
 src = list(csv.reader(io.StringIO(ncu("--page", "source", "--csv", "--print-source", "sass"))))
 sh = src[1]
 iS, iE = sh.index("Source"), sh.index("Instructions Executed")
@@ -89,4 +123,4 @@ for c, k in sorted(stalls, reverse=True):
     if c > 0:
         lines.append(f"  {k:<28s} {100 * c / tot_s:5.1f} %")
 open(f"{prefix}_ncu.txt", "w").write("\n".join(lines) + "\n")
-print(f"wrote {prefix}_ncu.txt, {prefix}_traffic.json; {tot / warp_steps if warp_steps else tot:.1f}")
+print(f"wrote {prefix}_ncu.txt, {prefix}_traffic.json, {prefix}_pipes.json; {tot / warp_steps if warp_steps else tot:.1f}")
