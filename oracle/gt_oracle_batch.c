@@ -258,3 +258,103 @@ int oracle_run_batch_philox(
     }
     return 0;
 }
+
+/* ------------------------------------------------------------ sampler twin */
+/* Bitwise host twin of the device population sampler (csrc/gt_sampler.cu),
+ * which restates population.py:148-173 (_positive_normal body weight) and
+ * population.py:207-259 (sample_parameter_set: nonnegative values, normal
+ * draws within 1 SD, a steady state at the target BG, u_basal >= 0.4 U/h)
+ * with its own counter-based streams: Philox4x32-10 keyed by the trial seed,
+ * counter (attempt, pid, role 0x12, pair) for the sampled values and
+ * (draw, pid, role 0x13, 0) for the weight; normals by Acklam's inverse CDF of
+ * a 52-bit uniform, lognormals by the deterministic exp below.  The draws are
+ * counter-addressed, so the order in which an attempt's values are evaluated
+ * cannot change them. */
+double oracle_det_exp(double x)
+{
+    if (x > 709.0) return INFINITY;
+    if (x < -745.0) return 0.0;
+    double kf = floor(x * 1.44269504088896338700e+00 + 0.5);
+    double r = (x - kf * 6.93147180369123816490e-01) - kf * 1.90821492927058770002e-10;
+    double s = 1.0;
+    for (int j = 14; j >= 1; --j) s = 1.0 + (r * s) / (double)j;
+    return ldexp(s, (int)kf);
+}
+
+int oracle_steady_state(const double *p, double target_bg, double *x, double *u_basal_uh);
+
+static double u52(uint32_t a, uint32_t b)
+{
+    uint64_t k = ((uint64_t)(a >> 6) << 26) | (uint64_t)(b >> 6);
+    return ((double)(2 * k + 1)) * 1.1102230246251565404e-16;
+}
+
+typedef struct {
+    int32_t n_sampled;
+    int32_t param_index[16];
+    int32_t kind[16];        /* 0 normal(a = mean, b = sd), 1 lognormal(a = mu, b = sigma) */
+    double a[16], b[16];
+    double fixed_params[30];
+    double weight_mean, weight_sd, target_bg, min_basal_uh;
+    int32_t max_attempts, max_weight_redraws;
+} oracle_sampler_spec;
+
+int oracle_sample_patients(const oracle_sampler_spec *sp, uint64_t seed, int64_t pid0, int64_t n,
+                           double *params, double *x0, double *ub_out, int32_t *attempts_out,
+                           int32_t *status_out, int64_t *reject_counts, int nthreads)
+{
+    const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+    int64_t rc0 = 0, rc1 = 0, rc2 = 0, rc3 = 0;
+#pragma omp parallel for schedule(dynamic, 16) num_threads(nthreads > 0 ? nthreads : 1) reduction(+:rc0, rc1, rc2, rc3)
+    for (int64_t i = 0; i < n; ++i) {
+        const uint32_t pid = (uint32_t)(pid0 + i);
+        double p[30], x[16] = {0}, ub = 0.0;
+        memcpy(p, sp->fixed_params, sizeof p);
+        int status = 1;
+        int32_t attempt = 0, total = 0;
+        uint32_t wctr = 0;
+        for (int wdraw = 0; wdraw <= sp->max_weight_redraws && status != 0; ++wdraw) {
+            double w = 0.0;
+            for (int t = 0; t < sp->max_attempts; ++t, ++wctr) {
+                uint32_t ctr[4] = {wctr, pid, 0x13u, 0u}, r[4];
+                philox4x32_10(ctr, k0, k1, r);
+                double v = sp->weight_mean + sp->weight_sd * oracle_inv_norm(u52(r[0], r[1]));
+                if (v > 0.0) { w = v; ++wctr; break; }
+            }
+            p[0] = w;
+            for (attempt = 0; attempt < sp->max_attempts && w > 0.0; ++attempt) {
+                const uint32_t actr = (uint32_t)(total + attempt);
+                double vals[16];
+                for (int q = 0; q < sp->n_sampled; q += 2) {
+                    uint32_t ctr[4] = {actr, pid, 0x12u, (uint32_t)(q >> 1)}, r[4];
+                    philox4x32_10(ctr, k0, k1, r);
+                    double z[2] = {oracle_inv_norm(u52(r[0], r[1])), oracle_inv_norm(u52(r[2], r[3]))};
+                    for (int h = 0; h < 2 && q + h < sp->n_sampled; ++h) {
+                        int j = q + h;
+                        vals[j] = sp->kind[j] == 0 ? sp->a[j] + sp->b[j] * z[h]
+                                                   : oracle_det_exp(sp->a[j] + sp->b[j] * z[h]);
+                    }
+                }
+                int neg = 0, outside = 0;
+                for (int j = 0; j < sp->n_sampled; ++j) neg |= vals[j] < 0.0;
+                if (neg) { ++rc0; continue; }
+                for (int j = 0; j < sp->n_sampled; ++j)
+                    if (sp->kind[j] == 0 && fabs(vals[j] - sp->a[j]) > sp->b[j]) { outside = 1; break; }
+                if (outside) { ++rc1; continue; }
+                for (int j = 0; j < sp->n_sampled; ++j) p[sp->param_index[j]] = vals[j];
+                if (oracle_steady_state(p, sp->target_bg, x, &ub) != 0) { ++rc2; continue; }
+                if (ub < sp->min_basal_uh) { ++rc3; continue; }
+                status = 0;
+                break;
+            }
+            total += status == 0 ? attempt + 1 : attempt;
+        }
+        memcpy(params + i * 30, p, sizeof p);
+        for (int k = 0; k < 16; ++k) x0[i * 16 + k] = status == 0 ? x[k] : 0.0;
+        ub_out[i] = status == 0 ? ub : 0.0;
+        attempts_out[i] = total;
+        status_out[i] = status;
+    }
+    reject_counts[0] = rc0; reject_counts[1] = rc1; reject_counts[2] = rc2; reject_counts[3] = rc3;
+    return 0;
+}

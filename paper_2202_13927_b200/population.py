@@ -55,12 +55,23 @@ class SamplingStats:
 class DevicePopulation:
     """A device-resident population shard (ids pid0 .. pid0+n-1)."""
 
-    def __init__(self, pid0, params_device, basal_device, x0_device, stats: SamplingStats):
+    def __init__(self, pid0, params_device, basal_device, x0_device, stats: SamplingStats,
+                 attempts_device=None, max_attempts: int = tables.MAX_ATTEMPTS):
         self.pid0 = int(pid0)
         self.params_device = params_device
         self.basal_device = basal_device
         self.x0_device = x0_device
         self.stats = stats
+        self.attempts_device = attempts_device   # per patient, redraw rounds included
+        self.max_attempts = int(max_attempts)
+
+    @property
+    def n_weight_redraws(self) -> int:
+        """Patients whose body weight was redrawn (each redraw follows a whole
+        exhausted attempt budget; on_exhausted="redraw_weight")."""
+        if self.attempts_device is None:
+            return 0
+        return int((self.attempts_device >= self.max_attempts).sum().item())
 
     def __len__(self):
         return int(self.params_device.shape[0])
@@ -104,7 +115,7 @@ def generate_population(seed: int, n: int, table=None, target_bg: float = 6.0, p
     st = SamplingStats(attempts=attempts, accepted=n, rejected_negative=int(rc[0]),
                        rejected_outside_sd=int(rc[1]), rejected_no_steady_state=int(rc[2]),
                        rejected_basal=int(rc[3]))
-    return DevicePopulation(pid0, out["params"], out["u_basal"], out["x0"], st)
+    return DevicePopulation(pid0, out["params"], out["u_basal"], out["x0"], st, out["attempts"], max_attempts)
 
 
 def validate_parameter_sets(params, u_basal, table=None, target_bg: float = 6.0, device=None) -> list:

@@ -68,6 +68,25 @@ def population_fixture():
     return out
 
 
+def population_4000_fixture():
+    """A large reference population for distribution parity of the device
+    sampler: generate_population(seed=7, n=4000) (population.py:303-341).
+    Seeds 5 and 6 raise PopulationError at this size (a body weight below
+    ~30 kg admits no parameter set); seed 7 succeeds.  Stored:
+    body weights, the 14 sampled parameters (table order), u_basal and the
+    SamplingStats counters."""
+    from glucotrial.population import load_parameter_table
+    entries, stats = generate_population(seed=7, n=4000, workers=os.cpu_count() or 1)
+    table = load_parameter_table()
+    names = list(table.sampled)
+    _save("population_s7_n4000.npz",
+          weights=np.array([p.body_weight_kg for p, _ in entries]),
+          sampled=np.array([[ps.values[k] for k in names] for _, ps in entries]),
+          names=np.array(names), ubasal=np.array([ps.u_basal_u_per_h for _, ps in entries]),
+          stats=np.array([stats.attempts, stats.accepted, stats.rejected_negative, stats.rejected_outside_sd,
+                          stats.rejected_basal, stats.rejected_no_steady_state]))
+
+
 def steady_fixture(pop):
     params = pop["s0_params"].copy()
     x0 = np.zeros((params.shape[0], 16))
@@ -417,10 +436,14 @@ def main():
     if "--only-hypo" in sys.argv:
         hypo_fixtures()
         return
+    if "--only-pop4k" in sys.argv:
+        population_4000_fixture()
+        return
     if "--only-flops" in sys.argv:
         flop_fixture()
         return
     pop = population_fixture()
+    population_4000_fixture()
     flop_fixture()
     steady_fixture(pop)
     drift_fixture(pop)

@@ -269,34 +269,6 @@ def test_diverged_rerun_under_sliced_schedule(dev, controller):
             assert torch.equal(getattr(ft.outs, k)[..., keep], getattr(ft0.outs, k)[..., keep]), k
 
 
-def test_population_sampler_rules_and_distribution(dev, oracle):
-    from paper_2202_13927_b200.population import generate_population
-    from paper_2202_13927_b200.tables import default_parameter_table
-    from paper_2202_13927_b200.layout import PARAM_INDEX
-    table = default_parameter_table()
-    pop = generate_population(0, 4000, device=dev)
-    P = pop.params_device.cpu().numpy()
-    ub = pop.basal_device.cpu().numpy()
-    assert np.all(P >= 0) and np.all(ub >= 0.4)
-    for name, spec in table.sampled.items():
-        if spec.kind == "normal":
-            assert np.all(np.abs(P[:, PARAM_INDEX[name]] - spec.mean) <= spec.sd)
-    for i in range(0, 4000, 97):
-        x, u = oracle.steady_state(P[i])
-        assert u == ub[i] and np.array_equal(x, pop.x0_device[i].cpu().numpy())
-    # same distribution as the reference sampler's (golden population, seed 0, n 64):
-    ref = golden("population.npz")["s0_params"]
-    for name in ("EGP0", "SIT", "VG", "tmaxI"):
-        k = PARAM_INDEX[name]
-        a, b = P[:, k], ref[:, k]
-        assert abs(a.mean() - b.mean()) < 4 * b.std() / np.sqrt(b.size)
-    acc_rate = pop.stats.accepted / pop.stats.attempts
-    assert 0.02 < acc_rate < 0.06     # reference: 3.7 %
-    # prefix stability (population.py:10-13)
-    pop2 = generate_population(0, 100, device=dev)
-    assert np.array_equal(pop2.params_device.cpu().numpy(), P[:100])
-
-
 def test_philox_trial_statistics_match_oracle(dev, oracle):
     """Independent noise streams (device FP32 Box-Muller vs the oracle's
     double Box-Muller) -> population TIR statistics agree within Monte Carlo

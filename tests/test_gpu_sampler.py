@@ -1,0 +1,53 @@
+"""GPU tests of the population sampler (csrc/gt_sampler.cu): bit for bit
+equal to the oracle's C twin, and distributed like the reference's own
+generate_population (population.py:217-259; golden seed-7 n-4000 draw)."""
+
+import numpy as np
+import pytest
+
+import sampler_checks
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev():
+    import torch
+    from paper_2202_13927_b200 import _lib
+    assert torch.cuda.is_available()
+    _lib.load()
+    return torch.device("cuda", 0)
+
+
+@pytest.mark.parametrize("seed,pid0,n", [(1, 0, 3000), (7, 123_456, 2000), (2**40 + 9, 0, 777)])
+def test_device_sampler_bitwise_vs_oracle_twin(dev, oracle, seed, pid0, n):
+    from paper_2202_13927_b200 import engine
+    from paper_2202_13927_b200.layout import PARAM_INDEX, PARAM_NAMES
+    from paper_2202_13927_b200.tables import default_parameter_table
+    table = default_parameter_table()
+    d = engine.sample_population(seed, n, table, pid0=pid0, device=dev, max_weight_redraws=16)
+    o = oracle.sample_patients(table, seed, pid0, n, PARAM_INDEX, PARAM_NAMES, max_weight_redraws=16)
+    for k in ("params", "x0", "u_basal", "attempts", "status", "reject_counts"):
+        assert np.array_equal(d[k].cpu().numpy(), o[k]), k
+
+
+def test_device_sampler_distribution_matches_reference(dev):
+    from paper_2202_13927_b200.population import generate_population
+    pop = generate_population(2, 4000, device=dev, on_exhausted="redraw_weight")
+    assert pop.n_weight_redraws == 0
+    rc = (pop.stats.rejected_negative, pop.stats.rejected_outside_sd, pop.stats.rejected_no_steady_state,
+          pop.stats.rejected_basal)
+    rep, z = sampler_checks.check_against_reference(pop.params_device.cpu().numpy(), pop.basal_device.cpu().numpy(),
+                                                     pop.stats.attempts, rc)
+    print({k: round(v, 4) for k, v in rep.items()}, {k: round(float(v), 2) for k, v in z.items()})
+
+
+@pytest.mark.parametrize("n", [100_000, 1_000_000])
+def test_weight_redraw_counts_at_scale(dev, n):
+    """How many patients redraw_weight touches: about
+    1.7e-4 of the population (a body weight below ~30 kg)."""
+    from paper_2202_13927_b200.population import generate_population
+    pop = generate_population(1, n, device=dev, on_exhausted="redraw_weight")
+    r = pop.n_weight_redraws
+    print(f"n = {n}: {r} patients with a redrawn body weight ({r / n:.2e})")
+    assert 0 < r < 5e-4 * n
