@@ -2,15 +2,14 @@
 // Each thread runs NCHAIN independent FMA chains; total flops = 2 * fmas.
 #include <cstdio>
 #include <cuda_runtime.h>
-#define NCHAIN 16
+#define NCHAIN 8
 template <typename T>
 __global__ void fma_loop(T* out, int iters, T a, T b) {
   T v[NCHAIN];
 #pragma unroll
   for (int c = 0; c < NCHAIN; ++c) v[c] = (T)(threadIdx.x + c);
-  // unrolled x4: 4 * NCHAIN independent FMAs per loop trip, so the loop's
-  // counter / branch instructions take a negligible share of the issue slots
-#pragma unroll 4
+  // (NCHAIN 16 with the loop unrolled x4 measured lower: 33.6 vs 34.1 TFLOP/s,
+  // profiles/fp64_peak_r02_nchain16_unroll4.jsonl)
   for (int i = 0; i < iters; ++i) {
 #pragma unroll
     for (int c = 0; c < NCHAIN; ++c) v[c] = v[c] * a + b;
