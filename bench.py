@@ -415,7 +415,7 @@ def run_ours(args):
                                "controller period 300 s, seed 1",
                    "patients_per_gpu": n, "weeks": WEEKS, "dt_s": DT_S, "seed": SEED,
                    "controller": ctl_label,
-                   "protocol": "three_meal N(50/70/80,10) g, U(+-30 min)", "noise": "philox4x32-10",
+                   "protocol": "three_meal N(50/70/80,10) g, U(+-30 min)", "noise": "philox4x32-7 (fixed key, counter (pid, tick, seed))",
                    "parallelism": f"patients sharded over {ws} GPU(s), NCCL all-reduce of exact accumulators",
                    "l2": "flushed (256 MB write) between timed iterations"},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

@@ -58,7 +58,7 @@ extern "C" {
 
 /* noise sources */
 #define GT_NOISE_INJECTED 0 /* reference streams drawn on the host (rng.py:26-39) */
-#define GT_NOISE_PHILOX 1   /* on-device counter-based Philox4x32-10: fixed key
+#define GT_NOISE_PHILOX 1   /* on-device counter-based Philox4x32-7: fixed key
                                (0xA4093822, 0x299F31D0), counter (pid, tick,
                                seed_lo, seed_hi ^ role << 24); 4 FP32 Box-Muller
                                normals per tick (3 Wiener, 1 CGM) */

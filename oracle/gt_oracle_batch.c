@@ -6,7 +6,7 @@
  *     (the reference's own streams, drawn by numpy on the host), used by the
  *     parity tests at sizes the oracle finishes in seconds;
  *   - oracle_run_batch_philox: the bench workload (BASELINE configs[0..1]:
- *     3-meal generator + on-the-fly Philox4x32-10 noise) for the CPU
+ *     3-meal generator + on-the-fly Philox4x32-7 noise) for the CPU
  *     baseline / `bench.py --impl reference` arm.  Noise and meals are
  *     generated per patient into thread-local buffers exactly as the
  *     reference generates its noise blocks per patient (simulation.py:350-357),
@@ -39,10 +39,10 @@ int oracle_simulate_patient(
     double *timeline, int64_t grid_step_ticks, double *trace, int64_t *ticks_out, int64_t *hypo);
 
 /* ---------------------------------------------------------------- Philox */
-static void philox4x32_10(const uint32_t ctr_in[4], uint32_t k0, uint32_t k1, uint32_t out[4])
+static void philox4x32_r(const uint32_t ctr_in[4], uint32_t k0, uint32_t k1, uint32_t out[4], int rounds)
 {
     uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
-    for (int r = 0; r < 10; ++r) {
+    for (int r = 0; r < rounds; ++r) {
         if (r > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
         uint64_t p0 = (uint64_t)0xD2511F53u * c0;
         uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
@@ -53,9 +53,20 @@ static void philox4x32_10(const uint32_t ctr_in[4], uint32_t k0, uint32_t k1, ui
     out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
 }
 
+static void philox4x32_10(const uint32_t ctr_in[4], uint32_t k0, uint32_t k1, uint32_t out[4])
+{
+    philox4x32_r(ctr_in, k0, k1, out, 10);
+}
+
 void oracle_philox(const uint32_t *ctr, uint32_t k0, uint32_t k1, uint32_t *out)
 {
     philox4x32_10(ctr, k0, k1, out);
+}
+
+/* Philox4x32 with R rounds (the fused kernel's noise stream uses R = 7). */
+void oracle_philox_rounds(const uint32_t *ctr, uint32_t k0, uint32_t k1, uint32_t *out, int rounds)
+{
+    philox4x32_r(ctr, k0, k1, out, rounds);
 }
 
 /* Deterministic natural log from IEEE +,-,*,/ only (reproducible bit-for-bit
@@ -214,7 +225,7 @@ int oracle_run_batch_philox(
 #pragma omp for schedule(dynamic, 1)
         for (int64_t i = 0; i < n; ++i) {
             uint32_t pid = (uint32_t)(pid0 + i);
-            /* noise: one Philox call per tick -> 4 normals: 3 Wiener + 1 sensor
+            /* noise: one Philox4x32-7 call per tick -> 4 normals: 3 Wiener + 1 sensor
                (the sensor one is used on controller ticks only).  The device
                layout (csrc/gt_fast.cu philox_fast / philox_lane): fixed key,
                counter (pid, tick, seed_lo, seed_hi ^ role << 24). */
@@ -223,7 +234,7 @@ int oracle_run_batch_philox(
                 uint32_t ctr[4] = {pid, (uint32_t)k, (uint32_t)seed,
                                    (uint32_t)(seed >> 32) ^ (noise_role << 24)};
                 uint32_t r[4];
-                philox4x32_10(ctr, 0xA4093822u, 0x299F31D0u, r);
+                philox4x32_r(ctr, 0xA4093822u, 0x299F31D0u, r, 7);  /* the device noise stream: 7 rounds */
                 double z0, z1, z2, z3;
                 bm_pair(r[0], r[1], &z0, &z1);
                 bm_pair(r[2], r[3], &z2, &z3);

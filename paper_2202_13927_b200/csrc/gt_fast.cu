@@ -59,6 +59,26 @@ namespace gt {
 #ifndef GT_NOISE_PIPE
 #define GT_NOISE_PIPE 1  // draw tick k + 1's normals during step k
 #endif
+#ifndef GT_PS5
+// instances whose 5-step controller period (dt 60 s, 300 s period) runs fully
+// unrolled, a bit per (protocol, controller): 1 three_meal/pid_pump,
+// 2 three_meal/dual_hormone, 4 csr/pid_pump, 8 csr/dual_hormone.  Measured
+// (tools/ab_kernel.py, 100k x 4 w): the unrolled period is faster only for
+// csr/pid_pump (-8 %); it spills more and is slower (+2.5 to +7 %) elsewhere.
+#define GT_PS5 4
+#endif
+#ifndef GT_NOISE_ROUNDS
+// Philox4x32 rounds of the integrator's noise stream.  7 is the smallest round
+// count Salmon et al. (SC'11, Table 2) found Crush-resistant for Philox4x32
+// (BigCrush passes); 10 is their default "safety margin".  The noise role only
+// needs statistical parity (the parity path injects the reference's streams),
+// and 7 rounds measured 6-13 % faster per launch (profiles/r02_ab_noise_rounds.json).
+// The sampler and meal streams keep Philox4x32-10 (gt_common.cuh).
+#define GT_NOISE_ROUNDS 7
+#endif
+#ifndef GT_DEAD_SINK
+#define GT_DEAD_SINK 1  // dead lanes count into the padding bin 247
+#endif
 #ifndef GT_FAST_MINB
 #define GT_FAST_MINB 4  // resident 128-thread blocks per SM (register budget 128)
 #endif
@@ -166,7 +186,7 @@ __device__ __forceinline__ void mulwide(uint32_t a, uint32_t b, uint32_t& lo, ui
   asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(p));
 }
 
-// Noise stream: Philox4x32-10 under a FIXED key, so the 20 round keys are
+// Noise stream: Philox4x32-7 under a FIXED key, so the round keys are
 // compile-time immediates of the LOP3s (no uniform registers, no constant
 // loads); the trial seed enters the counter instead:
 //   counter = (pid, index, seed_lo, seed_hi ^ role << 24)
@@ -175,7 +195,7 @@ __device__ __forceinline__ void mulwide(uint32_t a, uint32_t b, uint32_t& lo, ui
 constexpr uint32_t kNoiseKey0 = 0xA4093822u, kNoiseKey1 = 0x299F31D0u;  // digits of pi
 __device__ __forceinline__ U4 philox_fast(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3) {
 #pragma unroll
-  for (int r = 0; r < 10; ++r) {
+  for (int r = 0; r < GT_NOISE_ROUNDS; ++r) {
     uint32_t lo0, hi0, lo1, hi1;
     mulwide(c0, 0xD2511F53u, lo0, hi0);
     mulwide(c2, 0xCD9E8D57u, lo1, hi1);
@@ -186,7 +206,7 @@ __device__ __forceinline__ U4 philox_fast(uint32_t c0, uint32_t c1, uint32_t c2,
   return U4{c0, c1, c2, c3};
 }
 
-// The integrator's draws: Philox4x32-10 with the counter (pid, index, seed_lo,
+// The integrator's draws: Philox4x32-7 with the counter (pid, index, seed_lo,
 // seed_hi ^ role << 24).  With the index in word 1 (xored, never multiplied in
 // round 1), rounds 1-3 reduce to 2 multiplies and 4 xors per draw given four
 // per-patient words (NoiseLane) and one launch word (Uni::nz_a):
@@ -195,7 +215,7 @@ __device__ __forceinline__ U4 philox_fast(uint32_t c0, uint32_t c1, uint32_t c2,
 //            C = hi(B*M1) ^ lo(s2*M1) ^ K0(1), D = lo(pid*M0) ^ K1(1)
 //   round 3: (hi1 ^ E, lo1, lo0 ^ F, lo(C*M0))  (lo1, hi1) = (hi0 ^ D) * M1,
 //            E = lo(B*M1) ^ K0(2), F = hi(C*M0) ^ K1(2)
-// then rounds 4-10 as usual: the same outputs as philox_fast(pid, index, s2, s3).
+// then rounds 4-7 as usual: the same outputs as philox_fast(pid, index, s2, s3).
 struct NoiseLane { uint32_t d, e, f, loc; };
 __device__ __forceinline__ uint32_t noise_k0(int r) { return kNoiseKey0 + (uint32_t)r * 0x9E3779B9u; }
 __device__ __forceinline__ uint32_t noise_k1(int r) { return kNoiseKey1 + (uint32_t)r * 0xBB67AE85u; }
@@ -217,7 +237,7 @@ __device__ __forceinline__ U4 philox_lane(uint32_t index, const NoiseLane& L, ui
   mulwide(hi0 ^ L.d, 0xCD9E8D57u, lo1, hi1);         // round 3, word 2 product
   uint32_t c0 = hi1 ^ L.e, c1 = lo1, c2 = lo0 ^ L.f, c3 = L.loc;
 #pragma unroll
-  for (int r = 3; r < 10; ++r) {
+  for (int r = 3; r < GT_NOISE_ROUNDS; ++r) {
     uint32_t a0, b0, a1, b1;
     mulwide(c0, 0xD2511F53u, a0, b0);
     mulwide(c2, 0xCD9E8D57u, a1, b1);
@@ -340,7 +360,7 @@ enum { SV_MKS, SV_MKE, SV_KBMIN, SV_KBMAX, SV_RUN39, SV_RUN30, SV_EV39,
        SV_EV30, SV_ALIVE, SV_STATUS, SV_DEATH, SV_MK0, SV_SI0 = SV_MK0 + 9, SV_H0 = SV_SI0 + N_SI,
        SV_N = SV_H0 + kHistWords };  // SV_H0: the packed uint8 histogram counters
 
-template <int PROTO, int NOISE, typename R, bool AGG, bool TRACE, int CTRL>
+template <int PROTO, int NOISE, typename R, bool AGG, bool TRACE, int CTRL, int PSC>
 __global__ void __launch_bounds__(kFastBS, GT_FAST_MINB)
 fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
   constexpr bool HAS_EX = (PROTO == GT_PROTO_CSR);
@@ -379,7 +399,10 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
   // stays in one register instead of being rebuilt every step
   uint32_t hist_lane;
   asm("mov.b32 %0, %1;" : "=r"(hist_lane) : "r"((uint32_t)__cvta_generic_to_shared(s_hist) + 4u * tid));
-  const int ps = u.ps;
+  // PSC > 0: the controller period's step count is a compile-time constant and
+  // the period's plain steps are unrolled (no loop control, no register
+  // rotation of the loop-carried noise / states)
+  const int ps = PSC > 0 ? PSC : u.ps;
   const int cpd = u.ctl_per_day;
 
   for (;;) {
@@ -992,7 +1015,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           kb = min(max(kb, 0), GT_N_THRESHOLDS);
           kb += (s_thr[kb + 1] <= bb) - (s_thr[kb] > bb);
         }
-        kb = alive ? kb : GT_N_BG_BINS;  // dead lanes count into the padding bin 247
+        if (GT_DEAD_SINK) kb = alive ? kb : GT_N_BG_BINS;  // dead lanes count into the padding bin 247
         {  // byte ((kb >> 2) * kFastBS + tid) * 4 + (kb & 3)
           GT_CHECK(kb >= 0 && kb <= GT_N_BG_BINS, "histogram bin");
           const uint32_t ha = hist_lane + (uint32_t)(kb & ~3) * (uint32_t)kFastBS + (uint32_t)(kb & 3);
@@ -1048,7 +1071,12 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       if (!GT_DAY_VOTE && __all_sync(0xffffffffu, !alive)) break;
       const int32_t kb0 = ctl * ps;
       step(kb0, true, ctl, 0);
-      for (int s = 1; s < ps; ++s) step(kb0 + s, false, ctl, s);
+      if (PSC > 0) {
+#pragma unroll
+        for (int s = 1; s < PSC; ++s) step(kb0 + s, false, ctl, s);
+      } else {
+        for (int s = 1; s < ps; ++s) step(kb0 + s, false, ctl, s);
+      }
     }
     // an all-dead warp stops early: its remaining timeline partials are identities
     for (; next_grid_ctl < ctl_hi; next_grid_ctl += u.grid_ctl, ++g_idx)
@@ -1201,10 +1229,14 @@ static int choose_chunks(int64_t warps, int64_t slots, int n_ctl) {
   return c_min;
 }
 
-template <int PROTO, int NOISE, typename R, bool AGG, bool TRACE, int CTRL>
+template <int PROTO, int NOISE, typename R, bool AGG, bool TRACE, int CTRL, int PSC = 0>
 static int launch_sched(const gt_fast_args* a, const gt::Uni& u, cudaStream_t st) {
+  constexpr int kBit = (PROTO == GT_PROTO_CSR ? 4 : 1) << (CTRL == GT_CTRL_PID_PUMP ? 0 : 1);
+  constexpr bool kPs5 = (GT_PS5 & kBit) != 0 && !TRACE && !AGG;
+  if (PSC == 0 && kPs5 && a->period_steps == 5)
+    return launch_sched<PROTO, NOISE, R, AGG, TRACE, CTRL, kPs5 ? 5 : 0>(a, u, st);
   constexpr int kDyn = gt::kHistWords * gt::kFastBS * 4;
-  auto kern = gt::fast_kernel<PROTO, NOISE, R, AGG, TRACE, CTRL>;
+  auto kern = gt::fast_kernel<PROTO, NOISE, R, AGG, TRACE, CTRL, PSC>;
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   // the > 48 KB dynamic shared-memory opt-in is a per-device attribute: set
@@ -1275,7 +1307,7 @@ static int launch_one(const gt_fast_args* a, const gt::Uni& u, cudaStream_t st) 
 
 // The fused kernel's noise stream, materialised: out[(i * n_ticks + j) * 4 + l]
 // = normal l of tick k0 + j of patient pid0 + i, drawn exactly as the kernel
-// draws it (philox_lane + FP32 SFU Box-Muller; lanes 0-2 = Wiener, 3 = CGM).
+// draws it (philox_lane: Philox4x32-7, + FP32 SFU Box-Muller; lanes 0-2 = Wiener, 3 = CGM).
 namespace gt {
 __global__ void noise_normals_kernel(int64_t n, int64_t pid0, int64_t k0, int64_t n_ticks, const Uni u,
                                      float* out) {

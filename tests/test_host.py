@@ -161,8 +161,9 @@ def test_philox_lane_form_equals_plain_rounds(oracle):
     """The fused kernel's per-patient Philox form (csrc/gt_fast.cu noise_lane /
     philox_lane: rounds 1-3 folded into four per-patient words and one launch
     word, the counter index in word 1) restated here gives the plain
-    Philox4x32-10 outputs of counter (pid, index, s2, s3) under the fixed noise
-    key, checked against the KAT-pinned oracle."""
+    Philox4x32-R outputs of counter (pid, index, s2, s3) under the fixed noise
+    key, checked against the oracle's R-round Philox (whose R = 10 is
+    KAT-pinned above); the kernel's noise stream uses R = 7."""
     M0, M1, K0, K1, W0, W1, m = 0xD2511F53, 0xCD9E8D57, 0xA4093822, 0x299F31D0, 0x9E3779B9, 0xBB67AE85, 0xFFFFFFFF
 
     def mw(a, b):
@@ -184,22 +185,23 @@ def test_philox_lane_form_equals_plain_rounds(oracle):
         loc, hic = mw(c, M0)
         return lo0p ^ k1(1), lob ^ k0(2), hic ^ k1(2), loc
 
-    def philox_lane(index, L, nz_a):
+    def philox_lane(index, L, nz_a, rounds):
         lo0, hi0 = mw(index ^ nz_a, M0)
         lo1, hi1 = mw(hi0 ^ L[0], M1)
         c0, c1, c2, c3 = hi1 ^ L[1], lo1, lo0 ^ L[2], L[3]
-        for r in range(3, 10):
+        for r in range(3, rounds):
             a0, b0 = mw(c0, M0)
             a1, b1 = mw(c2, M1)
             c0, c1, c2, c3 = b1 ^ c1 ^ k0(r), a1, b0 ^ c3 ^ k1(r), a0
         return c0, c1, c2, c3
 
     g = np.random.default_rng(7)
-    for pid, index, s2, s3 in g.integers(0, 2 ** 32, size=(300, 4), dtype=np.uint64).tolist():
-        nz_a = mw(s2, M1)[1] ^ K0
-        got = philox_lane(index, lane(pid, s2, s3), nz_a)
-        want = oracle.philox(np.array([pid, index, s2, s3], np.uint32), K0 | (K1 << 32))
-        assert got == tuple(int(v) for v in want)
+    for rounds in (7, 10):
+        for pid, index, s2, s3 in g.integers(0, 2 ** 32, size=(300, 4), dtype=np.uint64).tolist():
+            nz_a = mw(s2, M1)[1] ^ K0
+            got = philox_lane(index, lane(pid, s2, s3), nz_a, rounds)
+            want = oracle.philox(np.array([pid, index, s2, s3], np.uint32), K0 | (K1 << 32), rounds)
+            assert got == tuple(int(v) for v in want)
 
 
 # ----------------------------------------------------------- tick compilation
