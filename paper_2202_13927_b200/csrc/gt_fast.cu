@@ -79,6 +79,12 @@ namespace gt {
 #ifndef GT_DEAD_SINK
 #define GT_DEAD_SINK 1  // dead lanes count into the padding bin 247
 #endif
+#ifndef GT_FKEY
+#define GT_FKEY 1   // extremes / hypo-run branch keyed on FP32 bounds of the extremes (not bins)
+#endif
+#ifndef GT_KLOOP
+#define GT_KLOOP 1  // plain-step loop over the tick index itself
+#endif
 #ifndef GT_FAST_MINB
 #define GT_FAST_MINB 4  // resident 128-thread blocks per SM (register budget 128)
 #endif
@@ -475,6 +481,13 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
     int ann_rel = 0xFFFF;  // THREE_MEAL: period (from the day start) of the day's next announcement
     uint32_t act_len = 0;  // THREE_MEAL: meal input on for steps act_lo <= s < act_lo + act_len of this period
     int kb_min, kb_max, run39, run30, ev39, ev30, trig_lo;
+    // GT_FKEY: FP32 round-toward-zero keys of the extremes so far and of the
+    // low trigger.  rz is monotone, so bg < min_bg implies rz(bg) <= f_mn, bg >
+    // max_bg implies rz(bg) >= f_mx and bg < 3.9 implies rz(bg) <= rz(3.9):
+    // the branch is entered on a superset of the ticks that can change an
+    // extreme or a hypo run, and decides exactly inside.
+    float f_mn, f_mx, f_lo;
+    constexpr uint32_t kF39Bits = 0x40799999u;   // rz(3.9) as FP32
     double tr_rate = 0.0, tr_y = 0.0, tr_basal = 0.0;  // TRACE only (held trace columns)
     bool alive;
     int status, death_tick;
@@ -503,6 +516,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       sdl[(SC_DGLUC) * kFastBS] = 0.0;
       bg_sum = 0.0; day_basal = 0.0; hu_ins = 0; hu2 = 0;
       kb_min = INT_MAX; kb_max = -1; run39 = run30 = ev39 = ev30 = 0;
+      f_mn = INFINITY; f_mx = -INFINITY;
       m_ks = m_ke = INT_MAX; gin = 0;
       if (PROTO == GT_PROTO_CSR) {
         const MealT m0 = meal_at(0);
@@ -549,6 +563,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         ann_rel = j < 3 ? (int)s_mk[2][j][tid] : 0xFFFF;
       }
       kb_min = LDI(SV_KBMIN); kb_max = LDI(SV_KBMAX); run39 = LDI(SV_RUN39); run30 = LDI(SV_RUN30);
+      f_mn = __int_as_float(kb_min); f_mx = __int_as_float(kb_max);   // (GT_FKEY: the slots hold the keys)
       ev39 = LDI(SV_EV39); ev30 = LDI(SV_EV30); alive = LDI(SV_ALIVE) != 0;
       status = LDI(SV_STATUS); death_tick = LDI(SV_DEATH);
 #undef LDD
@@ -567,6 +582,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
 
     // extremes / hypo-run bookkeeping is needed only for a bin <= trig_lo or >= kb_max
     trig_lo = run39 > 0 ? INT_MAX : max(kb_min, 34);  // 34: bg < 3.9 (THRESHOLDS[34])
+    f_lo = run39 > 0 ? INFINITY : fmaxf(f_mn, __int_as_float(kF39Bits));
 
     // THREE_MEAL day window: the day's 3 meals, generated warp-uniformly at
     // the day's first tick (no divergence), tick offsets relative to the day
@@ -706,7 +722,8 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         asm("mov.b32 %0, %1;" : "=r"(act_len) : "r"(m_ke - m_ks));
       }
       const R gin_k = PROTO == GT_PROTO_CSR ? ((k >= m_ks) ? gin : (R)0)
-                                            : ((uint32_t)(sk - act_lo) < act_len ? gin : (R)0);
+                      : GT_KLOOP ? ((uint32_t)(k - m_ks) < act_len ? gin : (R)0)
+                                 : ((uint32_t)(sk - act_lo) < act_len ? gin : (R)0);
       bool ex_active = false;
       if (HAS_EX) {
         if (__builtin_expect(k >= ex_ke_c, 0)) {  // the session ended: advance the cursor
@@ -1006,7 +1023,8 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         // (clamped to [0, 246]); the FP32 estimate decides whenever 10 bg is
         // more than 1e-4 from an integer (its error is < 4e-5 up to bg = 25.6)
         // and the exact int64 compare against the table settles the rest.
-        const float t10 = __double2float_rz(bg) * 10.0f;
+        const float fbg = __double2float_rz(bg);
+        const float t10 = fbg * 10.0f;
         const float fl = floorf(t10);
         int kb = min(max((int)fl - 4, 0), GT_N_THRESHOLDS);
         const float fr = t10 - fl;
@@ -1032,7 +1050,18 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         bg_sum += bg;
         // extremes: only a tick in the lowest/highest bin so far can move them;
         // hypo runs: only ticks below 3.9 mmol/L (or ending such a run) matter
-        if (__builtin_expect(kb <= trig_lo || kb >= kb_max, 0) && alive) {
+        if (GT_FKEY) {
+          if (__builtin_expect(fbg <= f_lo || fbg >= f_mx, 0) && alive) {
+            const double omn = sdl[(SC_BGMIN) * kFastBS], omx = sdl[(SC_BGMAX) * kFastBS];
+            if (bg < omn) { sdl[(SC_BGMIN) * kFastBS] = bg; f_mn = fbg; }   // _kernel.py:144-147
+            if (bg > omx) { sdl[(SC_BGMAX) * kFastBS] = bg; f_mx = fbg; }
+            run39 = kb <= 34 ? run39 + 1 : 0;  // bg < 3.9 (THRESHOLDS[34])
+            run30 = kb <= 25 ? run30 + 1 : 0;  // bg < 3.0 (THRESHOLDS[25])
+            ev39 += run39 == u.hypoL;
+            ev30 += run30 == u.hypoL;
+            f_lo = run39 > 0 ? INFINITY : fmaxf(f_mn, __int_as_float(kF39Bits));
+          }
+        } else if (__builtin_expect(kb <= trig_lo || kb >= kb_max, 0) && alive) {
           if (kb <= kb_min) { const double o = sdl[(SC_BGMIN) * kFastBS]; sdl[(SC_BGMIN) * kFastBS] = bg < o ? bg : o; kb_min = kb; }
           if (kb >= kb_max) { const double o = sdl[(SC_BGMAX) * kFastBS]; sdl[(SC_BGMAX) * kFastBS] = bg > o ? bg : o; kb_max = kb; }
           run39 = kb <= 34 ? run39 + 1 : 0;  // bg < 3.9 (THRESHOLDS[34])
@@ -1074,6 +1103,9 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       if (PSC > 0) {
 #pragma unroll
         for (int s = 1; s < PSC; ++s) step(kb0 + s, false, ctl, s);
+      } else if (GT_KLOOP) {
+        const int32_t kend = kb0 + ps;
+        for (int32_t k = kb0 + 1; k < kend; ++k) step(k, false, ctl, 0);
       } else {
         for (int s = 1; s < ps; ++s) step(kb0 + s, false, ctl, s);
       }
@@ -1125,7 +1157,9 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           }
         }
         STI(SV_MKS, m_ks); STI(SV_MKE, m_ke);
-        STI(SV_KBMIN, kb_min); STI(SV_KBMAX, kb_max); STI(SV_RUN39, run39); STI(SV_RUN30, run30);
+        if (GT_FKEY) { STI(SV_KBMIN, __float_as_int(f_mn)); STI(SV_KBMAX, __float_as_int(f_mx)); }
+        else { STI(SV_KBMIN, kb_min); STI(SV_KBMAX, kb_max); }
+        STI(SV_RUN39, run39); STI(SV_RUN30, run30);
         STI(SV_EV39, ev39); STI(SV_EV30, ev30); STI(SV_ALIVE, alive ? 1 : 0);
         STI(SV_STATUS, status); STI(SV_DEATH, death_tick);
 #undef STD
