@@ -385,6 +385,24 @@ def run_ours(args):
     assert analytics.report_bytes(analytics.build_trial_report(acc_e, {})) == \
         analytics.report_bytes(analytics.build_trial_report(acc, {})), "e2e result differs"
 
+    # the reference-signature drop-in (simulation.run_trial, simulation.py:551
+    # semantics) with host Patient / ParameterSet objects: packing the
+    # population on the host is part of that call (one measurement, rank 0)
+    api = None
+    if rank == 0 and ws == 1:
+        from paper_2202_13927_b200.simulation import run_trial
+        entries = pop.entries()
+        walls = []
+        for _ in range(2):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            res = run_trial(entries, gen, args.controller, prof, "hovorka_ext", cfg, noise="philox", device=device)
+            walls.append(time.perf_counter() - t0)
+        assert analytics.report_bytes(analytics.build_trial_report(res.accumulator, {})) == \
+            analytics.report_bytes(analytics.build_trial_report(acc, {})), "run_trial result differs"
+        api = {"value": n * WEEKS / walls[-1], "unit": "patient-weeks/s", "wall_s": walls[-1],
+               "path": "simulation.run_trial(population=[(Patient, ParameterSet)] * n, noise='philox'): host "
+                       "packing of the reference's objects + staging + fused kernel + reduction + report"}
     if rank != 0:
         if ws > 1:
             torch.distributed.destroy_process_group()
@@ -435,6 +453,7 @@ def run_ours(args):
         "e2e": {"value": pw_per_step / (e2e / 1000.0), "unit": "patient-weeks/s",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "path": "trial.run_population_arrays (pinned host params -> report fields + per-patient metrics)"},
+        "e2e_run_trial_api": api,
         "gpu_launches": args.steps * 6,   # per step: fused kernel + exclusion re-run + 4 reduction kernels
         "clocks": clk.summary(),
         "sampler_s": sampler_s,

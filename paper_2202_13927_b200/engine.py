@@ -37,6 +37,28 @@ def require_device(device=None):
     return t.device(device)
 
 
+class nvtx:
+    """NVTX range around a host-side phase (sampler, schedule planning,
+    integrator, exclusion re-run, reduction, read-back), visible in Nsight
+    Systems / ncu --nvtx timelines.  A no-op without a CUDA build of torch."""
+
+    def __init__(self, name: str):
+        self.name = name
+
+    def __enter__(self):
+        try:
+            torch().cuda.nvtx.range_push(self.name)
+            self._on = True
+        except Exception:
+            self._on = False
+        return self
+
+    def __exit__(self, *exc):
+        if self._on:
+            torch().cuda.nvtx.range_pop()
+        return False
+
+
 def ptr(x) -> C.c_void_p:
     return C.c_void_p(0 if x is None else x.data_ptr())
 

@@ -101,11 +101,12 @@ def generate_population(seed: int, n: int, table=None, target_bg: float = 6.0, p
     if n < 1:
         raise PopulationError("population size must be >= 1")
     table = table or tables.default_parameter_table()
-    out = engine.sample_population(seed, n, table, pid0=pid0, target_bg=target_bg, device=device,
-                                   max_attempts=max_attempts,
-                                   weight=(tables.WEIGHT_MEAN_KG, tables.WEIGHT_SD_KG),
-                                   min_basal=tables.MIN_BASAL_U_PER_H,
-                                   max_weight_redraws=16 if on_exhausted == "redraw_weight" else 0)
+    with engine.nvtx("gt.population_sampler"):
+        out = engine.sample_population(seed, n, table, pid0=pid0, target_bg=target_bg, device=device,
+                                       max_attempts=max_attempts,
+                                       weight=(tables.WEIGHT_MEAN_KG, tables.WEIGHT_SD_KG),
+                                       min_basal=tables.MIN_BASAL_U_PER_H,
+                                       max_weight_redraws=16 if on_exhausted == "redraw_weight" else 0)
     status = out["status"]
     if bool((status != 0).any()):
         bad = int(np.nonzero(status.cpu().numpy())[0][0]) + pid0

@@ -134,6 +134,10 @@ class FastTrial:
         inputs = dict(self._inputs)
         if active is not None:
             inputs["active"] = active
+        with engine.nvtx("gt.exclusion_rerun" if rerun_diverged else "gt.fused_integrator"):
+            self._launch(inputs, injected, rerun_diverged)
+
+    def _launch(self, inputs, injected, rerun_diverged):
         engine.launch_fast(inputs, self.outs, self.sz, self.config.dt_s,
                            self.config.controller_period_s, self.seed, rng.ROLE_DEVICE_NOISE,
                            self.hypo_min_ticks, self.device, meal_spec=self.meal_spec, csr=self.csr,
@@ -169,6 +173,10 @@ class FastTrial:
         return tr[0, : int(ticks[0])]
 
     def reduce(self):
+        with engine.nvtx("gt.reduction"):
+            self._reduce()
+
+    def _reduce(self):
         engine.launch_reduce(self.outs, self.red, self.sz, self.config.dt_s, self.device)
 
     def step(self):
