@@ -269,18 +269,112 @@ def golden_population(n):
     return params, ub, x0
 
 
+REF_DIR = os.path.join(REPO, "baseline", "_ref")
+
+
+def reference_available() -> bool:
+    """The unmodified reference (glucotrial, pip-installed into baseline/_ref)
+    and its numba JIT importable on this host."""
+    if not os.path.isdir(os.path.join(REF_DIR, "glucotrial")):
+        return False
+    try:
+        import numba  # noqa: F401
+    except ImportError:
+        return False
+    return True
+
+
+_REF_CACHE = {}
+
+
+class _RefPatient:
+    """The two Patient fields the reference's simulation reads (id, weight)."""
+
+    def __init__(self, pid, w):
+        self.id, self.body_weight_kg = pid, w
+
+
+def reference_numba(n_sample: int, weeks: int, threads: int):
+    """The reference's OWN CPU path on the host cores: glucotrial.simulation.
+    run_trial(..., workers=threads) from baseline/_ref on its numba fast engine
+    (hovorka_ext + dual_hormone, simulation.py:301-311; the BASELINE's PID runs
+    only on the reference's ~300x slower generic engine, so the reference's
+    own controller is the conservative baseline), after _warmup_fast_path()
+    (simulation.py:534-548).  Same shape as the GPU workload: 3-meal generator
+    (the product's plug-in through the reference's generator contract), dt
+    60 s, seed 1, the reference sampler's own seed-7 parameter sets tiled to
+    n_sample patients.  Returns (patient-weeks/s over run_trial's own wall_s,
+    wall_s)."""
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    from glucotrial.controller import load_profile
+    from glucotrial.population import ParameterSet, load_parameter_table
+    from glucotrial.simulation import SimulationConfig as RefConfig
+    from glucotrial.simulation import _warmup_fast_path, run_trial
+    from paper_2202_13927_b200.protocol import ThreeMealProtocol
+    if n_sample not in _REF_CACHE:
+        g = np.load(os.path.join(REPO, "tests", "golden", "population_s7_n4000.npz"))
+        fixed = load_parameter_table().fixed
+        names = [str(x) for x in g["names"]]
+
+        entries = []
+        for i in range(n_sample):
+            j = i % g["weights"].size
+            v = {"weight_kg": float(g["weights"][j])}
+            v.update({k: float(x) for k, x in zip(names, g["sampled"][j])})
+            v.update(fixed)
+            entries.append((_RefPatient(i, float(g["weights"][j])), ParameterSet(values=v, u_basal_u_per_h=float(g["ubasal"][j]))))
+        _REF_CACHE[n_sample] = entries
+    _warmup_fast_path()
+    cfg = RefConfig(horizon_s=weeks * 7 * 86400.0, seed=SEED, dt_s=DT_S)
+    res = run_trial(_REF_CACHE[n_sample], ThreeMealProtocol(), "dual_hormone", load_profile(), "hovorka_ext", cfg,
+                    workers=threads)
+    assert res.accumulator.n_patients == n_sample
+    return n_sample * weeks / res.wall_s, res.wall_s
+
+
+def reference_sample_size(weeks: int, threads: int) -> int:
+    """Patients per reference sample: a pilot sizes it to about
+    CPU_SAMPLE_SECONDS of reference work on this host."""
+    pilot = max(threads * 32, 256)
+    rate, _ = reference_numba(pilot, weeks, threads)
+    return int(min(max(pilot, rate * CPU_SAMPLE_SECONDS / weeks), 400_000))
+
+
+def cpu_reference_or_port(weeks: int, threads: int, controller_id: str):
+    """The CPU baseline of record: the reference itself (numba) when it is
+    installed, else the oracle's C port.  Returns (value, wall_s, kind, sample)."""
+    if reference_available():
+        n = reference_sample_size(weeks, threads)
+        v, wall = reference_numba(n, weeks, threads)
+        return v, wall, "reference", (f"{n} patients x {weeks} weeks, dt 60 s: glucotrial.simulation.run_trial("
+                                      f"workers={threads}) from baseline/_ref, numba fast engine, dual_hormone, "
+                                      f"3-meal plug-in ({wall:.1f} s wall)")
+    n = cpu_sample_size(weeks, threads, controller_id)
+    v, wall = cpu_baseline(n, weeks, threads, controller_id)
+    return v, wall, "port", (f"{n} patients x {weeks} weeks (oracle C restatement, OpenMP, {wall:.1f} s wall; "
+                             "reference not installed)")
+
+
 def run_reference_arm(args):
     ws, rank, local = dist_env()
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    n_sample = cpu_sample_size(WEEKS, threads, args.controller)
+    use_ref = reference_available()
+    n_sample = reference_sample_size(WEEKS, threads) if use_ref else cpu_sample_size(WEEKS, threads, args.controller)
     vals = []
     for i in range(args.warmup + args.steps):
-        v, wall = cpu_baseline(n_sample, WEEKS, threads, args.controller)
+        if use_ref:
+            v, wall = reference_numba(n_sample, WEEKS, threads)
+        else:
+            v, wall = cpu_baseline(n_sample, WEEKS, threads, args.controller)
         if i >= args.warmup:
             vals.append(v)
     v = float(np.mean(vals))
+    # the oracle's C port on the same host, for the record (kind "port")
+    port_n = cpu_sample_size(WEEKS, threads, "dual_hormone")
+    port_v, port_wall = cpu_baseline(port_n, WEEKS, threads, "dual_hormone")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "patient-weeks/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -288,10 +382,18 @@ def run_reference_arm(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"BASELINE configs[1] shape ({N_PATIENTS} patients x {WEEKS} weeks), "
                                f"timed on a {n_sample}-patient sample at full horizon",
-                   "dt_s": DT_S, "seed": SEED, "controller": controller_setup(args.controller)[2],
+                   "dt_s": DT_S, "seed": SEED,
+                   "controller": ("dual_hormone (the reference's own controller on its numba fast engine; "
+                                  "the BASELINE's PID runs only on its ~300x slower generic engine)")
+                   if use_ref else controller_setup(args.controller)[2],
                    "protocol": "three_meal"},
-        "cpu_baseline": {"value": v, "unit": "patient-weeks/s", "cores": threads, "kind": "port",
-                         "sample": f"{n_sample} patients x {WEEKS} weeks, dt 60 s, all {threads} host threads"},
+        "cpu_baseline": {"value": v, "unit": "patient-weeks/s", "cores": threads,
+                         "kind": "reference" if use_ref else "port",
+                         "sample": (f"{n_sample} patients x {WEEKS} weeks, dt 60 s: glucotrial.simulation.run_trial("
+                                    f"workers={threads}) from baseline/_ref (numba), after _warmup_fast_path()")
+                         if use_ref else f"{n_sample} patients x {WEEKS} weeks, dt 60 s, all {threads} host threads"},
+        "port": {"value": port_v, "unit": "patient-weeks/s", "kind": "port", "threads": threads,
+                 "sample": f"{port_n} patients x {WEEKS} weeks, dual_hormone, oracle C restatement (OpenMP)"},
         "e2e": {"value": v, "unit": "patient-weeks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -415,11 +517,10 @@ def run_ours(args):
     sim_s = float(np.mean(sim_ms)) / 1000.0
     peak, peak_burst, peak_src = fp64_peak()
     achieved = flop_per_launch / sim_s / 1e12
-    cpu_v, cpu_wall = (None, None)
+    cpu_v, cpu_wall, cpu_kind, cpu_sample = None, None, None, None
     if not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        cpu_n = cpu_sample_size(WEEKS, threads, args.controller)
-        cpu_v, cpu_wall = cpu_baseline(cpu_n, WEEKS, threads, args.controller)
+        cpu_v, cpu_wall, cpu_kind, cpu_sample = cpu_reference_or_port(WEEKS, threads, args.controller)
     q = analytics.metric_quantiles(acc_all)
     h2d = params_h.numel() * 8 + basal_h.numel() * 8
     d2h = n * (5 * 4 + 2 * 4 + 4) + 8 * (4 + 5 + 5 * 201 + 247 + 2 * 246 + 2 + 3 * ft.sz["n_grid"] + 603 + 3 + 4 + 7 * 201)
@@ -447,9 +548,8 @@ def run_ours(args):
                      "algorithmic_flops_per_launch": flop_per_launch,
                      "flops_per_step": F, "peak_source": peak_src,
                      "kernel_ms": sim_s * 1000.0, "share_of_step": float(np.mean(sim_ms) / np.mean(step_ms))},
-        "cpu_baseline": ({"value": cpu_v, "unit": "patient-weeks/s", "cores": os.cpu_count(), "kind": "port",
-                          "sample": f"{cpu_n} patients x {WEEKS} weeks (oracle C "
-                                    f"restatement, OpenMP, {cpu_wall:.1f} s wall)"} if cpu_v else None),
+        "cpu_baseline": ({"value": cpu_v, "unit": "patient-weeks/s", "cores": os.cpu_count(), "kind": cpu_kind,
+                          "sample": cpu_sample} if cpu_v else None),
         "e2e": {"value": pw_per_step / (e2e / 1000.0), "unit": "patient-weeks/s",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "path": "trial.run_population_arrays (pinned host params -> report fields + per-patient metrics)"},
