@@ -56,6 +56,15 @@ namespace gt {
 #ifndef GT_DAY_VOTE
 #define GT_DAY_VOTE 1
 #endif
+// Per-instance code shape, a bit per (protocol, controller) as GT_PS5:
+// 1 three_meal/pid_pump, 2 three_meal/dual_hormone, 4 csr/pid_pump,
+// 8 csr/dual_hormone (measured with tools/ab_kernel.py, profiles/r02_ab_*.json).
+#ifndef GT_PAIRS
+#define GT_PAIRS 8      // plain steps in pairs (-4.7 % csr/dual_hormone; +3 to +24 % on three_meal)
+#endif
+#ifndef GT_NOPIPE
+#define GT_NOPIPE 4     // instances drawing each tick's normals at use, not one step ahead (-0.8 % csr/pid_pump)
+#endif
 #ifndef GT_NOISE_PIPE
 #define GT_NOISE_PIPE 1  // draw tick k + 1's normals during step k
 #endif
@@ -646,7 +655,9 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
 
     // software-pipelined noise: the normals of tick k + 1 are drawn during
     // step k, next to its Euler update, so no step waits on its own Philox
-    constexpr bool PIPE = GT_NOISE_PIPE && NOISE == GT_NOISE_PHILOX && !AGG;
+    constexpr int kShapeBit = (PROTO == GT_PROTO_CSR ? 4 : 1) << (CTRL == GT_CTRL_PID_PUMP ? 0 : 1);
+    constexpr bool PIPE = GT_NOISE_PIPE && !(GT_NOPIPE & kShapeBit) && NOISE == GT_NOISE_PHILOX && !AGG;
+    constexpr bool PAIRS = (GT_PAIRS & kShapeBit) != 0;
     float pz0 = 0.f, pz1 = 0.f, pz2 = 0.f, pz3 = 0.f;
     auto draw_pipe = [&](int32_t kk) {
       const U4 r = philox_draw((uint32_t)kk);
@@ -1103,6 +1114,11 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       if (PSC > 0) {
 #pragma unroll
         for (int s = 1; s < PSC; ++s) step(kb0 + s, false, ctl, s);
+      } else if (GT_KLOOP == 2 || PAIRS) {   // pairs of plain steps (loop-carried registers alternate)
+        const int32_t kend = kb0 + ps;
+        int32_t k = kb0 + 1;
+        for (; k + 1 < kend; k += 2) { step(k, false, ctl, 0); step(k + 1, false, ctl, 0); }
+        if (k < kend) step(k, false, ctl, 0);
       } else if (GT_KLOOP) {
         const int32_t kend = kb0 + ps;
         for (int32_t k = kb0 + 1; k < kend; ++k) step(k, false, ctl, 0);
