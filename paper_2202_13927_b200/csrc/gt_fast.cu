@@ -65,6 +65,9 @@ namespace gt {
 #ifndef GT_NOPIPE
 #define GT_NOPIPE 4     // instances drawing each tick's normals at use, not one step ahead (-0.8 % csr/pid_pump)
 #endif
+#ifndef GT_LATE
+#define GT_LATE 1       // controller after the tick's Euler update (only S1 / Z1 take its output)
+#endif
 #ifndef GT_NOISE_PIPE
 #define GT_NOISE_PIPE 1  // draw tick k + 1's normals during step k
 #endif
@@ -928,7 +931,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       // late control measured -1.2 % under pid_pump and +3.8 % under
       // dual_hormone (whose larger controller then spills), and +2 % on the
       // CSR (NorthernYear) path: pid_pump with the generated meals only
-      constexpr bool kLateControl = !TRACE && CTRL == GT_CTRL_PID_PUMP && PROTO == GT_PROTO_THREE_MEAL;
+      constexpr bool kLateControl = !TRACE && (GT_LATE & kShapeBit) != 0;
       if (tick && !kLateControl) control();
       // statistics at tick k (_kernel.py:137-160)
       double bg = (double)MR_(Q1, pc.invVGw);  // explicit: never fused into the sums below
