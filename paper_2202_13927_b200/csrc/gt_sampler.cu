@@ -13,6 +13,7 @@
 // device population bit for bit (oracle_sample_patients; tests/test_gpu_sampler.py).
 // COMPILED WITH --fmad=false (exact translation unit).
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include "gt_ref_model.cuh"
 
@@ -49,14 +50,29 @@ __device__ __forceinline__ double sampled_value(const gt_sampler_args& a, int j,
 // and the order of the rules are the reference's (population.py:217-259),
 // so the population is bit-identical to the one-thread-per-patient loop
 // (oracle_sample_patients, tests/test_gpu_sampler.py).
-__global__ void __launch_bounds__(128) sampler_kernel(gt_sampler_args a, unsigned long long* queue) {
+// A patient still without an accepted set after kPark attempts of one body
+// weight (a feasible weight needs more than 384 with probability ~1e-5; a
+// weight below ~30 kg never succeeds and spends the whole 10 000-attempt
+// budget) is handed to straggler_kernel, which searches its remaining
+// attempts 128 at a time with a whole block instead of one lane.
+constexpr int kPark = 384;
+struct Straggler {
+  int64_t i;
+  int32_t total, attempt, wdraw, last_surv;  // last_surv: counter of the latest cheap-rule survivor, -1 none
+  uint32_t wctr, pad;
+  double w;
+};
+
+__global__ void __launch_bounds__(128) sampler_kernel(gt_sampler_args a, unsigned long long* queue,
+                                                      Straggler* park, unsigned int* n_park, int park_cap) {
   const int lane = threadIdx.x & 31;
   const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
   double p[GT_N_PARAMS], x[GT_N_STATES], vals[16];
   double ub = 0.0, w = 0.0;
   int64_t i = -1;                       // this lane's patient (-1: none)
-  int32_t attempt = 0, total = 0, wdraw = 0;
+  int32_t attempt = 0, total = 0, wdraw = 0, last_surv = -1;
   uint32_t wctr = 0, pid = 0;
+  bool park_full = false;
   long long rej_neg = 0, rej_sd = 0, rej_ss = 0, rej_basal = 0;
   bool drained = false;
   auto draw_weight = [&]() {             // population.py:148-153
@@ -90,7 +106,7 @@ __global__ void __launch_bounds__(128) sampler_kernel(gt_sampler_args a, unsigne
           i = next;
           pid = (uint32_t)(a.pid0 + i);
           for (int k = 0; k < GT_N_PARAMS; ++k) p[k] = a.fixed_params[k];
-          total = 0; wdraw = 0; wctr = 0;
+          total = 0; wdraw = 0; wctr = 0; last_surv = -1;
           draw_weight();
         } else {
           drained = true;
@@ -108,6 +124,15 @@ __global__ void __launch_bounds__(128) sampler_kernel(gt_sampler_args a, unsigne
           if (wdraw < a.max_weight_redraws) { ++wdraw; draw_weight(); continue; }
           finish(1);
           break;
+        }
+        if (attempt >= kPark && !park_full) {   // hand the rest of this patient to straggler_kernel
+          const unsigned slot = atomicAdd(n_park, 1u);
+          if ((int)slot < park_cap) {
+            park[slot] = Straggler{i, total, attempt, wdraw, last_surv, wctr, 0u, w};
+            i = -1;
+            break;
+          }
+          park_full = true;   // list full: carry on in this lane
         }
         const uint32_t actr = (uint32_t)(total + attempt);
         bool neg = false;
@@ -140,6 +165,7 @@ __global__ void __launch_bounds__(128) sampler_kernel(gt_sampler_args a, unsigne
           vals[q + 1] = sampled_value(a, q + 1, det_inv_norm(u52(r.z, r.w)));
       }
       for (int j = 0; j < a.n_sampled; ++j) p[a.param_index[j]] = vals[j];
+      last_surv = (int32_t)actr;
       if (!steady_state_dev(p, a.target_bg, x, &ub)) { ++rej_ss; ++attempt; }
       else if (ub < a.min_basal_uh) { ++rej_basal; ++attempt; }
       else { total += attempt + 1; finish(0); }
@@ -156,6 +182,124 @@ __global__ void __launch_bounds__(128) sampler_kernel(gt_sampler_args a, unsigne
       if (lane == 0 && v) atomicAdd((unsigned long long*)&a.reject_counts[k], v);
     }
   }
+}
+
+// One attempt's values (all sampled parameters), counter-addressed.
+__device__ void draw_attempt(const gt_sampler_args& a, uint32_t actr, uint32_t pid, uint32_t k0, uint32_t k1,
+                             double* vals) {
+  for (int q = 0; q < a.n_sampled; q += 2) {
+    const U4 r = philox4x32_10(actr, pid, kRoleSamplerParams, (uint32_t)(q >> 1), k0, k1);
+    vals[q] = sampled_value(a, q, det_inv_norm(u52(r.x, r.y)));
+    if (q + 1 < a.n_sampled) vals[q + 1] = sampled_value(a, q + 1, det_inv_norm(u52(r.z, r.w)));
+  }
+}
+
+// The parked patients, one block each: thread t evaluates attempt a0 + t of
+// the current body weight (cheap rules, then the steady-state solve of the
+// survivors), the lowest accepted attempt wins, and only the attempts before
+// it are counted -- exactly the sequential loop's result and rejection
+// counts, 128 attempts per round.
+__global__ void __launch_bounds__(128) straggler_kernel(gt_sampler_args a, const Straggler* park,
+                                                        const unsigned int* n_park, int park_cap,
+                                                        unsigned int* next) {
+  __shared__ int s_amin, s_last, s_j;
+  const int t = threadIdx.x;
+  const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
+  const int n_list = min((int)*n_park, park_cap);
+  long long rej[4] = {0, 0, 0, 0};
+  double p[GT_N_PARAMS], x[GT_N_STATES], vals[16];
+  for (;;) {
+    if (t == 0) s_j = (int)atomicAdd(next, 1u);
+    __syncthreads();
+    const int j = s_j;
+    __syncthreads();
+    if (j >= n_list) break;
+    const Straggler st = park[j];
+    const int64_t i = st.i;
+    const uint32_t pid = (uint32_t)(a.pid0 + i);
+    int32_t total = st.total, a0 = st.attempt, wdraw = st.wdraw, last_surv = st.last_surv;
+    uint32_t wctr = st.wctr;
+    double w = st.w;
+    for (int k = 0; k < GT_N_PARAMS; ++k) p[k] = a.fixed_params[k];
+    p[PW] = w;
+    int status = 1;
+    for (;;) {
+      if (a0 >= a.max_attempts || !(w > 0.0)) {   // this body weight's budget is spent
+        total += a0 < a.max_attempts ? a0 : a.max_attempts;
+        if (wdraw >= a.max_weight_redraws) break;
+        ++wdraw;
+        w = 0.0;                                  // population.py:148-153 (every thread, same draws)
+        for (int q = 0; q < a.max_attempts; ++q, ++wctr) {
+          const U4 r = philox4x32_10(wctr, pid, kRoleSamplerWeight, 0u, k0, k1);
+          const double v = A_(a.weight_mean, M_(a.weight_sd, det_inv_norm(u52(r.x, r.y))));
+          if (v > 0.0) { w = v; ++wctr; break; }
+        }
+        p[PW] = w;
+        a0 = 0;
+        continue;
+      }
+      const int32_t att = a0 + t;
+      const bool valid = att < a.max_attempts;
+      const uint32_t actr = (uint32_t)(total + att);
+      int reason = 0;        // 1 negative, 2 outside 1 SD, 3 no steady state, 4 basal, 5 accepted
+      double ub = 0.0;
+      if (valid) {
+        draw_attempt(a, actr, pid, k0, k1, vals);
+        bool neg = false, outside = false;
+        for (int q = 0; q < a.n_sampled; ++q) neg |= vals[q] < 0.0;
+        for (int q = 0; q < a.n_sampled; ++q)
+          if (a.kind[q] == 0 && fabs(S_(vals[q], a.a[q])) > a.b[q]) outside = true;
+        if (neg) reason = 1;
+        else if (outside) reason = 2;
+        else {
+          for (int q = 0; q < a.n_sampled; ++q) p[a.param_index[q]] = vals[q];
+          if (!steady_state_dev(p, a.target_bg, x, &ub)) reason = 3;
+          else reason = ub < a.min_basal_uh ? 4 : 5;
+        }
+      }
+      if (t == 0) { s_amin = INT_MAX; s_last = -1; }
+      __syncthreads();
+      if (reason == 5) atomicMin(&s_amin, att);
+      __syncthreads();
+      const int amin = s_amin;
+      const bool counted = valid && att <= amin;   // attempts the sequential loop reaches
+      if (counted && reason >= 3) atomicMax(&s_last, (int)actr);
+      if (counted && reason >= 1 && reason <= 4) ++rej[reason - 1];
+      __syncthreads();
+      if (s_last >= 0) last_surv = s_last;
+      if (amin != INT_MAX) {
+        total += amin + 1;
+        status = 0;
+        if (att == amin) {   // the accepted attempt writes the patient
+          for (int k = 0; k < GT_N_PARAMS; ++k) a.params[i * GT_N_PARAMS + k] = p[k];
+          for (int k = 0; k < GT_N_STATES; ++k) a.x0[i * GT_N_STATES + k] = x[k];
+          a.u_basal_uh[i] = ub;
+          a.attempts[i] = total;
+          a.status[i] = 0;
+        }
+        break;
+      }
+      a0 += blockDim.x;
+      __syncthreads();
+    }
+    if (status != 0 && t == 0) {   // exhausted: the sequential loop's last p (latest survivor's values)
+      for (int k = 0; k < GT_N_PARAMS; ++k) p[k] = a.fixed_params[k];
+      p[PW] = w;
+      if (last_surv >= 0) {
+        draw_attempt(a, (uint32_t)last_surv, pid, k0, k1, vals);
+        for (int q = 0; q < a.n_sampled; ++q) p[a.param_index[q]] = vals[q];
+      }
+      for (int k = 0; k < GT_N_PARAMS; ++k) a.params[i * GT_N_PARAMS + k] = p[k];
+      for (int k = 0; k < GT_N_STATES; ++k) a.x0[i * GT_N_STATES + k] = 0.0;
+      a.u_basal_uh[i] = 0.0;
+      a.attempts[i] = total;
+      a.status[i] = 1;
+    }
+    __syncthreads();
+  }
+  if (a.reject_counts)
+    for (int k = 0; k < 4; ++k)
+      if (rej[k]) atomicAdd((unsigned long long*)&a.reject_counts[k], (unsigned long long)rej[k]);
 }
 
 // Materialise the 3-meal schedule (gt_common.cuh gen_meal).
@@ -184,16 +328,27 @@ int gt_launch_sampler(const gt_sampler_args* a, cudaStream_t st) {
   if (per_sm < 1) per_sm = 1;
   // persistent grid: at most one resident wave, never more lanes than patients
   const int64_t blocks = std::min<int64_t>((int64_t)sms * per_sm, (a->n + bs - 1) / bs);
-  unsigned long long* queue = nullptr;
+  // workspace: patient queue, straggler count and cursor, straggler list
+  const int cap = (int)std::min<int64_t>(std::max<int64_t>(256, a->n / 256), 1 << 20);
+  const size_t head = 64;
+  char* ws = nullptr;
   gt_keep_pool_mapped();
-  if (cudaMallocAsync(&queue, sizeof(unsigned long long), st) != cudaSuccess) {
-    gt_set_error("gt_sample_population: queue allocation failed");
+  if (cudaMallocAsync(&ws, head + sizeof(gt::Straggler) * (size_t)cap, st) != cudaSuccess) {
+    gt_set_error("gt_sample_population: workspace allocation failed");
     return GT_ECUDA;
   }
-  cudaMemsetAsync(queue, 0, sizeof(unsigned long long), st);
-  gt::sampler_kernel<<<(unsigned)blocks, bs, 0, st>>>(*a, queue);
-  const int e = gt_check_launch("sampler_kernel");
-  cudaFreeAsync(queue, st);
+  cudaMemsetAsync(ws, 0, head, st);
+  auto* queue = reinterpret_cast<unsigned long long*>(ws);
+  auto* n_park = reinterpret_cast<unsigned int*>(ws + 8);
+  auto* cursor = reinterpret_cast<unsigned int*>(ws + 16);
+  auto* park = reinterpret_cast<gt::Straggler*>(ws + head);
+  gt::sampler_kernel<<<(unsigned)blocks, bs, 0, st>>>(*a, queue, park, n_park, cap);
+  int e = gt_check_launch("sampler_kernel");
+  if (e == GT_OK) {
+    gt::straggler_kernel<<<(unsigned)(2 * sms), bs, 0, st>>>(*a, park, n_park, cap, cursor);
+    e = gt_check_launch("straggler_kernel");
+  }
+  cudaFreeAsync(ws, st);
   return e;
 }
 
