@@ -56,6 +56,11 @@ __device__ __forceinline__ double sampled_value(const gt_sampler_args& a, int j,
 // budget) is handed to straggler_kernel, which searches its remaining
 // attempts 128 at a time with a whole block instead of one lane.
 constexpr int kPark = 384;
+#ifndef GT_SAMPLER_CAP
+#define GT_SAMPLER_CAP 4   // measured best of 1,2,3,4,8,12,16 (tools/ab_sampler.sh)
+#endif
+constexpr int kCap = GT_SAMPLER_CAP;   // cheap attempts per lane per round
+constexpr int kMaxSampled = 16;
 struct Straggler {
   int64_t i;
   int32_t total, attempt, wdraw, last_surv;  // last_surv: counter of the latest cheap-rule survivor, -1 none
@@ -114,10 +119,12 @@ __global__ void __launch_bounds__(128) sampler_kernel(gt_sampler_args a, unsigne
       }
     }
     if (__all_sync(0xffffffffu, i < 0)) break;
-    // ---- phase 1: cheap rules until a survivor (or the budget is spent)
+    // ---- phase 1: cheap rules until a survivor, at most kCap attempts this
+    // round (a lane without a survivor skips phase 2 and continues next round:
+    // the warp never waits for one lane's long rejection chain)
     bool survivor = false;
     if (i >= 0) {
-      while (!survivor) {
+      for (int c = 0; c < kCap && !survivor && i >= 0; ++c) {
         if (attempt >= a.max_attempts || !(w > 0.0)) {
           // budget spent for this body weight: redraw it or fail
           total += attempt;
@@ -135,36 +142,43 @@ __global__ void __launch_bounds__(128) sampler_kernel(gt_sampler_args a, unsigne
           park_full = true;   // list full: carry on in this lane
         }
         const uint32_t actr = (uint32_t)(total + attempt);
-        bool neg = false;
-        for (int q = 0; q < a.n_sampled; q += 2) {
-          const bool has_normal = a.kind[q] == 0 || (q + 1 < a.n_sampled && a.kind[q + 1] == 0);
-          if (!has_normal) continue;
+        // the normal draws only (lognormals are never negative and have no SD rule)
+#pragma unroll
+        for (int q = 0; q < kMaxSampled; q += 2) {
+          if (q >= a.n_sampled) break;
+          const bool n0 = a.kind[q] == 0, n1 = q + 1 < a.n_sampled && a.kind[q + 1] == 0;
+          if (!(n0 || n1)) continue;
           const U4 r = philox4x32_10(actr, pid, kRoleSamplerParams, (uint32_t)(q >> 1), k0, k1);
-          if (a.kind[q] == 0) vals[q] = sampled_value(a, q, det_inv_norm(u52(r.x, r.y)));
-          if (q + 1 < a.n_sampled && a.kind[q + 1] == 0)
-            vals[q + 1] = sampled_value(a, q + 1, det_inv_norm(u52(r.z, r.w)));
+          if (n0) vals[q] = sampled_value(a, q, det_inv_norm(u52(r.x, r.y)));
+          if (n1) vals[q + 1] = sampled_value(a, q + 1, det_inv_norm(u52(r.z, r.w)));
         }
-        for (int j = 0; j < a.n_sampled; ++j) neg |= a.kind[j] == 0 && vals[j] < 0.0;
-        if (neg) { ++rej_neg; ++attempt; continue; }
-        bool outside = false;
-        for (int j = 0; j < a.n_sampled; ++j)
-          if (a.kind[j] == 0 && fabs(S_(vals[j], a.a[j])) > a.b[j]) { outside = true; break; }
-        if (outside) { ++rej_sd; ++attempt; continue; }
+        bool neg = false, outside = false;
+#pragma unroll
+        for (int j = 0; j < kMaxSampled; ++j)
+          if (j < a.n_sampled && a.kind[j] == 0) {
+            neg |= vals[j] < 0.0;
+            outside |= fabs(S_(vals[j], a.a[j])) > a.b[j];
+          }
+        if (neg) { ++rej_neg; ++attempt; continue; }          // population.py:234-236
+        if (outside) { ++rej_sd; ++attempt; continue; }       // population.py:237-244
         survivor = true;
       }
     }
     // ---- phase 2: the survivors' lognormal draws and steady-state solves
     if (survivor) {
       const uint32_t actr = (uint32_t)(total + attempt);
-      for (int q = 0; q < a.n_sampled; q += 2) {
-        const bool has_log = a.kind[q] == 1 || (q + 1 < a.n_sampled && a.kind[q + 1] == 1);
-        if (!has_log) continue;
+#pragma unroll
+      for (int q = 0; q < kMaxSampled; q += 2) {
+        if (q >= a.n_sampled) break;
+        const bool l0 = a.kind[q] == 1, l1 = q + 1 < a.n_sampled && a.kind[q + 1] == 1;
+        if (!(l0 || l1)) continue;
         const U4 r = philox4x32_10(actr, pid, kRoleSamplerParams, (uint32_t)(q >> 1), k0, k1);
-        if (a.kind[q] == 1) vals[q] = sampled_value(a, q, det_inv_norm(u52(r.x, r.y)));
-        if (q + 1 < a.n_sampled && a.kind[q + 1] == 1)
-          vals[q + 1] = sampled_value(a, q + 1, det_inv_norm(u52(r.z, r.w)));
+        if (l0) vals[q] = sampled_value(a, q, det_inv_norm(u52(r.x, r.y)));
+        if (l1) vals[q + 1] = sampled_value(a, q + 1, det_inv_norm(u52(r.z, r.w)));
       }
-      for (int j = 0; j < a.n_sampled; ++j) p[a.param_index[j]] = vals[j];
+#pragma unroll
+      for (int j = 0; j < kMaxSampled; ++j)
+        if (j < a.n_sampled) p[a.param_index[j]] = vals[j];
       last_surv = (int32_t)actr;
       if (!steady_state_dev(p, a.target_bg, x, &ub)) { ++rej_ss; ++attempt; }
       else if (ub < a.min_basal_uh) { ++rej_basal; ++attempt; }
@@ -329,7 +343,8 @@ int gt_launch_sampler(const gt_sampler_args* a, cudaStream_t st) {
   // persistent grid: at most one resident wave, never more lanes than patients
   const int64_t blocks = std::min<int64_t>((int64_t)sms * per_sm, (a->n + bs - 1) / bs);
   // workspace: patient queue, straggler count and cursor, straggler list
-  const int cap = (int)std::min<int64_t>(std::max<int64_t>(256, a->n / 256), 1 << 20);
+  // ~0.5 % of patients (light body weights: low acceptance) pass 384 attempts
+  const int cap = (int)std::min<int64_t>(std::max<int64_t>(1024, a->n / 16), 1 << 22);
   const size_t head = 64;
   char* ws = nullptr;
   gt_keep_pool_mapped();
