@@ -518,3 +518,24 @@ def test_philox_forms_agree_generator_vs_csr(dev):
     b = _run_fast(case, sub, dev, meal_spec=ThreeMealProtocol().device_spec(), injected=None)
     for k in ("status", "ticks", "bg_hist", "bg_stats", "day_dose", "hypo_events", "timeline_pp", "x_out"):
         assert np.array_equal(_h(getattr(a, k)), _h(getattr(b, k))), k
+
+
+@pytest.mark.parametrize("name,controller", [("sim_hypo_threemeal_dt60.npz", 0), ("sim_hypo_pid_threemeal_dt60.npz", 1),
+                                             ("sim_hypo_northern_dt30.npz", 0)])
+def test_tie_classifier_runners_on_device(dev, oracle, name, controller):
+    """The classifier's two runners (tests/ties.py) on real patients: the fused
+    TRACE run reproduces the fused statistics it stands for, and against the
+    reference's trace it has no discrete divergence (so a real tie would be
+    located at its first tick)."""
+    case = SimCase(name)
+    sub = case.subset(case.valid())
+    mk = ties.case_inputs(case, sub, controller)
+    for j in range(min(4, len(sub["idx"]))):
+        pi = mk(j)
+        tr_r, ticks = ties.oracle_trace(oracle, pi)
+        tr_f, outs = ties.fused_trace(pi, dev)
+        hist_f, _ = ties.trace_hist(tr_f, ticks)
+        assert np.array_equal(hist_f, _h(outs.bg_hist)[:, 0])
+        assert np.array_equal(_h(outs.hypo_events)[:, 0], case.g["hypo"][sub["idx"][j]])
+        assert ties.first_divergence(tr_r, tr_f) is None
+        assert np.allclose(tr_f[:ticks, 1], tr_r[:ticks, 1], rtol=1e-9, atol=0)
