@@ -332,6 +332,12 @@ typedef struct {
     double *ex_start_s, *ex_hrr, *ex_announced;  /* [n][GT_NY_EX] */
     int32_t *n_meals, *n_ex;        /* optional [n]: events before the horizon
                                        (n_meals = -1: week plan failed) */
+    /* announcement policy (protocol.py:373-394, NorthernYearProtocol.announcement):
+     * each meal of the year is left unannounced with probability
+     * fraction_unannounced, else announced at magnitude x U(factor_lo,
+     * factor_hi), drawn from the reference's stream(trial_seed, pid, 4).
+     * fraction 0 and factors (1, 1) = the default policy (no draws). */
+    double fraction_unannounced, factor_lo, factor_hi;
     uint16_t *week_days;            /* optional [52][n]: 2-bit day types
                                        (standard, active, movie, late) */
 } gt_northern_args;

@@ -114,7 +114,8 @@ class NorthernArgs(C.Structure):
         ("n", I64), ("pid0", I64), ("trial_seed", U64), ("dt_s", D), ("period_s", D), ("horizon_s", D),
         ("params", P), ("meal_ks", P), ("meal_ke", P), ("meal_kp", P), ("meal_rate", P), ("meal_ann", P),
         ("ex_ks", P), ("ex_ke", P), ("ex_start_s", P), ("ex_hrr", P), ("ex_announced", P),
-        ("n_meals", P), ("n_ex", P), ("week_days", P),
+        ("n_meals", P), ("n_ex", P), ("fraction_unannounced", D), ("factor_lo", D), ("factor_hi", D),
+        ("week_days", P),
     ]
 
 

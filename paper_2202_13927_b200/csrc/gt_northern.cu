@@ -89,6 +89,9 @@ struct Stream {
     if (pos >= 4) refill();
     return buf[pos++];
   }
+  __device__ double next_double() {  // numpy next_double: (next_uint64 >> 11) * 2^-53
+    return (double)(next64() >> 11) * (1.0 / 9007199254740992.0);
+  }
   __device__ uint32_t next32() {
     if (has32) { has32 = false; return u32; }
     const uint64_t v = next64();
@@ -164,6 +167,22 @@ __global__ void northern_kernel(const gt_northern_args a) {
   g.key1 = (uint64_t)w4[2] | ((uint64_t)w4[3] << 32);
   g.pos = 4;
 
+  // announcement policy stream: stream(trial_seed, pid, ROLE_ANNOUNCEMENT = 4)
+  // (rng.py:26-39), used only when the policy is not the default
+  // (simulation.py:441-444)
+  const bool policy = a.fraction_unannounced > 0.0 || a.factor_lo != 1.0 || a.factor_hi != 1.0;
+  Stream ga{};
+  if (policy) {
+    Entropy run3{}, spawn3{};
+    push_words(run3, a.trial_seed);
+    push_words(spawn3, pid);
+    push_words(spawn3, 4u);
+    uint32_t k4[4];
+    seed_sequence(run3, spawn3, k4, 4);
+    ga.key0 = (uint64_t)k4[0] | ((uint64_t)k4[1] << 32);
+    ga.key1 = (uint64_t)k4[2] | ((uint64_t)k4[3] << 32);
+    ga.pos = 4;
+  }
   const double w = a.params[i * NP + PW];
   const double dt = a.dt_s, period = a.period_s, horizon = a.horizon_s;
   int32_t* mks = a.meal_ks + i * GT_NY_MEALS;
@@ -217,11 +236,20 @@ __global__ void northern_kernel(const gt_northern_args a) {
           if (ev.cls >= 0) {
             const double end = start + kMealDurS;
             const double mag = kChoPerKg[ev.cls] * w;
+            // apply_announcement_policy (protocol.py:373-394), every meal of the
+            // year in compose order: Generator.random() < fraction -> unannounced,
+            // else magnitude * (lo if lo == hi else Generator.uniform(lo, hi))
+            double ann = mag;
+            if (policy) {
+              if (ga.next_double() < a.fraction_unannounced) ann = 0.0;
+              else ann = mag * (a.factor_lo == a.factor_hi ? a.factor_lo
+                                                           : a.factor_lo + (a.factor_hi - a.factor_lo) * ga.next_double());
+            }
             mks[nm] = in_h ? (int32_t)ceil(start / dt) : INT_MAX;
             mke[nm] = in_h ? (int32_t)ceil(end / dt) : INT_MAX;
             mkp[nm] = in_h ? (int32_t)floor(start / period) : INT_MAX;
             mrate[nm] = in_h ? mag / ((end - start) / 60.0) : 0.0;
-            mann[nm] = in_h ? mag : 0.0;
+            mann[nm] = in_h ? ann : 0.0;
             ++nm; nm_h += in_h;
           } else {
             const double end = start + kExDurS;

@@ -273,7 +273,7 @@ def launch_fast(inputs: dict, outs: FastOutputs, sz: dict, dt_s: float, period_s
 
 
 def northern_csr(params, pid0: int, trial_seed: int, dt_s: float, period_s: float, horizon_s: float,
-                 device, week_days: bool = False) -> dict:
+                 device, week_days: bool = False, announcement=None) -> dict:
     """Device NorthernYearProtocol in the fused kernel's CSR layout (fixed
     stride GT_NY_MEALS / GT_NY_EX per patient; see include/glucosim.h).
     Returns the CSR dict of FastTrial plus ``n_meals`` / ``n_ex`` (events
@@ -303,6 +303,9 @@ def northern_csr(params, pid0: int, trial_seed: int, dt_s: float, period_s: floa
               "ex_hrr", "ex_announced", "n_meals", "n_ex"):
         setattr(a, k, ptr(out[k]))
     a.week_days = ptr(out.get("week_days"))
+    frac, (lo, hi) = (0.0, (1.0, 1.0)) if announcement is None else (
+        float(announcement.fraction_unannounced), tuple(float(v) for v in announcement.misannouncement_factor_range))
+    a.fraction_unannounced, a.factor_lo, a.factor_hi = frac, lo, hi
     check(_lib.load().gt_northern_protocol(C.byref(a), stream_ptr(device)), "gt_northern_protocol")
     return out
 

@@ -174,11 +174,10 @@ class NorthernYearProtocol:
         return proto
 
     def on_device(self) -> bool:
-        """The device builder (csrc/gt_northern.cu) covers the default
-        announcement policy and the bundled basis days."""
-        pol = self.announcement
-        return (self.basis_days_path is None and pol.fraction_unannounced == 0.0
-                and tuple(pol.misannouncement_factor_range) == (1.0, 1.0))
+        """The device builder (csrc/gt_northern.cu) covers the bundled basis
+        days with any announcement policy (drawn from the reference's own
+        stream(trial_seed, pid, ROLE_ANNOUNCEMENT))."""
+        return self.basis_days_path is None
 
     def describe(self) -> dict:
         return {"kind": "northern_year",

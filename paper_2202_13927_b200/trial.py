@@ -97,7 +97,7 @@ class FastTrial:
         if isinstance(generator, NorthernYearProtocol) and generator.on_device():
             # planned on the device from the reference's own keyed stream
             csr = engine.northern_csr(self.params, self.pid0, cfg.seed, cfg.dt_s, cfg.controller_period_s,
-                                      cfg.horizon_s, self.device)
+                                      cfg.horizon_s, self.device, announcement=generator.announcement)
             if bool((csr["n_meals"] < 0).any()):
                 raise SimulationError("NorthernYear week plan failed (no admissible day order)")
             return csr

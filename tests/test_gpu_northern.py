@@ -81,3 +81,57 @@ def test_fused_trial_on_device_northern_equals_host_csr(dev):
         accs.append(ft.accumulator())
     ra, rb = (analytics.report_bytes(analytics.build_trial_report(a, {})) for a in accs)
     assert ra == rb and np.array_equal(accs[0].metric_hist, accs[1].metric_hist)
+
+
+@pytest.mark.parametrize("frac,lo,hi", [(0.3, 0.8, 1.2), (0.0, 0.9, 0.9), (1.0, 1.0, 1.0), (0.05, 1.0, 1.5)])
+def test_device_announcement_policy_equals_host(dev, frac, lo, hi):
+    """The announcement policy (protocol.py:373-394) applied on the device
+    from the reference's own stream(trial_seed, pid, ROLE_ANNOUNCEMENT):
+    announced carbs of every meal equal the host path (numpy Generator)."""
+    import torch
+    from paper_2202_13927_b200 import engine, northern
+    from paper_2202_13927_b200.protocol import compile_protocol, compile_ticks
+    n, days, dt_s, trial_seed, pid0 = 24, 364, 60.0, 11, 500
+    rs = np.random.default_rng(3)
+    params = np.zeros((n, 30))
+    params[:, 0] = rs.uniform(30.0, 120.0, n)
+    pol = northern.AnnouncementPolicy(fraction_unannounced=frac, misannouncement_factor_range=(lo, hi))
+    gen = northern.NorthernYearProtocol(announcement=pol)
+    assert gen.on_device()
+    csr = engine.northern_csr(engine.dev(params, torch.float64, dev), pid0, trial_seed, dt_s, 300.0,
+                              days * 86400.0, dev, announcement=pol)
+    ann = csr["meal_ann"].cpu().numpy()
+    for i in range(n):
+        pa = compile_protocol(gen.build(trial_seed, _P(pid0 + i, float(params[i, 0]))), days * 86400.0)
+        ta = compile_ticks(pa, dt_s, 300.0)
+        m0 = i * 1588
+        assert np.array_equal(ann[m0:m0 + ta.meal_ann.size], ta.meal_ann), i
+    if frac == 1.0:
+        assert not ann.any()
+
+
+def test_fused_trial_with_announcement_policy_on_device(dev):
+    """A fused trial under a non-default policy planned on the device equals
+    the one on the host-compiled schedule, report bytes included."""
+    from paper_2202_13927_b200 import analytics
+    from paper_2202_13927_b200.config import SimulationConfig
+    from paper_2202_13927_b200.controller import ControllerHyperparameters
+    from paper_2202_13927_b200.northern import AnnouncementPolicy, NorthernYearProtocol
+    from paper_2202_13927_b200.population import generate_population
+    from paper_2202_13927_b200.trial import FastTrial
+    cfg = SimulationConfig(horizon_s=9 * 86400.0, seed=6, dt_s=60.0)
+    pop = generate_population(4, 64, device=dev, on_exhausted="redraw_weight")
+    pol = AnnouncementPolicy(fraction_unannounced=0.25, misannouncement_factor_range=(0.7, 1.3))
+
+    class HostOnly(NorthernYearProtocol):
+        def on_device(self):
+            return False
+
+    accs = []
+    for gen in (NorthernYearProtocol(announcement=pol), HostOnly(announcement=pol)):
+        ft = FastTrial(0, pop.params_device, pop.basal_device, gen, ControllerHyperparameters(), cfg,
+                       device=dev, per_patient_metrics=True)
+        ft.step()
+        accs.append(ft.accumulator())
+    ra, rb = (analytics.report_bytes(analytics.build_trial_report(a, {})) for a in accs)
+    assert ra == rb
