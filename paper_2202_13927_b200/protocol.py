@@ -210,6 +210,12 @@ class ThreeMealProtocol:
                 "sd_g": self.sd_g, "jitter_s": self.jitter_s, "duration_s": self.duration_s,
                 "days": self.days}
 
+    @classmethod
+    def from_spec(cls, spec: dict) -> "ThreeMealProtocol":
+        """Inverse of describe() (trial records, records.generator_from_spec)."""
+        return cls(clock_s=tuple(spec["clock_s"]), mean_g=tuple(spec["mean_g"]), sd_g=spec["sd_g"],
+                   jitter_s=spec["jitter_s"], duration_s=spec["duration_s"], days=spec["days"])
+
     def device_spec(self) -> dict:
         return {"clock_s": tuple(float(c) for c in self.clock_s),
                 "mean_g": tuple(float(m) for m in self.mean_g), "sd_g": float(self.sd_g),

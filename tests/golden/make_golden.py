@@ -429,6 +429,38 @@ def hypo_fixtures():
                 prof=pp, make_ctl=lambda basal: PIDController(pp, 1.8 * basal))
 
 
+def record_fixture():
+    """The reference's own record round trip (storage.py:234-312; its test
+    test_storage.py:181-199) on a cohort of 6, a 2-day NorthernYear trial with a
+    NON-default announcement policy: the record, and the report its rerun
+    reproduces.  The product's records.rerun_trial must give the same bytes."""
+    import tempfile
+    from glucotrial.protocol import AnnouncementPolicy as RefPolicy
+    from glucotrial.storage import Store, TrialRecord, rerun_trial as ref_rerun
+    e101, _ = generate_population(seed=101, n=12)
+    prof = load_profile()
+    cfg = SimulationConfig(horizon_s=2 * DAY, seed=21)
+    gen = NorthernYearProtocol(announcement=RefPolicy(fraction_unannounced=0.2,
+                                                      misannouncement_factor_range=(0.8, 1.2)))
+    with tempfile.TemporaryDirectory() as d:
+        store = Store(d)
+        store.save_cohort("pop-a", e101[:6])
+        res = run_trial(e101[:6], gen, "dual_hormone", prof, "hovorka_ext", cfg, workers=1, basal_scale=1.0,
+                        run_meta={"trial_id": "trial-x", "population_ref": "pop-a"})
+        h = store.save_profile(prof)
+        rec = TrialRecord.create(trial_id="trial-x", seed=cfg.seed, model_id="hovorka_ext",
+                                 controller_id="dual_hormone", profile_hash=h, population_ref="pop-a",
+                                 protocol_generator=gen.describe(), basal_scale=1.0, config=cfg.to_dict())
+        fresh = ref_rerun(store, rec)
+        assert report_bytes(fresh.report) == report_bytes(res.report)
+    d = rec.to_dict()
+    d["created_at"] = "2026-01-01T00:00:00+00:00"   # fixed for a reproducible fixture
+    with open(os.path.join(HERE, "record_rerun.json"), "w") as fh:
+        json.dump(d, fh, indent=1, sort_keys=True)
+    with open(os.path.join(HERE, "report_rerun.json"), "wb") as fh:
+        fh.write(report_bytes(res.report))
+
+
 def main():
     if "--only-pid" in sys.argv:
         pid_fixtures()
@@ -439,11 +471,15 @@ def main():
     if "--only-pop4k" in sys.argv:
         population_4000_fixture()
         return
+    if "--only-record" in sys.argv:
+        record_fixture()
+        return
     if "--only-flops" in sys.argv:
         flop_fixture()
         return
     pop = population_fixture()
     population_4000_fixture()
+    record_fixture()
     flop_fixture()
     steady_fixture(pop)
     drift_fixture(pop)

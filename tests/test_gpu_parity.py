@@ -304,3 +304,35 @@ def test_unsupported_model_or_controller_raises(dev):
         run_trial(e, ThreeMealProtocol(), "pid_mpc", ControllerHyperparameters(), "hovorka_ext", cfg, device=dev)
     with pytest.raises(SimulationError):
         run_trial([], ThreeMealProtocol(), "dual_hormone", ControllerHyperparameters(), "hovorka_ext", cfg, device=dev)
+
+
+def test_rerun_trial_record_reproduces_reference_report(dev):
+    """records.rerun_trial on a record the REFERENCE wrote (storage.py:234-312,
+    golden record_rerun.json; NorthernYear with a non-default announcement
+    policy) reproduces the reference's report bytes -- both with the
+    population passed directly and through a store-like object."""
+    from paper_2202_13927_b200 import analytics, records
+    from paper_2202_13927_b200.controller import ControllerHyperparameters
+    from paper_2202_13927_b200.layout import PARAM_NAMES
+    from paper_2202_13927_b200.population import ParameterSet, Patient
+    rec = records.TrialRecord.from_dict(json.loads(golden_bytes("record_rerun.json")))
+    case = SimCase("sim_northern_dt30.npz")       # the same seed-101 cohort
+    entries = [(Patient(int(case.ids[i]), float(case.params[i, 0])),
+                ParameterSet(values=dict(zip(PARAM_NAMES, (float(v) for v in case.params[i]))),
+                             u_basal_u_per_h=float(case.basal[i]))) for i in range(6)]
+    prof = ControllerHyperparameters()
+    want = golden_bytes("report_rerun.json")
+    res = records.rerun_trial(entries, rec, profile=prof, device=dev)
+    assert analytics.report_bytes(res.report) == want
+
+    class Store:
+        def load_cohort(self, ref):
+            assert ref == "pop-a"
+            return entries
+
+        def load_profile(self, h):
+            assert h == prof.content_hash()
+            return prof
+
+    res = records.rerun_trial(Store(), rec, device=dev)
+    assert analytics.report_bytes(res.report) == want
