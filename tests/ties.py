@@ -38,6 +38,9 @@ RANGE_BOUNDS = np.array([3.0, 3.9, 10.0, 13.9])                # analytics.py:21
 EDGES = np.union1d(THRESHOLDS, RANGE_BOUNDS)
 REL_TIE = 1e-12     # "within rounding": ~4500 ulp, far below any physiological scale
 REL_DRIFT = 1e-9    # north_star's trajectory tolerance
+CTL_ATOL = 1e-12    # U/h, U, ug: a controller output this close is the same decision.  Outputs computed
+                    # from a cancellation (filt - setpoint, a clamp near 0) differ by ~1e-14 in absolute
+                    # terms between runs 1e-15 apart, which a purely relative test would call a divergence
 
 
 @dataclass
@@ -128,7 +131,8 @@ def first_divergence(tr_ref: np.ndarray, tr_fast: np.ndarray):
     bin_f = np.searchsorted(THRESHOLDS, bg_f, side="right")
     rng_r = np.searchsorted(RANGE_BOUNDS, bg_r, side="right")
     rng_f = np.searchsorted(RANGE_BOUNDS, bg_f, side="right")
-    ctl = np.any(_rel(tr_ref[:, 5:8], tr_fast[:, 5:8]) > REL_TIE, axis=1)
+    dc = np.abs(tr_ref[:, 5:8] - tr_fast[:, 5:8])
+    ctl = np.any(dc > REL_TIE * np.maximum(np.abs(tr_ref[:, 5:8]), np.abs(tr_fast[:, 5:8])) + CTL_ATOL, axis=1)
     drift = _rel(bg_r, bg_f) > REL_DRIFT
     flag = (bin_r != bin_f) | (rng_r != rng_f) | ctl | drift
     k = np.flatnonzero(flag)
@@ -161,7 +165,7 @@ def classify(oracle, pi: PatientInputs, tr_ref: np.ndarray, tr_fast: np.ndarray,
         fast_out = tr_fast[: k + 1: ps, 5:8]
         # the oracle replay of the reference readings is the reference run itself
         assert np.array_equal(rep_r, ref_out), f"patient {patient}: controller replay broken"
-        if not np.allclose(rep_f, fast_out, rtol=REL_TIE, atol=0):
+        if not np.allclose(rep_f, fast_out, rtol=REL_TIE, atol=CTL_ATOL):
             raise AssertionError(f"patient {patient}: fused controller output at tick {k} "
                                  f"{fast_out[-1]} is not the reference controller's on the same readings "
                                  f"{rep_f[-1]}")
