@@ -97,6 +97,9 @@ namespace gt {
 #ifndef GT_KLOOP
 #define GT_KLOOP 1  // plain-step loop over the tick index itself
 #endif
+#ifndef GT_EXFOLD
+#define GT_EXFOLD 1  // exercise input h/tau_hr * HRR folded per session (one DMUL less per step on CSR)
+#endif
 #ifndef GT_FAST_MINB
 #define GT_FAST_MINB 4  // resident 128-thread blocks per SM (register budget 128)
 #endif
@@ -646,9 +649,11 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
     // the cursor in shared memory moves only when a session ends
     int32_t ex_ks_c = INT_MAX, ex_ke_c = INT_MAX;
     double ex_hrr_c = 0.0;
+    R ex_e1_c = 0;   // GT_EXFOLD: h/tau_hr * HRR of the current session, folded at session change
     auto load_session = [&](int p) {
       if (p < n_ex) { ex_ks_c = a.ex_ks[ex_lo + p]; ex_ke_c = a.ex_ke[ex_lo + p]; ex_hrr_c = a.ex_hrr[ex_lo + p]; }
       else { ex_ks_c = ex_ke_c = INT_MAX; ex_hrr_c = 0.0; }
+      ex_e1_c = (R)(u.bE1 * ex_hrr_c);
     };
     if (HAS_EX) load_session(sil[(SI_EXPTR) * kFastBS]);
     // warp-uniform cursors derived from the slice start
@@ -747,7 +752,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           load_session(p);
         }
         ex_active = k >= ex_ks_c;   // (k < ex_ke_c here)
-        hrr = ex_active ? ex_hrr_c : 0.0;
+        if (!GT_EXFOLD || TRACE) hrr = ex_active ? ex_hrr_c : 0.0;
       }
       // controller tick (_kernel.py:98-135): the check, the announcement and
       // the reading here.  Under kLateControl the controller itself runs
@@ -1016,7 +1021,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       if (HAS_EX) {
         const R nE2 = FMR(E2, (R)u.aE2, E1 * (R)u.bE2);
         const R nE3 = FMR(E3, (R)u.aE3, E1 * (R)u.bE3);
-        E1 = FMR(E1, (R)u.aE1, (R)(u.bE1 * hrr));
+        E1 = FMR(E1, (R)u.aE1, GT_EXFOLD ? (ex_active ? ex_e1_c : (R)0) : (R)(u.bE1 * hrr));
         E2 = nE2; E3 = nE3;
       }
       G = FMR(G, (R)u.aS, bgR * (R)u.hS);
