@@ -68,7 +68,10 @@ struct Straggler {
   double w;
 };
 
-__global__ void __launch_bounds__(128) sampler_kernel(gt_sampler_args a, unsigned long long* queue,
+#ifndef GT_SAMPLER_MINB
+#define GT_SAMPLER_MINB 1
+#endif
+__global__ void __launch_bounds__(128, GT_SAMPLER_MINB) sampler_kernel(gt_sampler_args a, unsigned long long* queue,
                                                       Straggler* park, unsigned int* n_park, int park_cap) {
   const int lane = threadIdx.x & 31;
   const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
