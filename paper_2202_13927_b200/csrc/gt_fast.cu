@@ -104,6 +104,9 @@ namespace gt {
 #define GT_RINT 1   // instances (GT_PS5 bits) testing the near-edge bin as |t10 - rint(t10)| <= 1e-4:
                     // -0.7 % three_meal/pid_pump, +1.1 % three_meal/dual_hormone (profiles/r02_ab_code_shape.json)
 #endif
+#ifndef GT_DRAIN32
+#define GT_DRAIN32 6  // instances (GT_PS5 bits) forming the drain address from a 32-bit element offset
+#endif
 #ifndef GT_FAST_MINB
 #define GT_FAST_MINB 4  // resident 128-thread blocks per SM (register budget 128)
 #endif
@@ -1069,7 +1072,12 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           // column address is formed only on that path
           if (__builtin_expect(c == 255u, 0)) {
             asm volatile("st.shared.u8 [%0], 0;" :: "r"(ha) : "memory");
-            if (kb < GT_N_BG_BINS && inrange) atomicAdd(a.bg_hist + ((int64_t)kb * n + i), 255);
+            if (kb < GT_N_BG_BINS && inrange) {
+              // 32-bit element offset (the launcher bounds 247 n < 2^31): the drain
+              // path then needs fewer scratch registers than a 64-bit index
+              if (GT_DRAIN32 & kShapeBit) atomicAdd(a.bg_hist + (uint32_t)(kb * (uint32_t)n + (uint32_t)i), 255);
+              else atomicAdd(a.bg_hist + ((int64_t)kb * n + i), 255);
+            }
           }
         }
         bg_sum += bg;
@@ -1424,6 +1432,10 @@ int gt_launch_fast(const gt_fast_args* a, cudaStream_t st) {
                    "controller period apart, lasting >= one step, and dt >= 2 s");
       return GT_EUNSUPPORTED;
     }
+  }
+  if (a->n * (int64_t)GT_N_BG_BINS > (int64_t)INT32_MAX) {  // the histogram drain's 32-bit element offsets
+    gt_set_error("gt_simulate_fast: too many patients for one launch (247 n must fit 31 bits); shard the population");
+    return GT_EINVAL;
   }
   if ((a->n + 31) / 32 > INT32_MAX / 8) {
     gt_set_error("gt_simulate_fast: too many patients for one launch; shard the population");
