@@ -539,3 +539,33 @@ def test_tie_classifier_runners_on_device(dev, oracle, name, controller):
         assert np.array_equal(_h(outs.hypo_events)[:, 0], case.g["hypo"][sub["idx"][j]])
         assert ties.first_divergence(tr_r, tr_f) is None
         assert np.allclose(tr_f[:ticks, 1], tr_r[:ticks, 1], rtol=1e-9, atol=0)
+
+
+@pytest.mark.parametrize("controller", ["dual_hormone", "pid_pump"])
+def test_hypo_runs_across_slices(dev, controller):
+    """Hypoglycaemia runs carried across horizon slices (saved lane state):
+    an insulin-overdosed population (assumed basal x 2.6) has many events,
+    and their counts -- with every other output -- are identical for 1, 5 and
+    13 slices."""
+    import torch
+    from paper_2202_13927_b200.config import SimulationConfig
+    from paper_2202_13927_b200.controller import ControllerHyperparameters
+    from paper_2202_13927_b200.pid import PIDProfile
+    from paper_2202_13927_b200.population import generate_population
+    from paper_2202_13927_b200.protocol import ThreeMealProtocol
+    from paper_2202_13927_b200.trial import FastTrial
+    cfg = SimulationConfig(horizon_s=9 * 86400.0, seed=14, dt_s=60.0)
+    pop = generate_population(6, 160, device=dev, on_exhausted="redraw_weight")
+    prof = PIDProfile() if controller == "pid_pump" else ControllerHyperparameters()
+    basal = pop.basal_device * (1.8 if controller == "pid_pump" else 2.6)
+    runs = []
+    for s in (1, 5, 13):
+        ft = FastTrial(0, pop.params_device, basal, ThreeMealProtocol(), prof, cfg, controller_id=controller,
+                       device=dev, n_slices=s, per_patient_metrics=True)
+        ft.step()
+        runs.append(ft)
+    h0 = _h(runs[0].outs.hypo_events)
+    assert h0[0].sum() >= 100 and h0[1].sum() >= 10, h0.sum(axis=1)
+    for ft in runs[1:]:
+        for k in ("status", "bg_hist", "bg_stats", "hypo_events", "day_dose"):
+            assert torch.equal(getattr(ft.outs, k), getattr(runs[0].outs, k)), k
