@@ -114,7 +114,15 @@ static __device__ double brentq_flux(double xa, double xb, double xtol, double r
 }
 
 // hovorka.py:201-243 steady_state.  Returns true on success.
-static __device__ bool steady_state_dev(const double* p, double target_bg, double* x, double* u_basal_uh) {
+#ifndef GT_SS_NOINLINE
+#define GT_SS_NOINLINE 0
+#endif
+#if GT_SS_NOINLINE
+static __device__ __noinline__
+#else
+static __device__
+#endif
+bool steady_state_dev(const double* p, double target_bg, double* x, double* u_basal_uh) {
   if (!(target_bg > 0)) return false;
   const double w = p[PW];
   if (net_flux(0.0, target_bg, p) <= 0.0) return false;

@@ -57,9 +57,13 @@ __device__ __forceinline__ double sampled_value(const gt_sampler_args& a, int j,
 // attempts 128 at a time with a whole block instead of one lane.
 constexpr int kPark = 384;
 #ifndef GT_SAMPLER_CAP
-#define GT_SAMPLER_CAP 4   // measured best of 1,2,3,4,8,12,16 (tools/ab_sampler.sh)
+#define GT_SAMPLER_CAP 1   // with solve batching: 1 ~ 2 ~ 8 (tools/ab_sampler.sh); 4 was best without
 #endif
 constexpr int kCap = GT_SAMPLER_CAP;   // cheap attempts per lane per round
+#ifndef GT_SAMPLER_BATCH
+#define GT_SAMPLER_BATCH 24
+#endif
+constexpr int kBatch = GT_SAMPLER_BATCH;  // lanes holding a survivor before the warp solves
 constexpr int kMaxSampled = 16;
 struct Straggler {
   int64_t i;
@@ -81,6 +85,7 @@ __global__ void __launch_bounds__(128, GT_SAMPLER_MINB) sampler_kernel(gt_sample
   int32_t attempt = 0, total = 0, wdraw = 0, last_surv = -1;
   uint32_t wctr = 0, pid = 0;
   bool park_full = false;
+  bool survivor = false;   // holds a cheap-rule survivor awaiting its solve (phase 2)
   long long rej_neg = 0, rej_sd = 0, rej_ss = 0, rej_basal = 0;
   bool drained = false;
   auto draw_weight = [&]() {             // population.py:148-153
@@ -125,8 +130,7 @@ __global__ void __launch_bounds__(128, GT_SAMPLER_MINB) sampler_kernel(gt_sample
     // ---- phase 1: cheap rules until a survivor, at most kCap attempts this
     // round (a lane without a survivor skips phase 2 and continues next round:
     // the warp never waits for one lane's long rejection chain)
-    bool survivor = false;
-    if (i >= 0) {
+    if (i >= 0 && !survivor) {
       for (int c = 0; c < kCap && !survivor && i >= 0; ++c) {
         if (attempt >= a.max_attempts || !(w > 0.0)) {
           // budget spent for this body weight: redraw it or fail
@@ -167,8 +171,14 @@ __global__ void __launch_bounds__(128, GT_SAMPLER_MINB) sampler_kernel(gt_sample
         survivor = true;
       }
     }
-    // ---- phase 2: the survivors' lognormal draws and steady-state solves
-    if (survivor) {
+    // ---- phase 2: the survivors' lognormal draws and steady-state solves, once
+    // enough lanes hold one (kBatch) or every lane still working does, so the
+    // solves run with most of the warp converged on them
+    const unsigned hold = __ballot_sync(0xffffffffu, survivor);
+    const unsigned busy = __ballot_sync(0xffffffffu, i >= 0);
+    const bool go = __popc(hold) >= kBatch || hold == busy;
+    if (survivor && go) {
+      survivor = false;
       const uint32_t actr = (uint32_t)(total + attempt);
 #pragma unroll
       for (int q = 0; q < kMaxSampled; q += 2) {
