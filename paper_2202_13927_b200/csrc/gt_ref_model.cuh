@@ -51,28 +51,35 @@ __device__ __forceinline__ void drift_ref(const double* x, const double* u, cons
 }
 
 // ------------------------------------------------------------ steady state
-// hovorka.py:183-198 _net_glucose_flux_at
-static __device__ double net_flux(double ic, double bg, const double* p) {
-  const double w = p[PW];
-  const double q1 = bg * p[PVG] * w;
-  const double x1 = p[PSIT] * ic;
-  const double x2 = p[PSID] * ic;
-  const double x3 = p[PSIE] * ic;
-  const double q2 = x1 * q1 / (p[PK12] + x2);
-  const double f01c = bg < 4.5 ? p[PF01] * w * bg / 4.5 : p[PF01] * w;
-  const double renal = bg > 9.0 ? 0.003 * (bg - 9.0) * p[PVG] * w : 0.0;
-  const double v = p[PEGP0] * w * (1.0 - x3);
-  const double egp = v > 0.0 ? v : 0.0;  // python max(0.0, v)
-  return -f01c - x1 * q1 + p[PK12] * q2 - renal + egp;
-}
+// hovorka.py:183-198 _net_glucose_flux_at, with the terms that do not depend
+// on the insulin concentration evaluated once per solve (same operations, same order, same values: the
+// hoisted products are the left-most factors of the reference's expressions)
+struct NetFlux {
+  double q1, f01c, renal, egpw, k12, sit, sid, sie;
+  __device__ explicit NetFlux(double bg, const double* p) {
+    const double w = p[PW];
+    q1 = bg * p[PVG] * w;
+    f01c = bg < 4.5 ? p[PF01] * w * bg / 4.5 : p[PF01] * w;
+    renal = bg > 9.0 ? 0.003 * (bg - 9.0) * p[PVG] * w : 0.0;
+    egpw = p[PEGP0] * w;
+    k12 = p[PK12]; sit = p[PSIT]; sid = p[PSID]; sie = p[PSIE];
+  }
+  __device__ double operator()(double ic) const {
+    const double x1 = sit * ic, x2 = sid * ic, x3 = sie * ic;
+    const double q2 = x1 * q1 / (k12 + x2);
+    const double v = egpw * (1.0 - x3);
+    const double egp = v > 0.0 ? v : 0.0;
+    return -f01c - x1 * q1 + k12 * q2 - renal + egp;
+  }
+};
 
 // scipy/optimize/Zeros/brentq.c (Brent's method), restated.  err: 0 ok.
 static __device__ double brentq_flux(double xa, double xb, double xtol, double rtol, int iter,
-                              double bg, const double* p, int* err) {
+                                     const NetFlux& f, int* err) {
   double xpre = xa, xcur = xb, xblk = 0., fpre, fcur, fblk = 0., spre = 0., scur = 0., sbis;
   double delta, stry, dpre, dblk;
-  fpre = net_flux(xpre, bg, p);
-  fcur = net_flux(xcur, bg, p);
+  fpre = f(xpre);
+  fcur = f(xcur);
   *err = 0;
   if (isnan(fpre) || isnan(fcur)) { *err = 3; return 0.0; }
   if (fpre == 0) return xpre;
@@ -106,7 +113,7 @@ static __device__ double brentq_flux(double xa, double xb, double xtol, double r
     xpre = xcur; fpre = fcur;
     if (fabs(scur) > delta) xcur += scur;
     else xcur += (sbis > 0 ? delta : -delta);
-    fcur = net_flux(xcur, bg, p);
+    fcur = f(xcur);
     if (isnan(fcur)) { *err = 3; return 0.0; }
   }
   *err = 2;
@@ -125,16 +132,17 @@ static __device__
 bool steady_state_dev(const double* p, double target_bg, double* x, double* u_basal_uh) {
   if (!(target_bg > 0)) return false;
   const double w = p[PW];
-  if (net_flux(0.0, target_bg, p) <= 0.0) return false;
+  const NetFlux f(target_bg, p);
+  if (f(0.0) <= 0.0) return false;
   double lo = 0.0, hi = 50.0;
   bool found = false;
   for (int k = 0; k < 30; ++k) {
-    if (net_flux(hi, target_bg, p) < 0.0) { found = true; break; }
+    if (f(hi) < 0.0) { found = true; break; }
     lo = hi; hi = hi * 2.0;
   }
   if (!found) return false;
   int err = 0;
-  const double ic = brentq_flux(lo, hi, 1e-14, 8.9e-16, 200, target_bg, p, &err);
+  const double ic = brentq_flux(lo, hi, 1e-14, 8.9e-16, 200, f, &err);
   if (err) return false;
   const double u_basal_mU_min = ic * p[PKE] * p[PVI] * w;
   for (int k = 0; k < GT_N_STATES; ++k) x[k] = 0.0;
