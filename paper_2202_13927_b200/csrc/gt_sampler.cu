@@ -37,24 +37,24 @@ __device__ __forceinline__ double sampled_value(const gt_sampler_args& a, int j,
 // Persistent, warp-cooperative rejection sampler.  Each lane holds one
 // patient at a time and takes the next from a global queue (one atomic per
 // warp refill) when it finishes, so no lane idles while a neighbour works
-// through a long rejection chain.  A round has two phases:
-//   1. cheap rules: a lane draws only the normal values of its next attempts
-//      (3 of the 7 Philox blocks) and applies the reference's first two
-//      rules -- any value negative (lognormals never are), a normal draw
-//      outside 1 SD (85 % of all rejections) -- until an attempt survives or
-//      the attempt budget runs out;
-//   2. the steady-state solve (brentq) of every lane's survivor, with the
-//      lognormal values drawn only now; then the u_basal rule.
-// Every lane of the warp reaches phase 2 with a survivor in hand, so the
-// expensive solves run converged instead of one lane at a time.  The draws
-// and the order of the rules are the reference's (population.py:217-259),
-// so the population is bit-identical to the one-thread-per-patient loop
-// (oracle_sample_patients, tests/test_gpu_sampler.py).
+// through a long rejection chain.  Each round:
+//   1. cheap rules: a lane without a pending survivor draws only the normal
+//      values of its next attempt (3 of the 7 Philox blocks) and applies the
+//      reference's first two rules -- any value negative (lognormals never
+//      are), a normal draw outside 1 SD (85 % of all rejections);
+//   2. once kBatch lanes hold a survivor (or every lane still working does),
+//      those lanes draw the survivor's lognormal values and run the
+//      steady-state solve (brentq) together, then the u_basal rule.
+// A lane keeps its survivor across rounds until the batch fills, so the
+// expensive solves run with most of the warp converged.  The draws are
+// counter-addressed and the rules are applied in the reference's order
+// (population.py:217-259), so the population is bit-identical to the
+// one-thread-per-patient loop (oracle_sample_patients, tests/test_gpu_sampler.py).
 // A patient still without an accepted set after kPark attempts of one body
-// weight (a feasible weight needs more than 384 with probability ~1e-5; a
-// weight below ~30 kg never succeeds and spends the whole 10 000-attempt
-// budget) is handed to straggler_kernel, which searches its remaining
-// attempts 128 at a time with a whole block instead of one lane.
+// weight (~0.5 % of patients: light weights have low acceptance; a weight
+// below ~30 kg never succeeds and spends the whole 10 000-attempt budget) is
+// handed to straggler_kernel, which searches its remaining attempts 128 at a
+// time with a whole block instead of one lane.
 constexpr int kPark = 384;
 #ifndef GT_SAMPLER_CAP
 #define GT_SAMPLER_CAP 1   // with solve batching: 1 ~ 2 ~ 8 (tools/ab_sampler.sh); 4 was best without
