@@ -598,7 +598,8 @@ def run_trial1m(args):
         t0 = time.perf_counter()
         pop = generate_population(2, hi - lo, pid0=lo, device=device, on_exhausted="redraw_weight")
         ft = FastTrial(lo, pop.params_device, pop.basal_device, ThreeMealProtocol(), prof, cfg,
-                       controller_id=args.controller, device=device, per_patient_metrics=True)
+                       controller_id=args.controller, device=device, per_patient_metrics=True,
+                       x0=pop.x0_device if pop.target_bg == cfg.initial_bg_mmol_per_l else None)
         ft.step()
         acc = ft.accumulator()
         if ws > 1:

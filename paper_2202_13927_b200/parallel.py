@@ -136,7 +136,8 @@ def run_trial_sharded(n_total: int, population_seed: int, generator, controller_
     lo, hi = shard_range(n_total, rank, world)
     pop = generate_population(population_seed, hi - lo, pid0=lo, device=device, on_exhausted="redraw_weight")
     ft = FastTrial(lo, pop.params_device, pop.basal_device, generator, profile, config, controller_id,
-                   device, hypo_min_s=hypo_min_s, per_patient_metrics=gather_metrics)
+                   device, hypo_min_s=hypo_min_s, per_patient_metrics=gather_metrics,
+                   x0=pop.x0_device if pop.target_bg == config.initial_bg_mmol_per_l else None)
     ft.step()
     acc = allreduce_accumulator(ft.accumulator(), device, group)
     metrics = gather_per_patient(ft.metrics(), lo, n_total, device, group) if gather_metrics else None

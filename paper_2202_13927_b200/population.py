@@ -56,7 +56,7 @@ class DevicePopulation:
     """A device-resident population shard (ids pid0 .. pid0+n-1)."""
 
     def __init__(self, pid0, params_device, basal_device, x0_device, stats: SamplingStats,
-                 attempts_device=None, max_attempts: int = tables.MAX_ATTEMPTS):
+                 attempts_device=None, max_attempts: int = tables.MAX_ATTEMPTS, target_bg: float = 6.0):
         self.pid0 = int(pid0)
         self.params_device = params_device
         self.basal_device = basal_device
@@ -64,6 +64,7 @@ class DevicePopulation:
         self.stats = stats
         self.attempts_device = attempts_device   # per patient, redraw rounds included
         self.max_attempts = int(max_attempts)
+        self.target_bg = float(target_bg)   # the steady state x0_device was solved at
 
     @property
     def n_weight_redraws(self) -> int:
@@ -116,7 +117,8 @@ def generate_population(seed: int, n: int, table=None, target_bg: float = 6.0, p
     st = SamplingStats(attempts=attempts, accepted=n, rejected_negative=int(rc[0]),
                        rejected_outside_sd=int(rc[1]), rejected_no_steady_state=int(rc[2]),
                        rejected_basal=int(rc[3]))
-    return DevicePopulation(pid0, out["params"], out["u_basal"], out["x0"], st, out["attempts"], max_attempts)
+    return DevicePopulation(pid0, out["params"], out["u_basal"], out["x0"], st, out["attempts"], max_attempts,
+                            target_bg)
 
 
 def validate_parameter_sets(params, u_basal, table=None, target_bg: float = 6.0, device=None) -> list:

@@ -53,7 +53,7 @@ class FastTrial:
     def __init__(self, pid0, params, basal, generator, profile, config, controller_id="dual_hormone",
                  device=None, hypo_min_s: float = 900.0, per_patient_metrics: bool = False,
                  seed: int | None = None, n_slices: int = 0, noise_agg: int = 1,
-                 fp32: bool = False):
+                 fp32: bool = False, x0=None):
         self.n_slices = int(n_slices)   # 0 = chosen by the launcher
         # BASELINE configs[4]: each step's Brownian increment aggregated from
         # noise_agg fine Philox increments (the path a dt/noise_agg run draws),
@@ -74,7 +74,13 @@ class FastTrial:
         self.hypo_min_ticks = max(1, int(np.ceil(hypo_min_s / config.dt_s)))
         self.generator = generator
         with t.cuda.device(self.device):
-            self.x0, _ub, self.ss_status = engine.steady_state(params, config.initial_bg_mmol_per_l, self.device)
+            if x0 is not None:
+                # the sampler's own steady states (same solve, same target BG): every
+                # sampled patient has one, so nothing is aborted at staging
+                self.x0 = x0
+                self.ss_status = t.zeros((self.n,), dtype=t.int32, device=self.device)
+            else:
+                self.x0, _ub, self.ss_status = engine.steady_state(params, config.initial_bg_mmol_per_l, self.device)
             self.c0 = engine.controller_init(self.hyper, icr_initial_factor(profile), basal, self.device)
             self.hyper_d = engine.dev(self.hyper, t.float64, self.device)
             self.fixed = engine.uniform_fixed(params)   # verified once, at staging

@@ -75,3 +75,26 @@ def test_straggler_path_bitwise(dev, oracle, max_attempts, n):
             assert int((o["attempts"] > 384).sum()) > 0       # the straggler kernel ran
         if max_attempts == 129 and redraws == 0:
             assert int((o["status"] != 0).sum()) > 0          # the failure path ran
+
+
+def test_sampler_steady_states_reused_by_the_trial(dev):
+    """FastTrial(x0=population.x0_device) skips the staging solve: the
+    sampler's steady states are the same solve at the same target BG, so the
+    trial's outputs are bit-identical."""
+    import torch
+    from paper_2202_13927_b200.config import SimulationConfig
+    from paper_2202_13927_b200.pid import PIDProfile
+    from paper_2202_13927_b200.population import generate_population
+    from paper_2202_13927_b200.protocol import ThreeMealProtocol
+    from paper_2202_13927_b200.trial import FastTrial
+    cfg = SimulationConfig(horizon_s=3 * 86400.0, seed=5, dt_s=60.0)
+    pop = generate_population(5, 300, device=dev, on_exhausted="redraw_weight")
+    runs = []
+    for x0 in (None, pop.x0_device):
+        ft = FastTrial(0, pop.params_device, pop.basal_device, ThreeMealProtocol(), PIDProfile(), cfg,
+                       controller_id="pid_pump", device=dev, per_patient_metrics=True, x0=x0)
+        ft.step()
+        runs.append(ft)
+    assert torch.equal(runs[0].x0, runs[1].x0)
+    for k in ("status", "bg_hist", "bg_stats", "hypo_events", "day_dose"):
+        assert torch.equal(getattr(runs[0].outs, k), getattr(runs[1].outs, k)), k
