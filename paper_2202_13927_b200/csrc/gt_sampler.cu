@@ -55,6 +55,16 @@ __device__ __forceinline__ double sampled_value(const gt_sampler_args& a, int j,
 // below ~30 kg never succeeds and spends the whole 10 000-attempt budget) is
 // handed to straggler_kernel, which searches its remaining attempts 128 at a
 // time with a whole block instead of one lane.
+// One attempt's values written into the packed parameter vector.
+__device__ void fill_attempt_p(const gt_sampler_args& a, uint32_t actr, uint32_t pid, uint32_t k0, uint32_t k1,
+                               double* p) {
+  for (int q = 0; q < a.n_sampled; q += 2) {
+    const U4 r = philox4x32_10(actr, pid, kRoleSamplerParams, (uint32_t)(q >> 1), k0, k1);
+    p[a.param_index[q]] = sampled_value(a, q, det_inv_norm(u52(r.x, r.y)));
+    if (q + 1 < a.n_sampled) p[a.param_index[q + 1]] = sampled_value(a, q + 1, det_inv_norm(u52(r.z, r.w)));
+  }
+}
+
 constexpr int kPark = 384;
 #ifndef GT_SAMPLER_CAP
 #define GT_SAMPLER_CAP 1   // with solve batching: 1 ~ 2 ~ 8 (tools/ab_sampler.sh); 4 was best without
@@ -79,7 +89,8 @@ __global__ void __launch_bounds__(128, GT_SAMPLER_MINB) sampler_kernel(gt_sample
                                                       Straggler* park, unsigned int* n_park, int park_cap) {
   const int lane = threadIdx.x & 31;
   const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
-  double p[GT_N_PARAMS], x[GT_N_STATES], vals[16];
+  // the attempt's values go straight into p (no separate value registers)
+  double p[GT_N_PARAMS], x[GT_N_STATES];
   double ub = 0.0, w = 0.0;
   int64_t i = -1;                       // this lane's patient (-1: none)
   int32_t attempt = 0, total = 0, wdraw = 0, last_surv = -1;
@@ -99,6 +110,12 @@ __global__ void __launch_bounds__(128, GT_SAMPLER_MINB) sampler_kernel(gt_sample
     attempt = 0;
   };
   auto finish = [&](int status) {
+    if (status != 0) {
+      // the sequential loop's last p holds the latest survivor's values (or the
+      // fixed ones if none survived); phase 1 wrote later attempts' normals
+      for (int j = 0; j < a.n_sampled; ++j) p[a.param_index[j]] = a.fixed_params[a.param_index[j]];
+      if (last_surv >= 0) fill_attempt_p(a, (uint32_t)last_surv, pid, k0, k1, p);
+    }
     for (int k = 0; k < GT_N_PARAMS; ++k) a.params[i * GT_N_PARAMS + k] = p[k];
     for (int k = 0; k < GT_N_STATES; ++k) a.x0[i * GT_N_STATES + k] = status == 0 ? x[k] : 0.0;
     a.u_basal_uh[i] = status == 0 ? ub : 0.0;
@@ -150,22 +167,21 @@ __global__ void __launch_bounds__(128, GT_SAMPLER_MINB) sampler_kernel(gt_sample
         }
         const uint32_t actr = (uint32_t)(total + attempt);
         // the normal draws only (lognormals are never negative and have no SD rule)
+        bool neg = false, outside = false;
+        auto check = [&](int j, double v) {
+          neg |= v < 0.0;
+          outside |= fabs(S_(v, a.a[j])) > a.b[j];
+          p[a.param_index[j]] = v;
+        };
 #pragma unroll
         for (int q = 0; q < kMaxSampled; q += 2) {
           if (q >= a.n_sampled) break;
           const bool n0 = a.kind[q] == 0, n1 = q + 1 < a.n_sampled && a.kind[q + 1] == 0;
           if (!(n0 || n1)) continue;
           const U4 r = philox4x32_10(actr, pid, kRoleSamplerParams, (uint32_t)(q >> 1), k0, k1);
-          if (n0) vals[q] = sampled_value(a, q, det_inv_norm(u52(r.x, r.y)));
-          if (n1) vals[q + 1] = sampled_value(a, q + 1, det_inv_norm(u52(r.z, r.w)));
+          if (n0) check(q, sampled_value(a, q, det_inv_norm(u52(r.x, r.y))));
+          if (n1) check(q + 1, sampled_value(a, q + 1, det_inv_norm(u52(r.z, r.w))));
         }
-        bool neg = false, outside = false;
-#pragma unroll
-        for (int j = 0; j < kMaxSampled; ++j)
-          if (j < a.n_sampled && a.kind[j] == 0) {
-            neg |= vals[j] < 0.0;
-            outside |= fabs(S_(vals[j], a.a[j])) > a.b[j];
-          }
         if (neg) { ++rej_neg; ++attempt; continue; }          // population.py:234-236
         if (outside) { ++rej_sd; ++attempt; continue; }       // population.py:237-244
         survivor = true;
@@ -186,12 +202,9 @@ __global__ void __launch_bounds__(128, GT_SAMPLER_MINB) sampler_kernel(gt_sample
         const bool l0 = a.kind[q] == 1, l1 = q + 1 < a.n_sampled && a.kind[q + 1] == 1;
         if (!(l0 || l1)) continue;
         const U4 r = philox4x32_10(actr, pid, kRoleSamplerParams, (uint32_t)(q >> 1), k0, k1);
-        if (l0) vals[q] = sampled_value(a, q, det_inv_norm(u52(r.x, r.y)));
-        if (l1) vals[q + 1] = sampled_value(a, q + 1, det_inv_norm(u52(r.z, r.w)));
+        if (l0) p[a.param_index[q]] = sampled_value(a, q, det_inv_norm(u52(r.x, r.y)));
+        if (l1) p[a.param_index[q + 1]] = sampled_value(a, q + 1, det_inv_norm(u52(r.z, r.w)));
       }
-#pragma unroll
-      for (int j = 0; j < kMaxSampled; ++j)
-        if (j < a.n_sampled) p[a.param_index[j]] = vals[j];
       last_surv = (int32_t)actr;
       if (!steady_state_dev(p, a.target_bg, x, &ub)) { ++rej_ss; ++attempt; }
       else if (ub < a.min_basal_uh) { ++rej_basal; ++attempt; }
