@@ -145,6 +145,7 @@ int gt_simulate_fast(const gt_fast_args* a, void* stream) {
           "gt_simulate_fast: the controller period must divide one day");
   REQUIRE((double)a->horizon_ticks * a->dt_s < 2147483647.0,
           "gt_simulate_fast: horizon too long for int32 tick arithmetic");
+  REQUIRE(a->n_slices >= 0, "gt_simulate_fast: n_slices must be >= 0 (0 = automatic)");
   REQUIRE(a->params && a->x0 && a->c0 && a->assumed_basal && a->status && a->ticks &&
               a->bg_hist && a->bg_stats && a->day_dose && a->hypo_events && a->timeline_warp,
           "gt_simulate_fast: null required pointer");
@@ -158,7 +159,6 @@ int gt_simulate_fast(const gt_fast_args* a, void* stream) {
   if (a->noise_kind == GT_NOISE_INJECTED)
     REQUIRE(a->wiener && a->has_noise && a->meas, "gt_simulate_fast: injected noise arrays required");
   REQUIRE(a->hypo_min_ticks > 0, "gt_simulate_fast: hypo_min_ticks must be positive");
-  REQUIRE(a->n_slices >= 0, "gt_simulate_fast: n_slices must be >= 0 (0 = automatic)");
   return gt_launch_fast(a, S(stream));
 }
 

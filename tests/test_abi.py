@@ -73,3 +73,50 @@ def test_no_cpu_fallback_without_device():
     from paper_2202_13927_b200 import engine, _lib
     with pytest.raises(_lib.GlucosimError):
         engine.require_device()
+
+
+def _fast_args(**kw):
+    from paper_2202_13927_b200 import _lib
+    a = _lib.FastArgs()
+    a.n, a.dt_s, a.period_s, a.period_steps = 4, 60.0, 300.0, 5
+    a.horizon_ticks, a.grid_step_ticks, a.n_days, a.n_grid = 2880, 60, 2, 48
+    a.hypo_min_ticks, a.controller = 15, 1
+    for k, v in kw.items():
+        setattr(a, k, v)
+    return a
+
+
+def _call_fast(lib, a):
+    from paper_2202_13927_b200 import _lib
+    fn = lib.gt_simulate_fast
+    fn.restype = C.c_int
+    fn.argtypes = [C.POINTER(_lib.FastArgs), C.c_void_p]
+    rc = fn(C.byref(a), None)
+    buf = C.create_string_buffer(512)
+    lib.gt_last_error(buf, C.c_int64(512))
+    return rc, buf.value.decode()
+
+
+@pytest.mark.parametrize("n_days", [1, 3, 0])
+def test_fast_rejects_a_day_buffer_that_does_not_match_the_horizon(lib, n_days):
+    """Advisor finding r01: the kernels index the day buffers by t // 86400
+    without a bound, so n_days must be exactly max(1, ceil(horizon / 1 day));
+    the check runs before any CUDA call (works without a GPU)."""
+    rc, msg = _call_fast(lib, _fast_args(n_days=n_days))
+    assert rc == -1 and "n_days" in msg, (rc, msg)   # GT_EINVAL
+
+
+def test_parity_rejects_a_short_day_buffer(lib):
+    from paper_2202_13927_b200 import _lib
+    a = _lib.ParityArgs()
+    a.n, a.dt_s, a.period_s, a.period_steps = 2, 30.0, 300.0, 10
+    a.horizon_ticks, a.grid_step_ticks, a.n_days, a.n_grid, a.block_ticks = 5760, 120, 1, 48, 5760
+    fn = lib.gt_simulate_parity
+    fn.restype = C.c_int
+    fn.argtypes = [C.POINTER(_lib.ParityArgs), C.c_void_p]
+    assert fn(C.byref(a), None) == -1
+
+
+def test_fast_rejects_negative_slice_count(lib):
+    rc, msg = _call_fast(lib, _fast_args(n_slices=-3))
+    assert rc == -1 and "n_slices" in msg, (rc, msg)
