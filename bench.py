@@ -554,7 +554,7 @@ def run_ours(args):
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "path": "trial.run_population_arrays (pinned host params -> report fields + per-patient metrics)"},
         "e2e_run_trial_api": api,
-        "gpu_launches": args.steps * 6,   # per step: fused kernel + exclusion re-run + 4 reduction kernels
+        "gpu_launches": args.steps * 7,   # per step: fused kernel + exclusion re-run + abort-tick pass + 4 reduction kernels
         "clocks": clk.summary(),
         "sampler_s": sampler_s,
         "trial": {"n_patients": acc_all.n_patients, "n_aborted": acc_all.n_aborted,

@@ -19,7 +19,7 @@
 extern "C" {
 #endif
 
-#define GT_ABI_VERSION 3  /* 2: gt_fast_args.hyper by value; 3: dose_sum_fp [6] (128-bit) */
+#define GT_ABI_VERSION 4  /* 2: gt_fast_args.hyper by value; 3: dose_sum_fp [6] (128-bit); 4: gt_stage_fast */
 
 /* layouts — hovorka.py:38-55, controller.py:32-41, analytics.py:21-37 */
 #define GT_N_STATES 16
@@ -90,6 +90,20 @@ int gt_steady_state(int64_t n, const double *params, double target_bg, double *x
 int gt_controller_init(int64_t n, const double *hyper, double icr_initial_factor,
                        const double *assumed_basal_uh,
                        double *c0, void *stream);
+
+/* ------------------------------------------------ fused-path staging */
+/* The fused kernel's launch-time inputs in one device pass (the reference
+ * runs hovorka.steady_state per patient and then simulates only patients
+ * with one, simulation.py:320-323, analytics.py:267-269):
+ *   active[i] = (ss_status == NULL || ss_status[i] == GT_STATUS_OK)
+ *   fixed[0..29] = params[0][0..29], and *mismatch = 1 when any patient's
+ *   fixed block params[i][GT_FIXED_FIRST..29] differs from row 0 (NaN counts
+ *   as a difference): the fused kernel folds that block into launch constants
+ *   (gt_fast_args.fixed), so the caller must reject such a population.
+ * All outputs are device pointers; active may be NULL. */
+#define GT_FIXED_FIRST 15
+int gt_stage_fast(int64_t n, const double *params, const int32_t *ss_status, int32_t *active,
+                  double *fixed, int32_t *mismatch, void *stream);
 
 /* ------------------------------------------------ parity-mode integrator */
 /* Batched restatement of _simulate_arrays' fast-engine loop
@@ -164,7 +178,11 @@ typedef struct gt_fast_args {
      * of a previous launch over the same arrays) is GT_STATUS_NONFINITE, with
      * those lanes masked: rewrites the other lanes' outputs and the warps'
      * timeline partials so no statistic includes a diverged patient
-     * (analytics.py:267-269); warps without one exit at once. */
+     * (analytics.py:267-269); warps without one exit at once.
+     * 2 = abort-tick pass, after the re-run: only those lanes run, with the
+     * reference's per-tick state and per-step BG checks (_kernel.py:98-103,
+     * 139-141), and only their `ticks` (the reference's abort tick,
+     * simulation.py:381) and `status` are written.  Takes no trace. */
     int32_t rerun_diverged;
     /* Values of the non-sampled ("fixed", hovorka_distributions.yaml:46-81)
      * parameters shared by every patient of the launch, in p[30] order; the

@@ -19,6 +19,7 @@ GT_STATUS_NONFINITE = 1
 GT_STATUS_NO_STEADY_STATE = 2
 GT_STATUS_EXCLUDED = 3
 GT_STATUS_BAD_INITIAL_STATE = 4
+GT_FIXED_FIRST = 15
 
 GT_PROTO_CSR = 0
 GT_PROTO_THREE_MEAL = 1
@@ -126,6 +127,7 @@ SIGNATURES = [
     ("gt_device_sm_count", C.c_int, [C.c_int]),
     ("gt_steady_state", C.c_int, [I64, P, D, P, P, P, P]),
     ("gt_controller_init", C.c_int, [I64, P, D, P, P, P]),
+    ("gt_stage_fast", C.c_int, [I64, P, P, P, P, P, P]),
     ("gt_simulate_parity", C.c_int, [C.POINTER(ParityArgs), P]),
     ("gt_simulate_fast", C.c_int, [C.POINTER(FastArgs), P]),
     ("gt_fast_num_warps", I64, [I64]),
@@ -161,7 +163,7 @@ def load(path: str | None = None):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.gt_abi_version() != 3:   # include/glucosim.h GT_ABI_VERSION
+    if lib.gt_abi_version() != 4:   # include/glucosim.h GT_ABI_VERSION
         raise GlucosimError("libglucosim ABI version mismatch")
     if path is None:
         _lib = lib

@@ -38,6 +38,8 @@ int gt_launch_steady_state(int64_t n, const double* params, double target_bg, do
                            double* ub, int32_t* status, cudaStream_t st);
 int gt_launch_controller_init(int64_t n, const double* hyper, double icr_initial_factor,
                               const double* basal, double* c0, cudaStream_t st);
+int gt_launch_stage_fast(int64_t n, const double* params, const int32_t* ss_status, int32_t* active,
+                         double* fixed, int32_t* mismatch, cudaStream_t st);
 int gt_launch_fast(const gt_fast_args* a, cudaStream_t st);
 int64_t gt_fast_scratch_need(int64_t n);
 int gt_launch_noise_normals(int64_t n, int64_t pid0, uint64_t seed, uint32_t role, int64_t k0,
@@ -90,6 +92,13 @@ int gt_controller_init(int64_t n, const double* hyper, double icr_initial_factor
   REQUIRE(n >= 0, "gt_controller_init: n < 0");
   REQUIRE(n == 0 || (hyper && assumed_basal_uh && c0), "gt_controller_init: null pointer");
   return gt_launch_controller_init(n, hyper, icr_initial_factor, assumed_basal_uh, c0, S(stream));
+}
+
+int gt_stage_fast(int64_t n, const double* params, const int32_t* ss_status, int32_t* active, double* fixed,
+                  int32_t* mismatch, void* stream) {
+  REQUIRE(n >= 1, "gt_stage_fast: n=%lld < 1 (row 0 is the reference row)", (long long)n);
+  REQUIRE(params && fixed && mismatch, "gt_stage_fast: null pointer");
+  return gt_launch_stage_fast(n, params, ss_status, active, fixed, mismatch, S(stream));
 }
 
 static int check_config(const char* who, double dt_s, double period_s, int64_t period_steps,
@@ -146,6 +155,9 @@ int gt_simulate_fast(const gt_fast_args* a, void* stream) {
   REQUIRE((double)a->horizon_ticks * a->dt_s < 2147483647.0,
           "gt_simulate_fast: horizon too long for int32 tick arithmetic");
   REQUIRE(a->n_slices >= 0, "gt_simulate_fast: n_slices must be >= 0 (0 = automatic)");
+  REQUIRE(a->rerun_diverged >= 0 && a->rerun_diverged <= 2,
+          "gt_simulate_fast: rerun_diverged must be 0, 1 (exclusion re-run) or 2 (abort-tick pass)");
+  REQUIRE(!(a->rerun_diverged == 2 && a->trace), "gt_simulate_fast: the abort-tick pass takes no trace");
   REQUIRE(a->params && a->x0 && a->c0 && a->assumed_basal && a->status && a->ticks &&
               a->bg_hist && a->bg_stats && a->day_dose && a->hypo_events && a->timeline_warp,
           "gt_simulate_fast: null required pointer");

@@ -454,8 +454,12 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       return philox_lane(index, nlane, u.nz_a);
     };
 
-    // rerun mode: only warps holding a diverged lane re-simulate (lanes masked)
+    // rerun mode: only warps holding a diverged lane re-simulate (lanes masked).
+    // Abort-tick pass (TRACE instance, rerun_diverged == 2): only the diverged
+    // lanes run, with the reference's per-tick state check and per-step BG
+    // check, and write nothing but their status and abort tick.
     const bool was_bad = a.rerun_diverged && inrange && a.status[i] == GT_STATUS_NONFINITE;
+    const bool abort_pass = TRACE && a.rerun_diverged == 2;
     if (a.rerun_diverged && !__any_sync(0xffffffffu, was_bad)) {
       __syncwarp();
       if (lane == 0) st_release(sch.done + warp_global, chunk + 1);
@@ -514,7 +518,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
     bool alive;
     int status, death_tick;
     if (first) {
-      alive = inrange && !was_bad && (a.active == nullptr || a.active[i] != 0);
+      alive = abort_pass ? was_bad : inrange && !was_bad && (a.active == nullptr || a.active[i] != 0);
       status = (inrange && !alive) ? GT_STATUS_EXCLUDED : GT_STATUS_OK;
       death_tick = -1;
       const double* x0 = a.x0 + ii * NS;
@@ -550,7 +554,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         sdl[(SC_ANNCARBS) * kFastBS] = m0.carbs;
         sil[(SI_EXPTR) * kFastBS] = 0;
       }
-      if (inrange)
+      if (inrange && !abort_pass)
         for (int b = 0; b < GT_N_BG_BINS; ++b) a.bg_hist[(int64_t)b * n + i] = 0;
     } else {
       // every lane (padding included) restores its own slot: a padding lane
@@ -641,7 +645,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         const uint32_t word = s_hist[w * kFastBS + tid];
         if (word == 0u) continue;
         s_hist[w * kFastBS + tid] = 0u;
-        if (!inrange) continue;
+        if (!inrange || abort_pass) continue;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           const uint32_t c = (word >> (8 * b)) & 0xFFu;
@@ -775,7 +779,9 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         // non-finite at any tick is non-finite at the horizon's last tick,
         // and that one check is equivalent to the reference's per-tick checks.
         // (The injected-noise gut clamp is the one exception, beyond ~30 sigma.)
-        if ((!GT_LASTCHECK || ctl == u.n_ctl - 1) && alive) {
+        // (a traced launch checks every tick, as the reference does, so its
+        // abort tick is the reference's: the abort-tick pass relies on it)
+        if ((!GT_LASTCHECK || TRACE || ctl == u.n_ctl - 1) && alive) {
           // x * 0 is +-0 for finite x and NaN for Inf/NaN: one FMA per state,
           // in four short chains
           const R z = 0;
@@ -952,6 +958,9 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         // SURVEY.md §7): use the reference's exact division for that tick
         bg = Q1 / (a.params[ii * NP + PVG] * a.params[ii * NP + PW]);
       }
+      // traced launches: the reference's per-step BG check (_kernel.py:139-141),
+      // so the abort tick is exact; other launches check bg_sum after the horizon
+      if (TRACE && alive && !(fabs(bg) < INFINITY)) { alive = false; status = GT_STATUS_NONFINITE; death_tick = k; }
       if (tick && ctl == next_grid_ctl) {  // timeline point (warp-uniform)
         next_grid_ctl += u.grid_ctl;
         const long long v = __double2ll_rn(bg * kFpScale);
@@ -970,15 +979,15 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           smin = mn == 0xFFFFFFFFu ? LLONG_MAX : (long long)mn;
           smax = mx < 0 ? LLONG_MIN : (long long)mx;
         }
-        if (lane == 0) {
+        if (lane == 0 && !abort_pass) {
           GT_CHECK(g_idx >= 0 && g_idx < a.n_grid, "timeline");
           long long* dst = (long long*)a.timeline_warp + ((int64_t)g_idx * n_warps + warp_global) * 3;
           dst[0] = ssum; dst[1] = smin; dst[2] = smax;
         }
-        if (a.timeline_pp && inrange) a.timeline_pp[(int64_t)g_idx * n + i] = alive ? bg : 0.0;
+        if (a.timeline_pp && inrange && !abort_pass) a.timeline_pp[(int64_t)g_idx * n + i] = alive ? bg : 0.0;
         ++g_idx;
       }
-      if (TRACE && inrange) {  // the parity kernel's 8 trace columns (simulation.py:61-64)
+      if (TRACE && inrange && a.trace) {  // the parity kernel's 8 trace columns (simulation.py:61-64)
         double* tr = a.trace + ((int64_t)i * a.horizon_ticks + k) * 8;
         tr[0] = (double)k * u.dt; tr[1] = bg; tr[2] = tr_y; tr[3] = gin_k != (R)0 ? tr_rate : 0.0;
         tr[4] = hrr; tr[5] = tr_basal; tr[6] = tr_bolus; tr[7] = tr_gluc;
@@ -1072,7 +1081,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           // column address is formed only on that path
           if (__builtin_expect(c == 255u, 0)) {
             asm volatile("st.shared.u8 [%0], 0;" :: "r"(ha) : "memory");
-            if (kb < GT_N_BG_BINS && inrange) {
+            if (kb < GT_N_BG_BINS && inrange && !abort_pass) {
               // 32-bit element offset (the launcher bounds 247 n < 2^31): the drain
               // path then needs fewer scratch registers than a 64-bit index
               if (GT_DRAIN32 & kShapeBit) atomicAdd(a.bg_hist + (uint32_t)(kb * (uint32_t)n + (uint32_t)i), 255);
@@ -1116,7 +1125,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         if (ctl > 0) {
           const int64_t day = ctl / cpd - 1;
           GT_CHECK(day >= 0 && day < a.n_days, "day flush");
-          if (inrange) {
+          if (inrange && !abort_pass) {
             double* dd = a.day_dose + (day * 3) * n + i;
             dd[0] = day_basal; dd[n] = sdl[(SC_DBOLUS) * kFastBS]; dd[2 * n] = sdl[(SC_DGLUC) * kFastBS];
           }
@@ -1150,7 +1159,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
     }
     // an all-dead warp stops early: its remaining timeline partials are identities
     for (; next_grid_ctl < ctl_hi; next_grid_ctl += u.grid_ctl, ++g_idx)
-      if (lane == 0) {
+      if (lane == 0 && !abort_pass) {
         GT_CHECK(g_idx >= 0 && g_idx < a.n_grid, "timeline tail");
         long long* dst = (long long*)a.timeline_warp + ((int64_t)g_idx * n_warps + warp_global) * 3;
         dst[0] = 0; dst[1] = LLONG_MAX; dst[2] = LLONG_MIN;
@@ -1202,6 +1211,11 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         STI(SV_STATUS, status); STI(SV_DEATH, death_tick);
 #undef STD
 #undef STI
+      }
+    } else if (abort_pass) {   // the diverged lanes' exact abort tick (simulation.py:381)
+      if (was_bad) {
+        a.status[i] = status == GT_STATUS_OK ? GT_STATUS_NONFINITE : status;
+        a.ticks[i] = status == GT_STATUS_OK ? a.horizon_ticks : (death_tick < 0 ? 0 : death_tick);
       }
     } else if (inrange && !was_bad) {  // a rerun keeps the diverged lanes' outputs
       // ---- final outputs
@@ -1370,7 +1384,7 @@ static int launch_sched(const gt_fast_args* a, const gt::Uni& u, cudaStream_t st
 template <int PROTO, int NOISE, typename R = double, bool AGG = false>
 static int launch_one(const gt_fast_args* a, const gt::Uni& u, cudaStream_t st) {
   const bool pid = a->controller == GT_CTRL_PID_PUMP;
-  if (a->trace)
+  if (a->trace || a->rerun_diverged == 2)   // traced, or the abort-tick pass (exact checks)
     return pid ? launch_sched<PROTO, NOISE, R, AGG, true, GT_CTRL_PID_PUMP>(a, u, st)
                : launch_sched<PROTO, NOISE, R, AGG, true, GT_CTRL_DUAL_HORMONE>(a, u, st);
   return pid ? launch_sched<PROTO, NOISE, R, AGG, false, GT_CTRL_PID_PUMP>(a, u, st)

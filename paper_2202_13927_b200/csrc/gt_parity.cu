@@ -290,6 +290,19 @@ __global__ void steady_state_kernel(int64_t n, const double* params, double targ
   status[i] = ok ? GT_STATUS_OK : GT_STATUS_NO_STEADY_STATE;
 }
 
+// gt_stage_fast (include/glucosim.h): active mask + fixed-block uniformity
+__global__ void stage_fast_kernel(int64_t n, const double* params, const int32_t* ss_status, int32_t* active,
+                                  double* fixed, int32_t* mismatch) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (i == 0)
+    for (int k = 0; k < GT_N_PARAMS; ++k) fixed[k] = params[k];
+  bool diff = false;
+  for (int k = GT_FIXED_FIRST; k < GT_N_PARAMS; ++k) diff |= !(params[i * GT_N_PARAMS + k] == params[k]);
+  if (diff) atomicOr(mismatch, 1);
+  if (active) active[i] = ss_status == nullptr || ss_status[i] == GT_STATUS_OK;
+}
+
 // controller.py:241-250 initial_icr + ControllerState defaults (:183-195,
 // to_vec :197-210).  np.clip propagates NaN.
 __global__ void controller_init_kernel(int64_t n, const double* hyper, double icr_initial_factor,
@@ -327,6 +340,15 @@ int gt_launch_steady_state(int64_t n, const double* params, double target_bg, do
   const int bs = 128;
   gt::steady_state_kernel<<<grid_for(n, bs), bs, 0, st>>>(n, params, target_bg, x0, ub, status);
   return gt_check_launch("steady_state_kernel");
+}
+
+int gt_launch_stage_fast(int64_t n, const double* params, const int32_t* ss_status, int32_t* active,
+                         double* fixed, int32_t* mismatch, cudaStream_t st) {
+  cudaMemsetAsync(mismatch, 0, sizeof(int32_t), st);
+  if (n <= 0) return gt_check_launch("stage_fast (memset)");
+  const int bs = 256;
+  gt::stage_fast_kernel<<<grid_for(n, bs), bs, 0, st>>>(n, params, ss_status, active, fixed, mismatch);
+  return gt_check_launch("stage_fast_kernel");
 }
 
 int gt_launch_controller_init(int64_t n, const double* hyper, double icr_initial_factor,

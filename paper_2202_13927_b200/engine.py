@@ -245,7 +245,7 @@ def launch_fast(inputs: dict, outs: FastOutputs, sz: dict, dt_s: float, period_s
                                                           sz["grid_step_ticks"])
     a.n_days, a.n_grid, a.hypo_min_ticks = sz["n_days"], sz["n_grid"], int(hypo_min_ticks)
     a.noise_role = noise_role
-    a.rerun_diverged = int(bool(rerun_diverged))
+    a.rerun_diverged = int(rerun_diverged)   # 0 off, 1 exclusion re-run, 2 abort-tick pass
     for k in ("params", "x0", "c0", "assumed_basal", "active"):
         setattr(a, k, ptr(inputs.get(k)))
     # hyperparameters by value (the kernel's parameter bank): the host copy
@@ -319,20 +319,40 @@ def noise_normals(n: int, pid0: int, seed: int, role: int, k0: int, n_ticks: int
     return out
 
 
-FIXED_PARAM_INDEX = tuple(range(15, 30))   # AG .. R: the table's fixed block (hovorka.py:53-55)
+FIXED_PARAM_INDEX = tuple(range(_lib.GT_FIXED_FIRST, 30))   # AG .. R: the table's fixed block (hovorka.py:53-55)
+
+
+def stage_fast(params, ss_status=None, want_active: bool = True):
+    """One device pass (gt_stage_fast): the fused kernel's launch constants
+    and active mask.  Returns (fixed [30] numpy = row 0 of ``params``, active
+    int32 device tensor or None); raises unless every patient shares the
+    fixed parameters (hovorka_distributions.yaml: 'identical for every
+    generated patient'), which the fused kernel folds into launch constants.
+    active[i] = ss_status[i] == GT_STATUS_OK (all ones without ss_status)."""
+    t = torch()
+    device = params.device
+    n = int(params.shape[0])
+    p = params.contiguous()
+    active = empty((n,), t.int32, device) if want_active else None
+    fixed_d = empty((30,), t.float64, device)
+    flag_d = empty((1,), t.int32, device)
+    check(_lib.load().gt_stage_fast(n, ptr(p), ptr(ss_status), ptr(active), ptr(fixed_d), ptr(flag_d),
+                                    stream_ptr(device)), "gt_stage_fast")
+    fixed_h = t.empty((30,), dtype=t.float64, pin_memory=True)
+    flag_h = t.empty((1,), dtype=t.int32, pin_memory=True)
+    fixed_h.copy_(fixed_d, non_blocking=True)
+    flag_h.copy_(flag_d, non_blocking=True)
+    t.cuda.current_stream(device).synchronize()
+    if int(flag_h[0]) != 0:
+        raise _lib.GlucosimError("the fused path needs fixed parameters shared by all patients; "
+                                 "use the parity path (noise='reference') for per-patient overrides")
+    return fixed_h.numpy().astype(np.float64), active
 
 
 def uniform_fixed(params) -> np.ndarray:
-    """Row 0 of the parameter matrix after verifying that every patient shares
-    the fixed parameters (hovorka_distributions.yaml: 'identical for every
-    generated patient'); the fused kernel folds them into launch constants."""
-    t = torch()
-    idx = list(FIXED_PARAM_INDEX)
-    cols = params[:, idx]
-    if not bool((cols == cols[0:1]).all()):
-        raise _lib.GlucosimError("the fused path needs fixed parameters shared by all patients; "
-                                 "use the parity path (noise='reference') for per-patient overrides")
-    return params[0].detach().cpu().numpy().astype(np.float64)
+    """Row 0 of the parameter matrix after verifying on the device that every
+    patient shares the fixed parameters (see :func:`stage_fast`)."""
+    return stage_fast(params, want_active=False)[0]
 
 
 @dataclass

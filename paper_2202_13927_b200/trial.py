@@ -78,13 +78,13 @@ class FastTrial:
                 # the sampler's own steady states (same solve, same target BG): every
                 # sampled patient has one, so nothing is aborted at staging
                 self.x0 = x0
-                self.ss_status = t.zeros((self.n,), dtype=t.int32, device=self.device)
+                self.ss_status = None
             else:
                 self.x0, _ub, self.ss_status = engine.steady_state(params, config.initial_bg_mmol_per_l, self.device)
             self.c0 = engine.controller_init(self.hyper, icr_initial_factor(profile), basal, self.device)
             self.hyper_d = engine.dev(self.hyper, t.float64, self.device)
-            self.fixed = engine.uniform_fixed(params)   # verified once, at staging
-            self.active = (self.ss_status == GT_STATUS_OK).to(t.int32)
+            # launch constants (fixed block verified uniform) and the active mask, one device pass
+            self.fixed, self.active = engine.stage_fast(params, self.ss_status)
             self.meal_spec, self.csr = None, None
             if isinstance(generator, ThreeMealProtocol):
                 self.meal_spec = generator.device_spec()
@@ -135,12 +135,15 @@ class FastTrial:
         }
 
     # ------------------------------------------------------------- running
-    def simulate(self, active=None, injected=None, rerun_diverged=False):
-        """Enqueue the fused integrator (current stream, no sync)."""
+    def simulate(self, active=None, injected=None, rerun_diverged=0):
+        """Enqueue the fused integrator (current stream, no sync).
+        rerun_diverged: 0 the full run, 1 the exclusion re-run, 2 the
+        abort-tick pass (see ``_rerun_if_diverged``)."""
         inputs = dict(self._inputs)
         if active is not None:
             inputs["active"] = active
-        with engine.nvtx("gt.exclusion_rerun" if rerun_diverged else "gt.fused_integrator"):
+        name = {0: "gt.fused_integrator", 1: "gt.exclusion_rerun", 2: "gt.abort_tick_pass"}[int(rerun_diverged)]
+        with engine.nvtx(name):
             self._launch(inputs, injected, rerun_diverged)
 
     def _launch(self, inputs, injected, rerun_diverged):
@@ -191,11 +194,16 @@ class FastTrial:
         self._rerun_if_diverged()
         self.reduce()
 
-    def _rerun_if_diverged(self):
+    def _rerun_if_diverged(self, injected=None):
         """Device-side: warps that hold a diverged patient re-simulate with it
-        masked (deterministic streams); all other warps exit at once.  No host
-        synchronisation."""
-        self.simulate(rerun_diverged=True)
+        masked (deterministic streams); all other warps exit at once.  Then
+        the abort-tick pass runs the diverged lanes alone with the reference's
+        per-tick state and per-step BG checks, so their ``ticks`` is the
+        reference's abort tick (simulation.py:381) rather than the horizon
+        (the throughput launch detects divergence at the horizon only).  No
+        host synchronisation; both passes exit at once when nothing diverged."""
+        self.simulate(injected=injected, rerun_diverged=1)
+        self.simulate(injected=injected, rerun_diverged=2)
 
     # ----------------------------------------------------------- readback
     def _fetch(self, *xs):
@@ -214,12 +222,17 @@ class FastTrial:
             t.cuda.current_stream(self.device).synchronize()
         return [h.numpy() for h in hosts]
 
+    def _ss_status_or_ok(self):
+        if self.ss_status is not None:
+            return self.ss_status
+        return engine.torch().zeros((self.n,), dtype=engine.torch().int32)   # host: every patient has one
+
     def accumulator(self) -> TrialAccumulator:
         cfg, sz, red = self.config, self.sz, self.red
         acc = TrialAccumulator(dt_s=cfg.dt_s, horizon_ticks=sz["horizon_ticks"], n_days=sz["n_days"],
                                n_grid=sz["n_grid"], grid_step_s=cfg.grid_step_s)
         (counts, status, ss, tir_total, tir_hist, bg_total, below_min, below_max, mm, tl, dh, dsum, mhist,
-         w) = self._fetch(red.counts, self.outs.status, self.ss_status, red.tir_ticks_total, red.tir_hist,
+         w) = self._fetch(red.counts, self.outs.status, self._ss_status_or_ok(), red.tir_ticks_total, red.tir_hist,
                           red.bg_hist_total, red.below_min, red.below_max, red.minmax_bg_bits, red.timeline,
                           red.dose_hist, red.dose_sum_fp, red.metric_hist, red.worst)
         acc.n_patients = int(counts[0])

@@ -40,7 +40,7 @@ def test_exports_every_declared_symbol(lib):
 
 def test_abi_version(lib):
     lib.gt_abi_version.restype = C.c_int
-    assert lib.gt_abi_version() == 3
+    assert lib.gt_abi_version() == 4
 
 
 def test_struct_layouts_match_c():

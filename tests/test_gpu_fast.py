@@ -569,3 +569,72 @@ def test_hypo_runs_across_slices(dev, controller):
     for ft in runs[1:]:
         for k in ("status", "bg_hist", "bg_stats", "hypo_events", "day_dose"):
             assert torch.equal(getattr(ft.outs, k), getattr(runs[0].outs, k)), k
+
+
+def test_abort_tick_matches_reference(dev):
+    """The fused path's abort tick of a diverging patient is the reference's
+    (simulation.py:381: ticks counted before the abort).  The reference's own
+    fault fixture (tau_cgm = -1: the sensor state diverges, caught by the
+    per-tick state check, _kernel.py:98-103) aborts at tick 1760; the
+    throughput launch detects the divergence at the horizon, and the
+    abort-tick pass (rerun_diverged = 2) recovers the exact tick."""
+    from paper_2202_13927_b200 import engine, rng
+    from paper_2202_13927_b200._lib import GT_STATUS_NONFINITE
+    case = SimCase("sim_faults.npz")
+    g = case.g
+    bad = int(np.nonzero(g["status"] == GT_STATUS_NONFINITE)[0][0])
+    sub = case.subset(np.arange(case.n) == bad)   # alone: its tau_cgm is a launch constant
+    inj = _injected(sub, dev)
+    csr = _csr_ticks(case, sub, dev)
+    outs = _run_fast(case, sub, dev, csr=csr, injected=inj)
+    assert _h(outs.status)[0] == GT_STATUS_NONFINITE
+    # lazy detection: the state check at the horizon's last controller tick
+    assert _h(outs.ticks)[0] == case.sz["horizon_ticks"] - case.sz["period_steps"]
+    for mode in (1, 2):
+        engine.launch_fast(_inputs(case, sub, dev), outs, case.sz, case.config.dt_s,
+                           case.config.controller_period_s, case.config.seed, rng.ROLE_DEVICE_NOISE,
+                           max(1, int(np.ceil(900 / case.config.dt_s))), dev, csr=csr, injected=inj,
+                           rerun_diverged=mode)
+    assert _h(outs.status)[0] == GT_STATUS_NONFINITE
+    assert int(_h(outs.ticks)[0]) == int(g["ticks"][bad]) == 1760
+
+
+@pytest.mark.parametrize("controller", ["dual_hormone", "pid_pump"])
+def test_fast_trial_abort_tick_is_exact(dev, controller):
+    """FastTrial.step() ends with the abort-tick pass: a diverging patient's
+    ticks is the first tick whose state or BG is non-finite (the traced
+    re-simulation, which checks every tick and step as the reference does,
+    agrees, and its BG column is finite before it), every other patient's
+    outputs are untouched by the pass."""
+    from paper_2202_13927_b200._lib import GT_STATUS_NONFINITE
+    from paper_2202_13927_b200.config import SimulationConfig
+    from paper_2202_13927_b200.controller import ControllerHyperparameters
+    from paper_2202_13927_b200.pid import PIDProfile
+    from paper_2202_13927_b200.population import generate_population
+    from paper_2202_13927_b200.protocol import ThreeMealProtocol
+    from paper_2202_13927_b200.trial import FastTrial
+    cfg = SimulationConfig(horizon_s=2 * 86400.0, seed=2, dt_s=60.0)
+    pop = generate_population(3, 64, device=dev, on_exhausted="redraw_weight")
+    params = pop.params_device.clone()
+    params[5, 4] = -5.0             # ka1 < 0: diverges mid-trial
+    prof = PIDProfile() if controller == "pid_pump" else ControllerHyperparameters()
+    ft = FastTrial(0, params, pop.basal_device, ThreeMealProtocol(), prof, cfg, controller, dev,
+                   per_patient_metrics=True)
+    ft.simulate()
+    ft.simulate(rerun_diverged=1)
+    before = {k: _h(getattr(ft.outs, k)).copy() for k in ("status", "ticks", "bg_hist", "bg_stats", "day_dose",
+                                                            "hypo_events", "timeline_warp")}
+    ft.simulate(rerun_diverged=2)
+    st, ticks = _h(ft.outs.status), _h(ft.outs.ticks)
+    H = ft.sz["horizon_ticks"]
+    assert st[5] == GT_STATUS_NONFINITE and 0 < ticks[5] < H
+    keep = np.arange(64) != 5
+    for k, v in before.items():
+        now = _h(getattr(ft.outs, k))
+        if k in ("status", "ticks"):
+            assert np.array_equal(now[keep], v[keep]), k
+        else:
+            assert np.array_equal(now, v, equal_nan=True), k
+    _s, tt, tr = ft.trace_range(5, 6)
+    assert _s[0] == GT_STATUS_NONFINITE and tt[0] == ticks[5]
+    assert np.all(np.isfinite(tr[0, : ticks[5], 1]))
