@@ -287,8 +287,13 @@ double oracle_det_exp(double x)
     if (x < -745.0) return 0.0;
     double kf = floor(x * 1.44269504088896338700e+00 + 0.5);
     double r = (x - kf * 6.93147180369123816490e-01) - kf * 1.90821492927058770002e-10;
-    double s = 1.0;
-    for (int j = 14; j >= 1; --j) s = 1.0 + (r * s) / (double)j;
+    static const double inv_fact[15] = {
+        1.0, 1.0, 0.5, 0.16666666666666666, 0.041666666666666664, 0.008333333333333333,
+        0.001388888888888889, 0.0001984126984126984, 2.48015873015873e-05, 2.7557319223985893e-06,
+        2.755731922398589e-07, 2.505210838544172e-08, 2.08767569878681e-09, 1.6059043836821613e-10,
+        1.1470745597729725e-11};
+    double s = inv_fact[14];
+    for (int j = 13; j >= 0; --j) s = inv_fact[j] + r * s;
     return ldexp(s, (int)kf);
 }
 

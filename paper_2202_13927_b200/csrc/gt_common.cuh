@@ -77,16 +77,23 @@ __device__ __forceinline__ double det_log(double x) {
   return A_(M_(de, 6.93147180369123816490e-01), A_(M_(de, 1.90821492927058770002e-10), logm));
 }
 
-// Deterministic exp from IEEE +,-,*,/ only: x = k*ln2 + r, Taylor(r) to
-// degree 14 (|r| <= ln2/2), then an exact scaling by 2^k.
+// Deterministic exp from IEEE +,-,* only: x = k*ln2 + r, Taylor(r) to
+// degree 14 (|r| <= ln2/2) by Horner on the doubles nearest 1/j!, then an
+// exact scaling by 2^k.  (No divisions: the sampler evaluates eight of these
+// per steady-state candidate.)
 __device__ __forceinline__ double det_exp(double x) {
+  constexpr double kInvFact[15] = {
+    1.0, 1.0, 0.5, 0.16666666666666666, 0.041666666666666664, 0.008333333333333333,
+    0.001388888888888889, 0.0001984126984126984, 2.48015873015873e-05, 2.7557319223985893e-06,
+    2.755731922398589e-07, 2.505210838544172e-08, 2.08767569878681e-09, 1.6059043836821613e-10,
+    1.1470745597729725e-11};
   if (x > 709.0) return INFINITY;
   if (x < -745.0) return 0.0;
   const double kf = floor(A_(M_(x, 1.44269504088896338700e+00), 0.5));
   const double r = S_(S_(x, M_(kf, 6.93147180369123816490e-01)), M_(kf, 1.90821492927058770002e-10));
-  // Horner for sum_{j=0}^{14} r^j / j!
-  double s = 1.0;
-  for (int j = 14; j >= 1; --j) s = A_(1.0, D_(M_(r, s), (double)j));
+  double s = kInvFact[14];
+#pragma unroll
+  for (int j = 13; j >= 0; --j) s = A_(kInvFact[j], M_(r, s));
   return ldexp(s, (int)kf);
 }
 

@@ -15,6 +15,9 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+// the steady-state solve is one out-of-line function (code size: the kernel is
+// instruction-fetch bound when every call site inlines it)
+#define GT_SS_NOINLINE 1
 #include "gt_ref_model.cuh"
 
 namespace gt {
@@ -56,8 +59,9 @@ __device__ __forceinline__ double sampled_value(const gt_sampler_args& a, int j,
 // handed to straggler_kernel, which searches its remaining attempts 128 at a
 // time with a whole block instead of one lane.
 // One attempt's values written into the packed parameter vector.
-__device__ void fill_attempt_p(const gt_sampler_args& a, uint32_t actr, uint32_t pid, uint32_t k0, uint32_t k1,
-                               double* p) {
+__device__ __noinline__ void fill_attempt_p(const gt_sampler_args& a, uint32_t actr, uint32_t pid, uint32_t k0,
+                                            uint32_t k1, double* p) {
+#pragma unroll 1
   for (int q = 0; q < a.n_sampled; q += 2) {
     const U4 r = philox4x32_10(actr, pid, kRoleSamplerParams, (uint32_t)(q >> 1), k0, k1);
     p[a.param_index[q]] = sampled_value(a, q, det_inv_norm(u52(r.x, r.y)));
@@ -65,7 +69,100 @@ __device__ void fill_attempt_p(const gt_sampler_args& a, uint32_t actr, uint32_t
   }
 }
 
-constexpr int kPark = 384;
+// ---- cheap rules on the uniform key
+// A normal value v = a + b * inv_norm(u52(k)) is a monotone function of the
+// 52-bit key k (the uniform's integer image), so each of the reference's
+// cheap rules -- v < 0, v - a < -b, v - a > b -- flips once along k.  A setup
+// kernel locates each flip with the exact device arithmetic (bisection on k);
+// phase 1 then decides a value from k alone, and evaluates it exactly only
+// when k falls within a band around a flip (about 1e-5 of the draws).  The
+// band (|k - K| <= min(K, 2^52 - K) / 2^16 + 2^16, i.e. ~1e-5 relative in u)
+// is many orders wider than the ulp-level non-monotonicity of the
+// floating-point inverse CDF, so every decision equals the exact one.
+struct KeyRule {
+  unsigned long long e[3], w[3];  // band of flip f: k - e[f] < w[f] (unsigned); f: 0 neg, 1 low, 2 high
+  unsigned long long k_neg, k_lo, k_hi;  // neg: k < k_neg; low: k < k_lo; high: k >= k_hi
+};
+constexpr unsigned long long kKeyEnd = 1ull << 52;
+
+__device__ __forceinline__ unsigned long long key52(uint32_t a, uint32_t b) {
+  return ((unsigned long long)(a >> 6) << 26) | (unsigned long long)(b >> 6);
+}
+__device__ __forceinline__ double normal_at(const gt_sampler_args& a, int j, unsigned long long k) {
+  return A_(a.a[j], M_(a.b[j], det_inv_norm(M_((double)(2 * k + 1), 1.1102230246251565404e-16))));
+}
+// rule f at key k, exactly (f 0: v < 0; 1: v - a < -b; 2: v - a > b)
+__device__ bool rule_exact(const gt_sampler_args& a, int j, int f, unsigned long long k) {
+  const double v = normal_at(a, j, k);
+  if (f == 0) return v < 0.0;
+  const double d = S_(v, a.a[j]);
+  return f == 1 ? d < -a.b[j] : d > a.b[j];
+}
+
+// thread (j, f): the flip of rule f of sampled normal j
+__global__ void key_rules_kernel(gt_sampler_args a, KeyRule* rules) {
+  const int j = threadIdx.x / 3, f = threadIdx.x % 3;
+  if (j >= a.n_sampled) return;
+  unsigned long long K;
+  if (a.kind[j] != 0) {
+    K = f == 2 ? kKeyEnd : 0;                     // lognormals: no cheap rule
+  } else if (f < 2) {                             // true below the flip
+    unsigned long long lo = 0, hi = kKeyEnd;      // rule(lo) true, rule(hi) false
+    if (!rule_exact(a, j, f, 0)) K = 0;
+    else {
+      while (hi - lo > 1) {
+        const unsigned long long mid = lo + (hi - lo) / 2;
+        if (rule_exact(a, j, f, mid)) lo = mid; else hi = mid;
+      }
+      K = hi;
+    }
+  } else {                                        // true from the flip on
+    unsigned long long lo = 0, hi = kKeyEnd - 1;  // rule(lo) false, rule(hi) true
+    if (!rule_exact(a, j, f, hi)) K = kKeyEnd;
+    else if (rule_exact(a, j, f, 0)) K = 0;
+    else {
+      while (hi - lo > 1) {
+        const unsigned long long mid = lo + (hi - lo) / 2;
+        if (rule_exact(a, j, f, mid)) hi = mid; else lo = mid;
+      }
+      K = hi;
+    }
+  }
+  const bool flips = a.kind[j] == 0 && K > 0 && K < kKeyEnd;
+  const unsigned long long m = flips ? ((K < kKeyEnd - K ? K : kKeyEnd - K) >> 16) + (1ull << 16) : 0;
+  const unsigned long long e = K > m ? K - m : 0;
+  rules[j].e[f] = e;
+  rules[j].w[f] = flips ? K + m + 1 - e : 0;
+  (f == 0 ? rules[j].k_neg : f == 1 ? rules[j].k_lo : rules[j].k_hi) = K;
+}
+
+// The reference's first two rules on one normal draw (population.py:234-244),
+// from its key: exact inside a flip band, by the flips elsewhere.
+// bit 0: v < 0, bit 1: outside one SD (out of line: rare)
+__device__ __noinline__ int key_exact(const gt_sampler_args& a, int j, unsigned long long k) {
+  const double v = normal_at(a, j, k);
+  return (v < 0.0 ? 1 : 0) | (fabs(S_(v, a.a[j])) > a.b[j] ? 2 : 0);
+}
+__device__ __forceinline__ void key_verdict(const gt_sampler_args& a, const KeyRule& r, int j,
+                                            unsigned long long k, bool& neg, bool& outside) {
+  if (k - r.e[0] < r.w[0] || k - r.e[1] < r.w[1] || k - r.e[2] < r.w[2]) {
+    const int v = key_exact(a, j, k);
+    neg |= (v & 1) != 0;
+    outside |= (v & 2) != 0;
+  } else {
+    neg |= k < r.k_neg;
+    outside |= k < r.k_lo || k >= r.k_hi;
+  }
+}
+
+#ifndef GT_SAMPLER_PARK
+#define GT_SAMPLER_PARK 384
+#endif
+constexpr int kPark = GT_SAMPLER_PARK;   // attempts of one body weight before a patient is parked
+#ifndef GT_STRAG_BS
+#define GT_STRAG_BS 512
+#endif
+constexpr int kStragBS = GT_STRAG_BS;    // straggler_kernel: attempts evaluated per round
 #ifndef GT_SAMPLER_CAP
 #define GT_SAMPLER_CAP 1   // with solve batching: 1 ~ 2 ~ 8 (tools/ab_sampler.sh); 4 was best without
 #endif
@@ -82,11 +179,30 @@ struct Straggler {
   double w;
 };
 
+// population.py:148-153 _positive_normal: the next positive weight draw of
+// the patient's weight stream (0 when the budget is spent); advances *wctr.
+__device__ __noinline__ double draw_weight_dev(const gt_sampler_args& a, uint32_t pid, uint32_t* wctr,
+                                               uint32_t k0, uint32_t k1) {
+  uint32_t c = *wctr;
+  double w = 0.0;
+  for (int t = 0; t < a.max_attempts; ++t, ++c) {
+    const U4 r = philox4x32_10(c, pid, kRoleSamplerWeight, 0u, k0, k1);
+    const double v = A_(a.weight_mean, M_(a.weight_sd, det_inv_norm(u52(r.x, r.y))));
+    if (v > 0.0) { w = v; ++c; break; }
+  }
+  *wctr = c;
+  return w;
+}
+
 #ifndef GT_SAMPLER_MINB
-#define GT_SAMPLER_MINB 1
+#define GT_SAMPLER_MINB 2
 #endif
-__global__ void __launch_bounds__(128, GT_SAMPLER_MINB) sampler_kernel(gt_sampler_args a, unsigned long long* queue,
+__global__ void __launch_bounds__(128, GT_SAMPLER_MINB) sampler_kernel(gt_sampler_args a, const KeyRule* rules,
+                                                      unsigned long long* queue,
                                                       Straggler* park, unsigned int* n_park, int park_cap) {
+  __shared__ KeyRule s_rules[kMaxSampled];
+  for (int t = threadIdx.x; t < a.n_sampled; t += blockDim.x) s_rules[t] = rules[t];
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
   // the attempt's values go straight into p (no separate value registers)
@@ -100,12 +216,7 @@ __global__ void __launch_bounds__(128, GT_SAMPLER_MINB) sampler_kernel(gt_sample
   long long rej_neg = 0, rej_sd = 0, rej_ss = 0, rej_basal = 0;
   bool drained = false;
   auto draw_weight = [&]() {             // population.py:148-153
-    w = 0.0;
-    for (int t = 0; t < a.max_attempts; ++t, ++wctr) {
-      const U4 r = philox4x32_10(wctr, pid, kRoleSamplerWeight, 0u, k0, k1);
-      const double v = A_(a.weight_mean, M_(a.weight_sd, det_inv_norm(u52(r.x, r.y))));
-      if (v > 0.0) { w = v; ++wctr; break; }
-    }
+    w = draw_weight_dev(a, pid, &wctr, k0, k1);
     p[PW] = w;
     attempt = 0;
   };
@@ -166,21 +277,16 @@ __global__ void __launch_bounds__(128, GT_SAMPLER_MINB) sampler_kernel(gt_sample
           park_full = true;   // list full: carry on in this lane
         }
         const uint32_t actr = (uint32_t)(total + attempt);
-        // the normal draws only (lognormals are never negative and have no SD rule)
+        // the normal draws' keys only (lognormals are never negative and have no SD rule)
         bool neg = false, outside = false;
-        auto check = [&](int j, double v) {
-          neg |= v < 0.0;
-          outside |= fabs(S_(v, a.a[j])) > a.b[j];
-          p[a.param_index[j]] = v;
-        };
-#pragma unroll
+#pragma unroll 1
         for (int q = 0; q < kMaxSampled; q += 2) {
           if (q >= a.n_sampled) break;
           const bool n0 = a.kind[q] == 0, n1 = q + 1 < a.n_sampled && a.kind[q + 1] == 0;
           if (!(n0 || n1)) continue;
           const U4 r = philox4x32_10(actr, pid, kRoleSamplerParams, (uint32_t)(q >> 1), k0, k1);
-          if (n0) check(q, sampled_value(a, q, det_inv_norm(u52(r.x, r.y))));
-          if (n1) check(q + 1, sampled_value(a, q + 1, det_inv_norm(u52(r.z, r.w))));
+          if (n0) key_verdict(a, s_rules[q], q, key52(r.x, r.y), neg, outside);
+          if (n1) key_verdict(a, s_rules[q + 1], q + 1, key52(r.z, r.w), neg, outside);
         }
         if (neg) { ++rej_neg; ++attempt; continue; }          // population.py:234-236
         if (outside) { ++rej_sd; ++attempt; continue; }       // population.py:237-244
@@ -196,15 +302,7 @@ __global__ void __launch_bounds__(128, GT_SAMPLER_MINB) sampler_kernel(gt_sample
     if (survivor && go) {
       survivor = false;
       const uint32_t actr = (uint32_t)(total + attempt);
-#pragma unroll
-      for (int q = 0; q < kMaxSampled; q += 2) {
-        if (q >= a.n_sampled) break;
-        const bool l0 = a.kind[q] == 1, l1 = q + 1 < a.n_sampled && a.kind[q + 1] == 1;
-        if (!(l0 || l1)) continue;
-        const U4 r = philox4x32_10(actr, pid, kRoleSamplerParams, (uint32_t)(q >> 1), k0, k1);
-        if (l0) p[a.param_index[q]] = sampled_value(a, q, det_inv_norm(u52(r.x, r.y)));
-        if (l1) p[a.param_index[q + 1]] = sampled_value(a, q + 1, det_inv_norm(u52(r.z, r.w)));
-      }
+      fill_attempt_p(a, actr, pid, k0, k1, p);   // the survivor's values, normals included
       last_surv = (int32_t)actr;
       if (!steady_state_dev(p, a.target_bg, x, &ub)) { ++rej_ss; ++attempt; }
       else if (ub < a.min_basal_uh) { ++rej_basal; ++attempt; }
@@ -225,8 +323,9 @@ __global__ void __launch_bounds__(128, GT_SAMPLER_MINB) sampler_kernel(gt_sample
 }
 
 // One attempt's values (all sampled parameters), counter-addressed.
-__device__ void draw_attempt(const gt_sampler_args& a, uint32_t actr, uint32_t pid, uint32_t k0, uint32_t k1,
-                             double* vals) {
+__device__ __noinline__ void draw_attempt(const gt_sampler_args& a, uint32_t actr, uint32_t pid, uint32_t k0,
+                                          uint32_t k1, double* vals) {
+#pragma unroll 1
   for (int q = 0; q < a.n_sampled; q += 2) {
     const U4 r = philox4x32_10(actr, pid, kRoleSamplerParams, (uint32_t)(q >> 1), k0, k1);
     vals[q] = sampled_value(a, q, det_inv_norm(u52(r.x, r.y)));
@@ -239,10 +338,13 @@ __device__ void draw_attempt(const gt_sampler_args& a, uint32_t actr, uint32_t p
 // survivors), the lowest accepted attempt wins, and only the attempts before
 // it are counted -- exactly the sequential loop's result and rejection
 // counts, 128 attempts per round.
-__global__ void __launch_bounds__(128) straggler_kernel(gt_sampler_args a, const Straggler* park,
+__global__ void __launch_bounds__(kStragBS) straggler_kernel(gt_sampler_args a, const KeyRule* rules,
+                                                        const Straggler* park,
                                                         const unsigned int* n_park, int park_cap,
                                                         unsigned int* next) {
   __shared__ int s_amin, s_last, s_j;
+  __shared__ KeyRule s_rules[kMaxSampled];
+  for (int q = threadIdx.x; q < a.n_sampled; q += blockDim.x) s_rules[q] = rules[q];
   const int t = threadIdx.x;
   const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
   const int n_list = min((int)*n_park, park_cap);
@@ -268,12 +370,7 @@ __global__ void __launch_bounds__(128) straggler_kernel(gt_sampler_args a, const
         total += a0 < a.max_attempts ? a0 : a.max_attempts;
         if (wdraw >= a.max_weight_redraws) break;
         ++wdraw;
-        w = 0.0;                                  // population.py:148-153 (every thread, same draws)
-        for (int q = 0; q < a.max_attempts; ++q, ++wctr) {
-          const U4 r = philox4x32_10(wctr, pid, kRoleSamplerWeight, 0u, k0, k1);
-          const double v = A_(a.weight_mean, M_(a.weight_sd, det_inv_norm(u52(r.x, r.y))));
-          if (v > 0.0) { w = v; ++wctr; break; }
-        }
+        w = draw_weight_dev(a, pid, &wctr, k0, k1);   // population.py:148-153 (every thread, same draws)
         p[PW] = w;
         a0 = 0;
         continue;
@@ -284,14 +381,18 @@ __global__ void __launch_bounds__(128) straggler_kernel(gt_sampler_args a, const
       int reason = 0;        // 1 negative, 2 outside 1 SD, 3 no steady state, 4 basal, 5 accepted
       double ub = 0.0;
       if (valid) {
-        draw_attempt(a, actr, pid, k0, k1, vals);
-        bool neg = false, outside = false;
-        for (int q = 0; q < a.n_sampled; ++q) neg |= vals[q] < 0.0;
-        for (int q = 0; q < a.n_sampled; ++q)
-          if (a.kind[q] == 0 && fabs(S_(vals[q], a.a[q])) > a.b[q]) outside = true;
+        bool neg = false, outside = false;   // the normal draws' keys (as sampler_kernel's phase 1)
+        for (int q = 0; q < a.n_sampled; q += 2) {
+          const bool n0 = a.kind[q] == 0, n1 = q + 1 < a.n_sampled && a.kind[q + 1] == 0;
+          if (!(n0 || n1)) continue;
+          const U4 r = philox4x32_10(actr, pid, kRoleSamplerParams, (uint32_t)(q >> 1), k0, k1);
+          if (n0) key_verdict(a, s_rules[q], q, key52(r.x, r.y), neg, outside);
+          if (n1) key_verdict(a, s_rules[q + 1], q + 1, key52(r.z, r.w), neg, outside);
+        }
         if (neg) reason = 1;
         else if (outside) reason = 2;
         else {
+          draw_attempt(a, actr, pid, k0, k1, vals);
           for (int q = 0; q < a.n_sampled; ++q) p[a.param_index[q]] = vals[q];
           if (!steady_state_dev(p, a.target_bg, x, &ub)) reason = 3;
           else reason = ub < a.min_basal_uh ? 4 : 5;
@@ -366,27 +467,35 @@ int gt_launch_sampler(const gt_sampler_args* a, cudaStream_t st) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gt::sampler_kernel, bs, 0);
   if (per_sm < 1) per_sm = 1;
+  int strag_per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&strag_per_sm, gt::straggler_kernel, gt::kStragBS, 0);
+  if (strag_per_sm < 1) strag_per_sm = 1;
   // persistent grid: at most one resident wave, never more lanes than patients
   const int64_t blocks = std::min<int64_t>((int64_t)sms * per_sm, (a->n + bs - 1) / bs);
   // workspace: patient queue, straggler count and cursor, straggler list
   // ~0.5 % of patients (light body weights: low acceptance) pass 384 attempts
   const int cap = (int)std::min<int64_t>(std::max<int64_t>(1024, a->n / 16), 1 << 22);
-  const size_t head = 64;
+  const size_t head = 64 + sizeof(gt::KeyRule) * gt::kMaxSampled;
   char* ws = nullptr;
   gt_keep_pool_mapped();
   if (cudaMallocAsync(&ws, head + sizeof(gt::Straggler) * (size_t)cap, st) != cudaSuccess) {
     gt_set_error("gt_sample_population: workspace allocation failed");
     return GT_ECUDA;
   }
-  cudaMemsetAsync(ws, 0, head, st);
+  cudaMemsetAsync(ws, 0, 64, st);
   auto* queue = reinterpret_cast<unsigned long long*>(ws);
   auto* n_park = reinterpret_cast<unsigned int*>(ws + 8);
   auto* cursor = reinterpret_cast<unsigned int*>(ws + 16);
+  auto* rules = reinterpret_cast<gt::KeyRule*>(ws + 64);
   auto* park = reinterpret_cast<gt::Straggler*>(ws + head);
-  gt::sampler_kernel<<<(unsigned)blocks, bs, 0, st>>>(*a, queue, park, n_park, cap);
-  int e = gt_check_launch("sampler_kernel");
+  gt::key_rules_kernel<<<1, 3 * gt::kMaxSampled, 0, st>>>(*a, rules);
+  int e = gt_check_launch("key_rules_kernel");
   if (e == GT_OK) {
-    gt::straggler_kernel<<<(unsigned)(2 * sms), bs, 0, st>>>(*a, park, n_park, cap, cursor);
+    gt::sampler_kernel<<<(unsigned)blocks, bs, 0, st>>>(*a, rules, queue, park, n_park, cap);
+    e = gt_check_launch("sampler_kernel");
+  }
+  if (e == GT_OK) {
+    gt::straggler_kernel<<<(unsigned)(sms * strag_per_sm), gt::kStragBS, 0, st>>>(*a, rules, park, n_park, cap, cursor);
     e = gt_check_launch("straggler_kernel");
   }
   cudaFreeAsync(ws, st);

@@ -118,14 +118,21 @@ def det_log(x: np.ndarray) -> np.ndarray:
     return de * _LN2_HI + (de * _LN2_LO + logm)
 
 
+# doubles nearest 1/j!, j = 0..14 (Horner coefficients of det_exp)
+_INV_FACT = (1.0, 1.0, 0.5, 0.16666666666666666, 0.041666666666666664, 0.008333333333333333,
+             0.001388888888888889, 0.0001984126984126984, 2.48015873015873e-05, 2.7557319223985893e-06,
+             2.755731922398589e-07, 2.505210838544172e-08, 2.08767569878681e-09, 1.6059043836821613e-10,
+             1.1470745597729725e-11)
+
+
 def det_exp(x: np.ndarray) -> np.ndarray:
     """exp from +,-,*,/ only (device: gt_common.cuh det_exp)."""
     x = np.asarray(x, dtype=np.float64)
     kf = np.floor(x * 1.44269504088896338700e+00 + 0.5)
     r = (x - kf * _LN2_HI) - kf * _LN2_LO
-    s = np.ones_like(r)
-    for j in range(14, 0, -1):
-        s = 1.0 + (r * s) / float(j)
+    s = np.full_like(r, _INV_FACT[14])
+    for j in range(13, -1, -1):
+        s = _INV_FACT[j] + r * s
     out = np.ldexp(s, kf.astype(np.int64))
     out = np.where(x > 709.0, np.inf, out)
     return np.where(x < -745.0, 0.0, out)
