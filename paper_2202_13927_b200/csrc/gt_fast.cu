@@ -107,6 +107,22 @@ namespace gt {
 #ifndef GT_DRAIN32
 #define GT_DRAIN32 6  // instances (GT_PS5 bits) forming the drain address from a 32-bit element offset
 #endif
+#ifndef GT_SCALE
+// States carried in a scaled form (a bit each), so that a per-step multiply
+// folds into the update: 1 S1*hTI, 2 X1*h, 4 G/hS, 8 D1,D2*hTG.
+#define GT_SCALE 15   // -1.7 % three_meal/pid_pump, -0.8 % three_meal/dual_hormone (profiles/r02d_ab_fused.json)
+#endif
+constexpr bool kScS1 = (GT_SCALE & 1) != 0, kScX1 = (GT_SCALE & 2) != 0, kScG = (GT_SCALE & 4) != 0,
+               kScD = (GT_SCALE & 8) != 0;
+#ifndef GT_LAZYZM
+// instances (GT_PS5 bits) whose pipelined draws keep the 4th normal as
+// (radius, angle), its sine taken only at ticks: -3.3 % three_meal/dual_hormone,
+// +0.5 % three_meal/pid_pump (profiles/r02d_ab_fused.json)
+#define GT_LAZYZM 14
+#endif
+#ifndef GT_F01Q
+#define GT_F01Q 0
+#endif
 #ifndef GT_FAST_MINB
 #define GT_FAST_MINB 4  // resident 128-thread blocks per SM (register budget 128)
 #endif
@@ -144,6 +160,7 @@ template <typename R>
 struct PC {
   R invVGw, aG, hTG, aI, hTI, cI, dI, ax1, bx1, ax2, bx2, ax3, bx3;
   R hF01w45, hk12, aK12, hE, rK0, sqE;
+  R hF01Q, Q45;   // GT_F01Q: h F01 / (4.5 VG) and 4.5 VG w (the flux on Q1 directly)
 };
 
 template <typename R>
@@ -155,10 +172,11 @@ __device__ __forceinline__ void make_pc(const double* __restrict__ p, const Uni&
   c.hTG = (R)hTG; c.aG = (R)(1.0 - hTG);
   c.hTI = (R)hTI; c.aI = (R)(1.0 - hTI);
   c.cI = (R)(1.0 - h * p[PKE]); c.dI = (R)(hTI / (p[PVI] * w));
-  c.ax1 = (R)(1.0 - h * p[PKA1]); c.bx1 = (R)(h * p[PKA1] * p[PSIT]);
+  c.ax1 = (R)(1.0 - h * p[PKA1]); c.bx1 = (R)((kScX1 ? h * h : h) * p[PKA1] * p[PSIT]);
   c.ax2 = (R)(1.0 - h * p[PKA2]); c.bx2 = (R)(h * p[PKA2] * p[PSID]);
   c.ax3 = (R)(1.0 - h * p[PKA3]); c.bx3 = (R)(h * p[PKA3] * p[PSIE]);
   c.hF01w45 = (R)(h * p[PF01] * w / 4.5);
+  c.hF01Q = (R)(h * p[PF01] / (4.5 * p[PVG])); c.Q45 = (R)(4.5 * p[PVG] * w);
   c.hk12 = (R)hk12; c.aK12 = (R)(1.0 - hk12);
   c.hE = (R)(h * p[PEGP0] * w);
   c.rK0 = (R)(h * 0.003 * 9.0 * p[PVG] * w);
@@ -294,11 +312,15 @@ __device__ __forceinline__ float cos_approx(float x) {
 // Box-Muller in FP32 on the SFU: u1 in [2^-33, 1] (never 0), radius
 // sqrt(-2 ln u1) by MUFU.SQRT (u1 = 1 gives radius 0, as it should), angle
 // 2*pi*u2 in [0, 2*pi).
-__device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float& z0, float& z1) {
+__device__ __forceinline__ void bm_polar(uint32_t a, uint32_t b, float& rad, float& ang) {
   const float u1 = fmaf((float)a, 2.3283064365386963e-10f, 1.1641532182693481e-10f);
-  const float ang = (float)b * 1.4629180792671596e-09f;  // 2*pi * 2^-32
+  ang = (float)b * 1.4629180792671596e-09f;  // 2*pi * 2^-32
   const float t = lg2_approx(u1) * -1.3862943611198906f;  // -2 ln 2 * log2(u1) > 0
-  const float rad = sqrt_approx(t);
+  rad = sqrt_approx(t);
+}
+__device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float& z0, float& z1) {
+  float rad, ang;
+  bm_polar(a, b, rad, ang);
   z0 = rad * cos_approx(ang);
   z1 = rad * sin_approx(ang);
 }
@@ -525,6 +547,11 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       Q1 = (R)x0[IQ1]; Q2 = (R)x0[IQ2]; S1 = (R)x0[IS1]; S2 = (R)x0[IS2]; I = (R)x0[II];
       X1 = (R)x0[IX1]; X2 = (R)x0[IX2]; X3 = (R)x0[IX3]; D1 = (R)x0[ID1]; D2 = (R)x0[ID2];
       G = (R)x0[IGSC]; Z1 = (R)x0[IZ1]; Z2 = (R)x0[IZ2];
+      // scaled carried forms (GT_SCALE); the saved slice state keeps them scaled
+      if (kScS1) S1 = (R)(x0[IS1] * (double)pc.hTI);
+      if (kScX1) X1 = (R)(x0[IX1] * u.h);
+      if (kScG) G = (R)(x0[IGSC] / u.hS);
+      if (kScD) { D1 = (R)(x0[ID1] * (double)pc.hTG); D2 = (R)(x0[ID2] * (double)pc.hTG); }
       if (CTRL == GT_CTRL_PID_PUMP) {  // no glucagon: Z1 = Z2 = 0 throughout (GT_STATUS_BAD_INITIAL_STATE)
         if (alive && (x0[IZ1] != 0.0 || x0[IZ2] != 0.0)) { alive = false; status = GT_STATUS_BAD_INITIAL_STATE; }
         Z1 = 0; Z2 = 0;
@@ -546,7 +573,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       m_ks = m_ke = INT_MAX; gin = 0;
       if (PROTO == GT_PROTO_CSR) {
         const MealT m0 = meal_at(0);
-        m_ks = m0.ks; m_ke = m0.ke; gin = (R)(u.ginK * m0.rate);
+        m_ks = m0.ks; m_ke = m0.ke; gin = (R)(u.ginK * m0.rate * (kScD ? (double)pc.hTG : 1.0));
         if (TRACE) tr_rate = m0.rate;
         sil[(SI_MEALM) * kFastBS] = 0;
         sil[(SI_ANNM) * kFastBS] = 0;
@@ -606,6 +633,11 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       alive = alive && inrange && !was_bad;  // padding lanes read patient 0's slot
     }
 
+    // GT_DEAD_SINK 0: a lane masked from the start (excluded, re-run mask, bad
+    // initial state) counts into its shared bins like any other, and its
+    // counts are never written out; a lane that dies during the run is
+    // aborted and its statistics are discarded by the host either way
+    const bool ran = status == GT_STATUS_OK || status == GT_STATUS_NONFINITE;
     // extremes / hypo-run bookkeeping is needed only for a bin <= trig_lo or >= kb_max
     trig_lo = run39 > 0 ? INT_MAX : max(kb_min, 34);  // 34: bg < 3.9 (THRESHOLDS[34])
     f_lo = run39 > 0 ? INFINITY : fmaxf(f_mn, __int_as_float(kF39Bits));
@@ -620,7 +652,8 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       const int ks = s_mk[0][j][tid];
       if (ks == 0xFFFF) { m_ks = m_ke = INT_MAX; gin = 0; return; }
       m_ks = day_k0 + ks; m_ke = day_k0 + s_mk[1][j][tid];
-      gin = (R)(u.ginK * (s_mc[j][tid] / u.meal_dur_min));  // rate = g / duration (simulation.py:162)
+      gin = (R)(u.ginK * (s_mc[j][tid] / u.meal_dur_min)   // rate = g / duration (simulation.py:162)
+                * (kScD ? (double)pc.hTG : 1.0));
       if (TRACE) tr_rate = s_mc[j][tid] / u.meal_dur_min;
     };
     auto gen_day = [&](int32_t d) {
@@ -646,6 +679,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         if (word == 0u) continue;
         s_hist[w * kFastBS + tid] = 0u;
         if (!inrange || abort_pass) continue;
+        if (!GT_DEAD_SINK && !ran) continue;   // a masked lane's counts are dropped
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           const uint32_t c = (word >> (8 * b)) & 0xFFu;
@@ -677,11 +711,14 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
     constexpr int kShapeBit = (PROTO == GT_PROTO_CSR ? 4 : 1) << (CTRL == GT_CTRL_PID_PUMP ? 0 : 1);
     constexpr bool PIPE = GT_NOISE_PIPE && !(GT_NOPIPE & kShapeBit) && NOISE == GT_NOISE_PHILOX && !AGG;
     constexpr bool PAIRS = (GT_PAIRS & kShapeBit) != 0;
-    float pz0 = 0.f, pz1 = 0.f, pz2 = 0.f, pz3 = 0.f;
+    float pz0 = 0.f, pz1 = 0.f, pz2 = 0.f, pz3 = 0.f;   // GT_LAZYZM: pz3 holds the angle
+    float prad = 0.f;
+    constexpr bool LAZYZM = (GT_LAZYZM & kShapeBit) != 0;
     auto draw_pipe = [&](int32_t kk) {
       const U4 r = philox_draw((uint32_t)kk);
       box_muller(r.x, r.y, pz0, pz1);
-      box_muller(r.z, r.w, pz2, pz3);
+      if (LAZYZM) { bm_polar(r.z, r.w, prad, pz3); pz2 = prad * cos_approx(pz3); }
+      else box_muller(r.z, r.w, pz2, pz3);
     };
     if (PIPE) draw_pipe(ctl_lo * ps);
 
@@ -697,7 +734,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       auto draw_noise = [&]() {
         if (PIPE) {
           z0 = pz0; z1 = pz1; z2 = pz2;
-          if (tick) zm = pz3;
+          if (tick) zm = LAZYZM ? prad * sin_approx(pz3) : pz3;
         } else if (NOISE == GT_NOISE_PHILOX) {
           if (!AGG) {
             const U4 r = philox_draw((uint32_t)k);
@@ -736,7 +773,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           const int32_t m = sil[(SI_MEALM) * kFastBS] + 1;
           sil[(SI_MEALM) * kFastBS] = m;
           const MealT mt = meal_at(m);
-          m_ks = mt.ks; m_ke = mt.ke; gin = (R)(u.ginK * mt.rate);
+          m_ks = mt.ks; m_ke = mt.ke; gin = (R)(u.ginK * mt.rate * (kScD ? (double)pc.hTG : 1.0));
           if (TRACE) tr_rate = mt.rate;
         }
       } else if (tick) {
@@ -821,7 +858,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           const int p = sil[(SI_EXPTR) * kFastBS];
           if (a.ex_announced[ex_lo + p] != 0.0) phase = t_s - a.ex_start_s[ex_lo + p];
         }
-        y = A_((double)G, M_(u.sqrtR, zm));
+        y = A_(kScG ? (double)G * u.hS : (double)G, M_(u.sqrtR, zm));
         if (TRACE) tr_y = y;
       }
       auto control = [&]() {
@@ -940,6 +977,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         day_basal = fma(b_basal, (double)ps, day_basal);  // basal held for the whole period
         if (TRACE) { tr_basal = b_basal; tr_bolus = b_bolus; tr_gluc = b_gluc; }
         hu_ins = (R)fma(b_bolus, u.u_bolus_k, b_basal * u.u_basal_k);   // h * (u[0] + u[1])
+        if (kScS1) hu_ins = hu_ins * pc.hTI;                            // carried S1 is hTI * S1
         hu2 = (R)(b_gluc * u.u_gluc_k);                                 // h * u[2]
         if (b_bolus > 0.0 || b_gluc > 0.0) {
           sdl[(SC_DBOLUS) * kFastBS] += b_bolus;
@@ -999,29 +1037,30 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       const R bgR = (R)bg, zero = 0, one = 1;
       const R ab = HAS_EX ? FMR((R)u.sex, E3, one) : one;
       const R ub = HAS_EX ? FMR((R)u.qex, E2, one) : one;
-      const R x1e = X1 * ab, x2e = X2 * ab;
+      const R x1e = X1 * ab, x2e = X2 * ab;   // (kScX1: x1e is h * X1 * ab)
       // Q1's loop-carried chain is kept short: the Q1-independent terms
       // (gut, Q2 exchange, EGP, noise) are summed first, off the chain, and
       // the Q1 terms enter as one FMA plus the two clamped fluxes
       const R egp = FMR(-pc.hE, X3, pc.hE);
       // pid_pump doses no glucagon: Z2 = 0 exactly and cG * 0 + e == e
       const R hegp = CTRL == GT_CTRL_PID_PUMP ? pos_or_zero(egp) : FMR((R)u.cG, Z2, pos_or_zero(egp));
-      R pq = FMR(pc.hk12, Q2, D2 * pc.hTG) + hegp;
+      R pq = FMR(pc.hk12, Q2, kScD ? D2 : D2 * pc.hTG) + hegp;
       pq = FMR(sqE, z0, pq);
-      const R a1 = FMR(-(R)u.h, x1e, one);                       // 1 - h x1e
-      const R hf01 = MR_(pc.hF01w45, lt_or(bgR, (R)4.5));        // h F01 w min(bg/4.5, 1)
+      const R a1 = kScX1 ? one - x1e : FMR(-(R)u.h, x1e, one);  // 1 - h x1e
+      // h F01 w min(bg/4.5, 1); GT_F01Q: as h F01/(4.5 VG) min(Q1, 4.5 VG w), off the bg multiply
+      const R hf01 = GT_F01Q ? MR_(pc.hF01Q, lt_or(Q1, pc.Q45)) : MR_(pc.hF01w45, lt_or(bgR, (R)4.5));
       const R hren = pos_or_zero(FMR(Q1, (R)u.rK1, -pc.rK0));
       R q1n = FMR(Q1, a1, pq);
       q1n = FMR(-hf01, ub, q1n);
       q1n = q1n - hren;
       // projection max(x, 0) (_kernel.py:175-177): keeps NaN like `if x < 0: x = 0`
-      const R q2n = FMR(Q2, FMR(-(R)u.h, x2e, pc.aK12), ((R)u.h * x1e) * Q1);
+      const R q2n = FMR(Q2, FMR(-(R)u.h, x2e, pc.aK12), (kScX1 ? x1e : (R)u.h * x1e) * Q1);
       const R nQ1 = zero_if_neg(q1n);
       const R nQ2 = zero_if_neg(q2n);
       R nD1 = FMR(D1, FMR(sqG, z1, pc.aG), gin_k);
       R nD2 = FMR(D2, FMR(sqG, z2, pc.aG), D1 * pc.hTG);
       if (CLAMP_GUT) { nD1 = zero_if_neg(nD1); nD2 = zero_if_neg(nD2); }
-      const R nS2 = FMR(S2, pc.aI, S1 * pc.hTI);
+      const R nS2 = FMR(S2, pc.aI, kScS1 ? S1 : S1 * pc.hTI);
       if (!tick || !kLateControl) S1 = FMR(S1, pc.aI, hu_ins);
       const R nI = FMR(I, pc.cI, S2 * pc.dI);
       S2 = nS2;
@@ -1040,7 +1079,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         E1 = FMR(E1, (R)u.aE1, GT_EXFOLD ? (ex_active ? ex_e1_c : (R)0) : (R)(u.bE1 * hrr));
         E2 = nE2; E3 = nE3;
       }
-      G = FMR(G, (R)u.aS, bgR * (R)u.hS);
+      G = kScG ? FMR(G, (R)u.aS, bgR) : FMR(G, (R)u.aS, bgR * (R)u.hS);
       Q1 = nQ1; Q2 = nQ2; D1 = nD1; D2 = nD2;
       if (tick && kLateControl) {  // the controller, then the two states that take its output
         control();
@@ -1081,7 +1120,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           // column address is formed only on that path
           if (__builtin_expect(c == 255u, 0)) {
             asm volatile("st.shared.u8 [%0], 0;" :: "r"(ha) : "memory");
-            if (kb < GT_N_BG_BINS && inrange && !abort_pass) {
+            if (kb < GT_N_BG_BINS && inrange && !abort_pass && (GT_DEAD_SINK || ran)) {
               // 32-bit element offset (the launcher bounds 247 n < 2^31): the drain
               // path then needs fewer scratch registers than a 64-bit index
               if (GT_DRAIN32 & kShapeBit) atomicAdd(a.bg_hist + (uint32_t)(kb * (uint32_t)n + (uint32_t)i), 255);
@@ -1230,9 +1269,12 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       a.hypo_events[i] = ev39;
       a.hypo_events[n + i] = ev30;
       if (a.x_out) {
-        const double xs[NS] = {(double)Q1, (double)Q2, (double)S1, (double)S2, (double)I, (double)X1,
-                               (double)X2, (double)X3, (double)D1, (double)D2, (double)G, (double)Z1,
-                               (double)Z2, (double)E1, (double)E2, (double)E3};
+        const double hTG = (double)pc.hTG;
+        const double xs[NS] = {(double)Q1, (double)Q2, kScS1 ? (double)S1 / (double)pc.hTI : (double)S1,
+                               (double)S2, (double)I, kScX1 ? (double)X1 / u.h : (double)X1,
+                               (double)X2, (double)X3, kScD ? (double)D1 / hTG : (double)D1,
+                               kScD ? (double)D2 / hTG : (double)D2, kScG ? (double)G * u.hS : (double)G,
+                               (double)Z1, (double)Z2, (double)E1, (double)E2, (double)E3};
         for (int k = 0; k < NS; ++k) a.x_out[(int64_t)k * n + i] = xs[k];
       }
     }
