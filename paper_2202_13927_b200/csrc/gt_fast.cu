@@ -114,6 +114,15 @@ namespace gt {
 #endif
 constexpr bool kScS1 = (GT_SCALE & 1) != 0, kScX1 = (GT_SCALE & 2) != 0, kScG = (GT_SCALE & 4) != 0,
                kScD = (GT_SCALE & 8) != 0;
+// per instance (GT_PS5 bits): X2 carried as h*X2, S2 as dI*S2 (then S1 as hTI*dI*S1)
+#ifndef GT_SCX2
+#define GT_SCX2 15   // every instance (profiles/r02d_ab_fused.json)
+#endif
+#ifndef GT_SCS2
+#define GT_SCS2 10   // the dual_hormone instances (a mask per controller keeps the 3-meal generator and
+                     // the CSR form of the same schedule bit-identical)
+#endif
+static_assert(!GT_SCS2 || kScS1, "GT_SCS2: S2 carried as dI*S2 needs S1 carried as hTI*dI*S1");
 #ifndef GT_LAZYZM
 // instances (GT_PS5 bits) whose pipelined draws keep the 4th normal as
 // (radius, angle), its sine taken only at ticks: -3.3 % three_meal/dual_hormone,
@@ -131,6 +140,13 @@ constexpr bool kScS1 = (GT_SCALE & 1) != 0, kScX1 = (GT_SCALE & 2) != 0, kScG = 
 #endif
 constexpr int kFastBS = GT_FAST_BS;
 constexpr int kHistWords = (GT_N_BG_BINS + 3) / 4;  // 62 packed uint8x4 words per lane
+#ifndef GT_HISTLIN
+// 1: each lane's 248 counter bytes contiguous (word tid * 62 + w), so a bin's
+// byte address is one add; 0: word-interleaved (word w * kFastBS + tid), bank
+// conflict free for any bins
+#define GT_HISTLIN 1   // -0.7 to -1.5 % on every instance (profiles/r02d_ab_fused.json)
+#endif
+__device__ __forceinline__ int hword(int w, int tid) { return GT_HISTLIN ? tid * kHistWords + w : w * kFastBS + tid; }
 
 // Launch-uniform constants derived from the fixed parameters (host-computed,
 // passed by value -> constant bank operands, no registers).
@@ -163,7 +179,7 @@ struct PC {
   R hF01Q, Q45;   // GT_F01Q: h F01 / (4.5 VG) and 4.5 VG w (the flux on Q1 directly)
 };
 
-template <typename R>
+template <typename R, bool kScX2>
 __device__ __forceinline__ void make_pc(const double* __restrict__ p, const Uni& u, PC<R>& c) {
   const double h = u.h, w = p[PW];
   // folded in FP64, then rounded once to R
@@ -173,7 +189,7 @@ __device__ __forceinline__ void make_pc(const double* __restrict__ p, const Uni&
   c.hTI = (R)hTI; c.aI = (R)(1.0 - hTI);
   c.cI = (R)(1.0 - h * p[PKE]); c.dI = (R)(hTI / (p[PVI] * w));
   c.ax1 = (R)(1.0 - h * p[PKA1]); c.bx1 = (R)((kScX1 ? h * h : h) * p[PKA1] * p[PSIT]);
-  c.ax2 = (R)(1.0 - h * p[PKA2]); c.bx2 = (R)(h * p[PKA2] * p[PSID]);
+  c.ax2 = (R)(1.0 - h * p[PKA2]); c.bx2 = (R)((kScX2 ? h * h : h) * p[PKA2] * p[PSID]);
   c.ax3 = (R)(1.0 - h * p[PKA3]); c.bx3 = (R)(h * p[PKA3] * p[PSIE]);
   c.hF01w45 = (R)(h * p[PF01] * w / 4.5);
   c.hF01Q = (R)(h * p[PF01] / (4.5 * p[PVG])); c.Q45 = (R)(4.5 * p[PVG] * w);
@@ -414,6 +430,8 @@ template <int PROTO, int NOISE, typename R, bool AGG, bool TRACE, int CTRL, int 
 __global__ void __launch_bounds__(kFastBS, GT_FAST_MINB)
 fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
   constexpr bool HAS_EX = (PROTO == GT_PROTO_CSR);
+  constexpr int kShape = (PROTO == GT_PROTO_CSR ? 4 : 1) << (CTRL == GT_CTRL_PID_PUMP ? 0 : 1);
+  constexpr bool kScX2 = (GT_SCX2 & kShape) != 0, kScS2 = (GT_SCS2 & kShape) != 0;
   constexpr bool CLAMP_GUT = (NOISE == GT_NOISE_INJECTED);
   // s_thr[k+1] = bits of THRESHOLDS[k]; s_thr[0] = -inf, s_thr[247] = +inf
   __shared__ long long s_thr[GT_N_THRESHOLDS + 2];
@@ -448,7 +466,8 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
   // shared address of this lane's bin-0 byte, opaque to the compiler so it
   // stays in one register instead of being rebuilt every step
   uint32_t hist_lane;
-  asm("mov.b32 %0, %1;" : "=r"(hist_lane) : "r"((uint32_t)__cvta_generic_to_shared(s_hist) + 4u * tid));
+  asm("mov.b32 %0, %1;" : "=r"(hist_lane)
+      : "r"((uint32_t)__cvta_generic_to_shared(s_hist) + 4u * (GT_HISTLIN ? kHistWords * tid : tid)));
   // PSC > 0: the controller period's step count is a compile-time constant and
   // the period's plain steps are unrolled (no loop control, no register
   // rotation of the loop-carried noise / states)
@@ -500,7 +519,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       double p[NP];
 #pragma unroll
       for (int k = 0; k < NP; ++k) p[k] = a.params[ii * NP + k];
-      make_pc(p, u, pc);
+      make_pc<R, kScX2>(p, u, pc);
     }
     R sqE = opaque(pc.sqE), sqG = (R)u.sqG;   // kept, not re-derived from the parameters in HBM
     if (NOISE == GT_NOISE_INJECTED && a.has_noise[ii] == 0) { sqE = 0; sqG = 0; }
@@ -548,8 +567,10 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       X1 = (R)x0[IX1]; X2 = (R)x0[IX2]; X3 = (R)x0[IX3]; D1 = (R)x0[ID1]; D2 = (R)x0[ID2];
       G = (R)x0[IGSC]; Z1 = (R)x0[IZ1]; Z2 = (R)x0[IZ2];
       // scaled carried forms (GT_SCALE); the saved slice state keeps them scaled
-      if (kScS1) S1 = (R)(x0[IS1] * (double)pc.hTI);
+      if (kScS1) S1 = (R)(x0[IS1] * (double)pc.hTI * (kScS2 ? (double)pc.dI : 1.0));
+      if (kScS2) S2 = (R)(x0[IS2] * (double)pc.dI);
       if (kScX1) X1 = (R)(x0[IX1] * u.h);
+      if (kScX2) X2 = (R)(x0[IX2] * u.h);
       if (kScG) G = (R)(x0[IGSC] / u.hS);
       if (kScD) { D1 = (R)(x0[ID1] * (double)pc.hTG); D2 = (R)(x0[ID2] * (double)pc.hTG); }
       if (CTRL == GT_CTRL_PID_PUMP) {  // no glucagon: Z1 = Z2 = 0 throughout (GT_STATUS_BAD_INITIAL_STATE)
@@ -601,7 +622,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       for (int q = 0; q < N_SC; ++q) sdl[(q) * kFastBS] = LDD(SD_SC0 + q);
       for (int q = 0; q < N_SI; ++q) sil[(q) * kFastBS] = LDI(SV_SI0 + q);
       // the histogram counters carried over from the previous slice
-      for (int w = 0; w < kHistWords; ++w) s_hist[w * kFastBS + tid] = (uint32_t)LDI(SV_H0 + w);
+      for (int w = 0; w < kHistWords; ++w) s_hist[hword(w, tid)] = (uint32_t)LDI(SV_H0 + w);
       asm volatile("" ::: "memory");  // before the asm increments
       if (PROTO == GT_PROTO_THREE_MEAL) {
         for (int j = 0; j < 3; ++j) {
@@ -675,9 +696,9 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
     auto flush_hist = [&]() {
       asm volatile("" ::: "memory");  // order after the asm increments
       for (int w = 0; w < kHistWords; ++w) {
-        const uint32_t word = s_hist[w * kFastBS + tid];
+        const uint32_t word = s_hist[hword(w, tid)];
         if (word == 0u) continue;
-        s_hist[w * kFastBS + tid] = 0u;
+        s_hist[hword(w, tid)] = 0u;
         if (!inrange || abort_pass) continue;
         if (!GT_DEAD_SINK && !ran) continue;   // a masked lane's counts are dropped
 #pragma unroll
@@ -978,6 +999,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         if (TRACE) { tr_basal = b_basal; tr_bolus = b_bolus; tr_gluc = b_gluc; }
         hu_ins = (R)fma(b_bolus, u.u_bolus_k, b_basal * u.u_basal_k);   // h * (u[0] + u[1])
         if (kScS1) hu_ins = hu_ins * pc.hTI;                            // carried S1 is hTI * S1
+        if (kScS2) hu_ins = hu_ins * pc.dI;                             //   (times dI)
         hu2 = (R)(b_gluc * u.u_gluc_k);                                 // h * u[2]
         if (b_bolus > 0.0 || b_gluc > 0.0) {
           sdl[(SC_DBOLUS) * kFastBS] += b_bolus;
@@ -1054,7 +1076,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       q1n = FMR(-hf01, ub, q1n);
       q1n = q1n - hren;
       // projection max(x, 0) (_kernel.py:175-177): keeps NaN like `if x < 0: x = 0`
-      const R q2n = FMR(Q2, FMR(-(R)u.h, x2e, pc.aK12), (kScX1 ? x1e : (R)u.h * x1e) * Q1);
+      const R q2n = FMR(Q2, kScX2 ? pc.aK12 - x2e : FMR(-(R)u.h, x2e, pc.aK12), (kScX1 ? x1e : (R)u.h * x1e) * Q1);
       const R nQ1 = zero_if_neg(q1n);
       const R nQ2 = zero_if_neg(q2n);
       R nD1 = FMR(D1, FMR(sqG, z1, pc.aG), gin_k);
@@ -1062,7 +1084,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       if (CLAMP_GUT) { nD1 = zero_if_neg(nD1); nD2 = zero_if_neg(nD2); }
       const R nS2 = FMR(S2, pc.aI, kScS1 ? S1 : S1 * pc.hTI);
       if (!tick || !kLateControl) S1 = FMR(S1, pc.aI, hu_ins);
-      const R nI = FMR(I, pc.cI, S2 * pc.dI);
+      const R nI = FMR(I, pc.cI, kScS2 ? S2 : S2 * pc.dI);
       S2 = nS2;
       X1 = FMR(X1, pc.ax1, I * pc.bx1);
       X2 = FMR(X2, pc.ax2, I * pc.bx2);
@@ -1112,7 +1134,8 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         if (GT_DEAD_SINK) kb = alive ? kb : GT_N_BG_BINS;  // dead lanes count into the padding bin 247
         {  // byte ((kb >> 2) * kFastBS + tid) * 4 + (kb & 3)
           GT_CHECK(kb >= 0 && kb <= GT_N_BG_BINS, "histogram bin");
-          const uint32_t ha = hist_lane + (uint32_t)(kb & ~3) * (uint32_t)kFastBS + (uint32_t)(kb & 3);
+          const uint32_t ha = GT_HISTLIN ? hist_lane + (uint32_t)kb
+                                         : hist_lane + (uint32_t)(kb & ~3) * (uint32_t)kFastBS + (uint32_t)(kb & 3);
           uint32_t c;
           asm volatile("{\n\t.reg .u32 t;\n\tld.shared.u8 t, [%1];\n\tadd.u32 %0, t, 1;\n\t"
                        "st.shared.u8 [%1], %0;\n\t}" : "=r"(c) : "r"(ha));
@@ -1233,8 +1256,8 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         for (int q = 0; q < N_SI; ++q) STI(SV_SI0 + q, sil[(q) * kFastBS]);
         asm volatile("" ::: "memory");  // after the asm increments
         for (int w = 0; w < kHistWords; ++w) {
-          STI(SV_H0 + w, (int)s_hist[w * kFastBS + tid]);
-          s_hist[w * kFastBS + tid] = 0u;
+          STI(SV_H0 + w, (int)s_hist[hword(w, tid)]);
+          s_hist[hword(w, tid)] = 0u;
         }
         if (PROTO == GT_PROTO_THREE_MEAL) {
           for (int j = 0; j < 3; ++j) {
@@ -1270,9 +1293,11 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       a.hypo_events[n + i] = ev30;
       if (a.x_out) {
         const double hTG = (double)pc.hTG;
-        const double xs[NS] = {(double)Q1, (double)Q2, kScS1 ? (double)S1 / (double)pc.hTI : (double)S1,
-                               (double)S2, (double)I, kScX1 ? (double)X1 / u.h : (double)X1,
-                               (double)X2, (double)X3, kScD ? (double)D1 / hTG : (double)D1,
+        const double fS1 = (kScS1 ? (double)pc.hTI : 1.0) * (kScS2 ? (double)pc.dI : 1.0);
+        const double xs[NS] = {(double)Q1, (double)Q2, (double)S1 / fS1,
+                               kScS2 ? (double)S2 / (double)pc.dI : (double)S2, (double)I,
+                               kScX1 ? (double)X1 / u.h : (double)X1,
+                               kScX2 ? (double)X2 / u.h : (double)X2, (double)X3, kScD ? (double)D1 / hTG : (double)D1,
                                kScD ? (double)D2 / hTG : (double)D2, kScG ? (double)G * u.hS : (double)G,
                                (double)Z1, (double)Z2, (double)E1, (double)E2, (double)E3};
         for (int k = 0; k < NS; ++k) a.x_out[(int64_t)k * n + i] = xs[k];
