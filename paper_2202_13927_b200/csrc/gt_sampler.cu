@@ -133,6 +133,12 @@ __global__ void key_rules_kernel(gt_sampler_args a, KeyRule* rules) {
   const unsigned long long e = K > m ? K - m : 0;
   rules[j].e[f] = e;
   rules[j].w[f] = flips ? K + m + 1 - e : 0;
+  // a normal entry whose value is not increasing in k (sd <= 0 or not finite):
+  // no flip structure to rely on, every draw is evaluated exactly
+  if (a.kind[j] == 0 && f == 0 && !(a.b[j] > 0.0 && a.b[j] < INFINITY && fabs(a.a[j]) < INFINITY)) {
+    rules[j].e[0] = 0;
+    rules[j].w[0] = kKeyEnd + 1;
+  }
   (f == 0 ? rules[j].k_neg : f == 1 ? rules[j].k_lo : rules[j].k_hi) = K;
 }
 

@@ -31,6 +31,29 @@ def test_device_sampler_bitwise_vs_oracle_twin(dev, oracle, seed, pid0, n):
         assert np.array_equal(d[k].cpu().numpy(), o[k]), k
 
 
+def test_device_sampler_bitwise_vs_oracle_twin_on_edited_table(dev, oracle):
+    """The cheap rules are decided on the uniform key with flip points found on
+    the device (gt_sampler.cu key_rules_kernel); tables whose normal entries
+    reject far more often (F01 sd x3: a value is negative below z = -1.47),
+    have a zero sd (no variability, the 1-SD rule never fires) or a wide sd
+    still give the sequential twin's populations and counters bit for bit."""
+    import dataclasses
+    from paper_2202_13927_b200 import engine
+    from paper_2202_13927_b200.layout import PARAM_INDEX, PARAM_NAMES
+    from paper_2202_13927_b200.tables import default_parameter_table
+    table = default_parameter_table()
+    s = dict(table.sampled)
+    s["F01"] = dataclasses.replace(s["F01"], sd=3 * s["F01"].sd)
+    s["EGP0"] = dataclasses.replace(s["EGP0"], sd=0.0)
+    s["ka2"] = dataclasses.replace(s["ka2"], sd=0.5 * s["ka2"].mean)
+    table = dataclasses.replace(table, sampled=s)
+    d = engine.sample_population(3, 3000, table, device=dev, max_attempts=2000, max_weight_redraws=2)
+    o = oracle.sample_patients(table, 3, 0, 3000, PARAM_INDEX, PARAM_NAMES, max_attempts=2000, max_weight_redraws=2)
+    for k in ("params", "x0", "u_basal", "attempts", "status", "reject_counts"):
+        assert np.array_equal(d[k].cpu().numpy(), o[k]), k
+    assert int(o["reject_counts"][0]) > 0   # the negative-value rule fired
+
+
 def test_device_sampler_distribution_matches_reference(dev):
     from paper_2202_13927_b200.population import generate_population
     pop = generate_population(2, 4000, device=dev, on_exhausted="redraw_weight")
