@@ -21,6 +21,8 @@ patients of a call run on the device.
 from __future__ import annotations
 
 import math
+import itertools
+import operator
 import os
 import time
 from dataclasses import dataclass
@@ -77,6 +79,23 @@ def pack_params(values: dict) -> np.ndarray:
     if missing:
         raise ValueError(f"missing parameters: {missing}")
     return np.array([float(values[n]) for n in PARAM_NAMES])
+
+
+_PARAM_GETTER = operator.itemgetter(*PARAM_NAMES)
+
+
+def pack_params_many(values_seq) -> np.ndarray:
+    """pack_params over a sequence of parameter maps -> [n, 30] float64 (one
+    C-level item lookup per map; the same values and the same error)."""
+    seq = list(values_seq)
+    try:
+        flat = np.fromiter(itertools.chain.from_iterable(map(_PARAM_GETTER, seq)), dtype=np.float64,
+                           count=len(seq) * len(PARAM_NAMES))
+    except KeyError:
+        for v in seq:
+            pack_params(v)   # raises the reference-shaped ValueError
+        raise
+    return flat.reshape(len(seq), len(PARAM_NAMES))
 
 
 def _controller_inputs(controller):

@@ -40,12 +40,12 @@ def population_to_device(population, basal_scale: float, device):
     t = engine.torch()
     if hasattr(population, "params_device"):
         return population.pid0, population.params_device, population.basal_device * basal_scale
-    from .simulation import pack_params
+    from .simulation import pack_params_many
     ids = np.array([int(pt.id) for pt, _ in population], dtype=np.int64)
     if ids.size and not np.array_equal(ids, ids[0] + np.arange(ids.size)):
         raise SimulationError("the fused path keys RNG streams by contiguous patient ids")
-    params = np.stack([pack_params(ps.values) for _, ps in population])
-    basal = np.array([float(ps.u_basal_u_per_h) * basal_scale for _, ps in population])
+    params = pack_params_many([ps.values for _, ps in population])
+    basal = np.array([ps.u_basal_u_per_h for _, ps in population], dtype=np.float64) * basal_scale
     return int(ids[0]), engine.dev(params, t.float64, device), engine.dev(basal, t.float64, device)
 
 

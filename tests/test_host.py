@@ -315,3 +315,17 @@ def test_merge_monoid_properties():
         assert _eq(merge(a, b), merge(b, a))
         assert _eq(merge(merge(a, b), c), merge(a, merge(b, c)))
     laws()
+
+
+def test_pack_params_many_equals_pack_params():
+    """The drop-in run_trial packs the reference's parameter maps in one pass
+    (simulation.pack_params_many); same values and same error as pack_params."""
+    from paper_2202_13927_b200.simulation import pack_params, pack_params_many
+    from paper_2202_13927_b200.tables import nominal_values
+    vs = [nominal_values(50.0 + 0.37 * i) for i in range(257)]
+    assert np.array_equal(pack_params_many(vs), np.stack([pack_params(v) for v in vs]))
+    assert pack_params_many([]).shape == (0, 30)
+    bad = dict(vs[0])
+    del bad["k12"]
+    with pytest.raises(ValueError, match="missing parameters"):
+        pack_params_many(vs[:2] + [bad])
