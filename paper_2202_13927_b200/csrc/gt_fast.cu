@@ -105,7 +105,8 @@ namespace gt {
                     // -0.7 % three_meal/pid_pump, +1.1 % three_meal/dual_hormone (profiles/r02_ab_code_shape.json)
 #endif
 #ifndef GT_DRAIN32
-#define GT_DRAIN32 6  // instances (GT_PS5 bits) forming the drain address from a 32-bit element offset
+#define GT_DRAIN32 15  // instances (GT_PS5 bits) forming the drain address from a 32-bit element offset
+                       // (-0.6 % three_meal/pid_pump, -0.9 % csr/dual_hormone, profiles/r02d_ab_fused.json)
 #endif
 #ifndef GT_SCALE
 // States carried in a scaled form (a bit each), so that a per-step multiply
