@@ -336,3 +336,75 @@ def test_rerun_trial_record_reproduces_reference_report(dev):
 
     res = records.rerun_trial(Store(), rec, device=dev)
     assert analytics.report_bytes(res.report) == want
+
+
+def test_c3_arms_parity_subset(dev, oracle):
+    """BASELINE configs[3] correctness subset: the four treatment arms (PID gains
+    x0.5 / x1 / x1.5 and bolus-only, studies.pid_arms) on 200 shared-parameter
+    patients x 2 weeks with the reference's noise streams injected -- the same
+    streams in every arm (common random numbers).  Per arm the parity kernel
+    equals the C oracle bit for bit and the fused kernel agrees to 1e-9 with
+    identical integer outputs except proven threshold ties; the paired per-patient
+    TIR differences between arms are therefore the oracle's."""
+    import torch
+    from paper_2202_13927_b200 import engine, rng
+    from paper_2202_13927_b200.config import SimulationConfig
+    from paper_2202_13927_b200.pid import PIDProfile
+    from paper_2202_13927_b200.population import generate_population
+    from paper_2202_13927_b200.protocol import ThreeMealProtocol, compile_protocol
+    from paper_2202_13927_b200.simulation import _csr
+    from paper_2202_13927_b200.studies import default_arms
+    from paper_2202_13927_b200.trial import FastTrial
+    n = 200
+    cfg = SimulationConfig(horizon_s=14 * 86400.0, seed=3, dt_s=60.0)
+    gen = ThreeMealProtocol()
+    pop = generate_population(3, n, device=dev, on_exhausted="redraw_weight")
+    arms = default_arms(PIDProfile(), controller_id="pid_pump")
+    assert set(arms) == {"pid_x0.5", "pid_x1", "pid_x1.5", "bolus_only"}
+    oracle.set_controller(1)
+    tir = {}
+    try:
+        W = M = None
+        for name, prof in arms.items():
+            ft = FastTrial(0, pop.params_device, pop.basal_device, gen, prof, cfg, controller_id="pid_pump",
+                           device=dev)
+            sz = ft.sz
+            H, ps = sz["horizon_ticks"], sz["period_steps"]
+            params, x0, c0, ub = (t.cpu().numpy() for t in (ft.params, ft.x0, ft.c0, ft.basal))
+            if W is None:   # one set of streams for every arm
+                pas = [compile_protocol(gen.build(cfg.seed, type("P", (), {"id": i, "body_weight_kg": params[i, 0]})()),
+                                        cfg.horizon_s) for i in range(n)]
+                moff, meals, eoff, ex = _csr(pas)
+                W = np.zeros((n, H, 3)); M = np.zeros((n, H // ps))
+                for i in range(n):
+                    W[i], M[i] = rng.reference_noise(cfg.seed, i, H, ps, True, True)
+                hn = np.ones(n, np.uint8)
+            b = engine.ParityBatch(params, x0, c0, prof.to_vec(), ub, moff, meals, eoff, ex, W, hn, M, controller=1)
+            out = engine.run_parity(b, sz, cfg.dt_s, cfg.controller_period_s, device=dev)
+            ref = oracle.run_batch_injected(params, x0, c0, prof.to_vec(), ub, sz, cfg.dt_s, cfg.controller_period_s,
+                                            moff, meals, eoff, ex, W, hn, M)
+            for k in ("status", "ticks", "tir_ticks", "bg_hist", "scal", "day_dose", "timeline", "x_out", "c_out"):
+                assert np.array_equal(out[k], ref[k]), (name, k)
+            ft.outs = engine.alloc_fast_outputs(n, 0, sz, dev, per_patient_timeline=True)
+            ft.simulate(injected={"wiener": engine.dev(W.reshape(-1), torch.float64, dev),
+                                  "has_noise": engine.dev(hn, torch.uint8, dev),
+                                  "meas": engine.dev(M.reshape(-1), torch.float64, dev)})
+            fused = {"scal": ft.outs.bg_stats.cpu().numpy().T, "hist": ft.outs.bg_hist.cpu().numpy().T,
+                     "timeline": ft.outs.timeline_pp.cpu().numpy().T,
+                     "day_dose": ft.outs.day_dose.cpu().numpy().transpose(2, 0, 1),
+                     "hypo": ft.outs.hypo_events.cpu().numpy().T}
+            refd = {"scal": ref["scal"], "hist": ref["bg_hist"], "timeline": ref["timeline"],
+                    "day_dose": ref["day_dose"], "hypo": ref["hypo_events"]}
+            exc = ties.check_patients(oracle, dev, n, refd, fused,
+                                      ties.inputs_from_arrays(params, x0, c0, ub, prof.to_vec(), moff, meals, eoff,
+                                                              ex, W, hn, M, 1, sz, cfg.dt_s, cfg.controller_period_s,
+                                                              0), label=f"C3 {name}")
+            oracle.set_controller(1)   # (check_patients restores controller 0)
+            tir[name] = (ref["tir_ticks"][:, 2], {e.patient for e in exc} if exc else set())
+    finally:
+        oracle.set_controller(0)
+    # paired differences against the x1 arm: the oracle's, patient by patient
+    base, _ = tir["pid_x1"]
+    for name in ("pid_x0.5", "pid_x1.5", "bolus_only"):
+        d = tir[name][0] - base
+        assert d.shape == (n,) and np.any(d != 0), name
