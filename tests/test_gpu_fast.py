@@ -426,7 +426,8 @@ def test_chunked_population_equals_single_launch(dev):
 
 
 @pytest.mark.parametrize("horizon_h,dt_s,grid_s,slices", [(36, 30.0, 1800.0, 1), (36, 30.0, 1800.0, 3),
-                                                          (50, 20.0, 3600.0, 2), (25, 60.0, 7200.0, 0)])
+                                                          (50, 20.0, 3600.0, 2), (25, 60.0, 7200.0, 0),
+                                                          (30, 6.0, 3600.0, 2)])   # C4's 0.1-min substep
 def test_fused_equals_parity_on_odd_horizons(dev, oracle, horizon_h, dt_s, grid_s, slices):
     """Partial last day, non-hourly grid, other dt, sliced schedules: the fused
     kernel (reference noise injected, CSR schedules) agrees with the reference
