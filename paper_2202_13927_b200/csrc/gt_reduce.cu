@@ -11,6 +11,10 @@
 namespace gt {
 
 constexpr int kRedBS = 256;
+#ifndef GT_RED_UNROLL
+#define GT_RED_UNROLL 8
+#endif
+constexpr int kRedUnroll = GT_RED_UNROLL;
 constexpr int kTirBins = GT_TIR_BINS + 1;
 constexpr int kDoseBins = GT_DOSE_BINS + 1;
 
@@ -119,13 +123,27 @@ __global__ void reduce_init_kernel(gt_reduce_args a, Worst* wblk, int nblk) {
   if (t < nblk) wblk[t] = Worst{LLONG_MAX, LLONG_MAX, LLONG_MAX};
 }
 
+// One count per valid lane into h[bin]: lanes with the same bin are merged
+// (match.any) and their leader adds the group size, so the 32 lanes of a warp
+// -- whose patients mostly share a bin (similar daily doses) -- cost one
+// shared-memory atomic per distinct bin instead of 32 serialised ones.
+// Called by all 32 lanes.
+__device__ __forceinline__ void warp_hist_add(unsigned* h, int bin, bool valid) {
+  const unsigned vm = __ballot_sync(0xffffffffu, valid);
+  const unsigned grp = __match_any_sync(0xffffffffu, valid ? bin : -1) & vm;
+  const int lane = threadIdx.x & 31;
+  if (valid && (grp & ((1u << lane) - 1u)) == 0u) atomicAdd(&h[bin], (unsigned)__popc(grp));
+}
+
 __global__ void __launch_bounds__(kRedBS) reduce_patients_kernel(gt_reduce_args a, Worst* wblk) {
   __shared__ unsigned long long s_bg[GT_N_BG_BINS];
   __shared__ int s_bmin[GT_N_THRESHOLDS], s_bmax[GT_N_THRESHOLDS];
-  __shared__ unsigned long long s_tirh[GT_N_RANGES * kTirBins];
-  __shared__ unsigned long long s_doseh[3 * kDoseBins];
-  __shared__ unsigned long long s_mh[2 * kTirBins];  // hypo-event histograms
-  __shared__ unsigned long long s_mr[3 * kTirBins];  // tbr70, tar180 combined-range hists
+  // per-block patient histograms: 32-bit counts (a block folds at most
+  // kRedBS patients per pass), filled by warp-aggregated adds (warp_hist_add)
+  __shared__ unsigned s_tirh[GT_N_RANGES * kTirBins];
+  __shared__ unsigned s_doseh[3 * kDoseBins];
+  __shared__ unsigned s_mh[2 * kTirBins];  // hypo-event histograms
+  __shared__ unsigned s_mr[3 * kTirBins];  // tbr70, tar180 combined-range hists
   __shared__ unsigned long long s_tir[GT_N_RANGES];
   __shared__ long long s_misc[8];  // n_ok, n_abort, sum_fp, d0, d1, d2, minb, maxb
   __shared__ unsigned long long s_carry[4];  // carry words of sum_fp, d0, d1, d2
@@ -156,8 +174,10 @@ __global__ void __launch_bounds__(kRedBS) reduce_patients_kernel(gt_reduce_args 
                     stv == GT_STATUS_BAD_INITIAL_STATE);
     // ---- histogram, below-threshold envelope, TIR ticks
     int cum = 0, c25 = 0, c34 = 0, c95 = 0, c134 = 0;
+    const int* hcol = a.bg_hist + (ok ? i : 0);
+#pragma unroll (kRedUnroll)
     for (int b = 0; b < GT_N_BG_BINS; ++b) {
-      const int v = ok ? a.bg_hist[(int64_t)b * n + i] : 0;
+      const int v = ok ? __ldg(hcol + (int64_t)b * n) : 0;
       cum += v;  // below[b] = cumsum(hist)[b] (analytics.py:129-131)
       if (b == 25) c25 = cum;
       if (b == 34) c34 = cum;
@@ -175,25 +195,27 @@ __global__ void __launch_bounds__(kRedBS) reduce_patients_kernel(gt_reduce_args 
       if (lane == 0 && sv) atomicAdd(&s_bg[b], (unsigned long long)sv);
     }
     const int tir[5] = {c25, c34 - c25, c95 - c34, c134 - c95, cum - c134};
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+      // analytics.py:240: min(TIR_BINS, ticks*200 // horizon)
+      long long fb = ((long long)tir[r] * GT_TIR_BINS) / H;
+      if (fb > GT_TIR_BINS) fb = GT_TIR_BINS;
+      warp_hist_add(s_tirh, r * kTirBins + (int)fb, ok);
+    }
+    // BASELINE metrics: TBR<70 = r0+r1, TAR>180 = r3+r4 (TIR, TBR<54, TAR>250 are r2, r0, r4)
+    const int comb[2] = {tir[0] + tir[1], tir[3] + tir[4]};
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      long long fb = ((long long)comb[q] * GT_TIR_BINS) / H;
+      if (fb > GT_TIR_BINS) fb = GT_TIR_BINS;
+      warp_hist_add(s_mr, q * kTirBins + (int)fb, ok);
+    }
+    {
+      const int e39 = ok ? a.hypo_events[i] : 0, e30 = ok ? a.hypo_events[n + i] : 0;
+      warp_hist_add(s_mh, min(e39, GT_TIR_BINS), ok);
+      warp_hist_add(s_mh, kTirBins + min(e30, GT_TIR_BINS), ok);
+    }
     if (ok) {
-#pragma unroll
-      for (int r = 0; r < 5; ++r) {
-        // analytics.py:240: min(TIR_BINS, ticks*200 // horizon)
-        long long fb = ((long long)tir[r] * GT_TIR_BINS) / H;
-        if (fb > GT_TIR_BINS) fb = GT_TIR_BINS;
-        atomicAdd(&s_tirh[r * kTirBins + fb], 1ull);
-      }
-      // BASELINE metrics: TBR<70 = r0+r1, TAR>180 = r3+r4 (TIR, TBR<54, TAR>250 are r2, r0, r4)
-      const int comb[2] = {tir[0] + tir[1], tir[3] + tir[4]};
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        long long fb = ((long long)comb[q] * GT_TIR_BINS) / H;
-        if (fb > GT_TIR_BINS) fb = GT_TIR_BINS;
-        atomicAdd(&s_mr[q * kTirBins + fb], 1ull);
-      }
-      const int e39 = a.hypo_events[i], e30 = a.hypo_events[n + i];
-      atomicAdd(&s_mh[min(e39, GT_TIR_BINS)], 1ull);
-      atomicAdd(&s_mh[kTirBins + min(e30, GT_TIR_BINS)], 1ull);
       if (a.metric_tir) {
         const float fH = (float)H;
         a.metric_tir[i] = tir[2] / fH;
@@ -228,20 +250,25 @@ __global__ void __launch_bounds__(kRedBS) reduce_patients_kernel(gt_reduce_args 
       const double width = k == 2 ? 10.0 : 0.5;  // DOSE_BIN_WIDTH, analytics.py:36
       const double dt = a.dt_s;
       // day_totals[:, 0] = day_dose[:, 0] * dt_s / 3600.0 (analytics.py:126)
+      // One pass over the days: numpy's pairwise sum visits every element once,
+      // in index order, so each day's value is binned as the sum reads it.
+      // Every lane walks the days (the bins are warp-aggregated, and the sum's
+      // control flow depends on n_days only); a lane without a patient reads
+      // patient 0's column and counts nothing.
       auto val = [&](int64_t d) {
-        const double v = col[d * stride];
-        return k == 0 ? D_(M_(v, dt), 3600.0) : v;
+        const double v0 = col[d * stride];
+        const double v = k == 0 ? D_(M_(v0, dt), 3600.0) : v0;
+        // Python's floordiv; for the 0.5 U widths (a power of two) and v >= 0
+        // it is exactly floor(2 v): fmod(v, 0.5) is exact and so is v - fmod
+        long long bin = !ok ? 0
+                        : (k < 2 && v >= 0.0) ? (long long)floor(M_(v, 2.0))
+                        : (v == 0.0 ? 0 : (long long)py_floordiv(v, width));
+        if (bin > GT_DOSE_BINS) bin = GT_DOSE_BINS;
+        warp_hist_add(s_doseh, k * kDoseBins + (int)bin, ok);
+        return v;
       };
-      double psum = 0.0;
-      if (ok) {
-        for (int64_t d = 0; d < a.n_days; ++d) {
-          long long bin = (long long)py_floordiv(val(d), width);
-          if (bin > GT_DOSE_BINS) bin = GT_DOSE_BINS;
-          atomicAdd(&s_doseh[k * kDoseBins + bin], 1ull);
-        }
-        psum = pairwise_sum(val, a.n_days);
-      }
-      const long long fp = ok ? __double2ll_rn(psum * kFpScale) : 0;
+      const double psum = pairwise_sum(val, a.n_days);
+      const long long fp = ok ? __double2ll_rn(psum * kFpScale) : 0;   // (0 for a lane without a patient)
       const long long wsf = wsum64(fp);
       if (lane == 0) add_u128((unsigned long long*)&s_misc[3 + k], &s_carry[1 + k], (unsigned long long)wsf);
     }
@@ -278,19 +305,19 @@ __global__ void __launch_bounds__(kRedBS) reduce_patients_kernel(gt_reduce_args 
     atomicMax((long long*)&a.below_max[k], (long long)s_bmax[k]);
   }
   for (int k = tid; k < GT_N_RANGES * kTirBins; k += kRedBS)
-    if (s_tirh[k]) atomicAdd((unsigned long long*)&a.tir_hist[k], s_tirh[k]);
+    if (s_tirh[k]) atomicAdd((unsigned long long*)&a.tir_hist[k], (unsigned long long)s_tirh[k]);
   for (int k = tid; k < 3 * kDoseBins; k += kRedBS)
-    if (s_doseh[k]) atomicAdd((unsigned long long*)&a.dose_hist[k], s_doseh[k]);
+    if (s_doseh[k]) atomicAdd((unsigned long long*)&a.dose_hist[k], (unsigned long long)s_doseh[k]);
   if (a.metric_hist) {
     // rows: 0 tir(normo) 1 tbr70 2 tbr54 3 tar180 4 tar250 5 events<3.9 6 events<3.0
     for (int k = tid; k < kTirBins; k += kRedBS) {
-      if (s_tirh[2 * kTirBins + k]) atomicAdd((unsigned long long*)&a.metric_hist[0 * kTirBins + k], s_tirh[2 * kTirBins + k]);
-      if (s_mr[k]) atomicAdd((unsigned long long*)&a.metric_hist[1 * kTirBins + k], s_mr[k]);
-      if (s_tirh[k]) atomicAdd((unsigned long long*)&a.metric_hist[2 * kTirBins + k], s_tirh[k]);
-      if (s_mr[kTirBins + k]) atomicAdd((unsigned long long*)&a.metric_hist[3 * kTirBins + k], s_mr[kTirBins + k]);
-      if (s_tirh[4 * kTirBins + k]) atomicAdd((unsigned long long*)&a.metric_hist[4 * kTirBins + k], s_tirh[4 * kTirBins + k]);
-      if (s_mh[k]) atomicAdd((unsigned long long*)&a.metric_hist[5 * kTirBins + k], s_mh[k]);
-      if (s_mh[kTirBins + k]) atomicAdd((unsigned long long*)&a.metric_hist[6 * kTirBins + k], s_mh[kTirBins + k]);
+      if (s_tirh[2 * kTirBins + k]) atomicAdd((unsigned long long*)&a.metric_hist[0 * kTirBins + k], (unsigned long long)s_tirh[2 * kTirBins + k]);
+      if (s_mr[k]) atomicAdd((unsigned long long*)&a.metric_hist[1 * kTirBins + k], (unsigned long long)s_mr[k]);
+      if (s_tirh[k]) atomicAdd((unsigned long long*)&a.metric_hist[2 * kTirBins + k], (unsigned long long)s_tirh[k]);
+      if (s_mr[kTirBins + k]) atomicAdd((unsigned long long*)&a.metric_hist[3 * kTirBins + k], (unsigned long long)s_mr[kTirBins + k]);
+      if (s_tirh[4 * kTirBins + k]) atomicAdd((unsigned long long*)&a.metric_hist[4 * kTirBins + k], (unsigned long long)s_tirh[4 * kTirBins + k]);
+      if (s_mh[k]) atomicAdd((unsigned long long*)&a.metric_hist[5 * kTirBins + k], (unsigned long long)s_mh[k]);
+      if (s_mh[kTirBins + k]) atomicAdd((unsigned long long*)&a.metric_hist[6 * kTirBins + k], (unsigned long long)s_mh[kTirBins + k]);
     }
   }
   if (tid < GT_N_RANGES) atomicAdd((unsigned long long*)&a.tir_ticks_total[tid], s_tir[tid]);
