@@ -151,7 +151,11 @@ class FastTrial:
                            self.config.controller_period_s, self.seed, rng.ROLE_DEVICE_NOISE,
                            self.hypo_min_ticks, self.device, meal_spec=self.meal_spec, csr=self.csr,
                            injected=injected, controller_code=self.code, fixed=self.fixed,
-                           rerun_diverged=rerun_diverged, n_slices=self.n_slices,
+                           rerun_diverged=rerun_diverged,
+                           # the re-run passes skip whole warps: one unit per warp (a slice of
+                           # a warp waits for the previous one anyway, and slicing is
+                           # bit-invisible), so a pass with nothing to do is one check per warp
+                           n_slices=1 if rerun_diverged else self.n_slices,
                            noise_agg=self.noise_agg, fp32=self.fp32)
 
     def trace_range(self, lo: int, hi: int):
