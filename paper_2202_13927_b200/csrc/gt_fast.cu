@@ -134,10 +134,13 @@ static_assert(!GT_SCS2 || kScS1, "GT_SCS2: S2 carried as dI*S2 needs S1 carried 
 #define GT_F01Q 0
 #endif
 #ifndef GT_FAST_MINB
-#define GT_FAST_MINB 4  // resident 128-thread blocks per SM (register budget 128)
+#define GT_FAST_MINB 2  // resident 256-thread blocks per SM (register budget 128: 16 warps per SM)
 #endif
 #ifndef GT_FAST_BS
-#define GT_FAST_BS 128  // threads per block (lanes sharing the block's shared-memory slots)
+#define GT_FAST_BS 256  // threads per block (lanes sharing the block's shared-memory slots); 256 against
+                        // 128: -7 % NorthernYear/dual_hormone, -3 % NorthernYear/pid_pump, -0.4 %
+                        // three_meal/pid_pump, +0.3 % three_meal/dual_hormone (profiles/r02d_ab_fused.json).
+                        // The static shared memory (45 KB at 256) must stay under 48 KB.
 #endif
 constexpr int kFastBS = GT_FAST_BS;
 constexpr int kHistWords = (GT_N_BG_BINS + 3) / 4;  // 62 packed uint8x4 words per lane
