@@ -63,7 +63,8 @@ namespace gt {
 #define GT_PAIRS 8      // plain steps in pairs (-4.7 % csr/dual_hormone; +3 to +24 % on three_meal)
 #endif
 #ifndef GT_NOPIPE
-#define GT_NOPIPE 4     // instances drawing each tick's normals at use, not one step ahead (-0.8 % csr/pid_pump)
+#define GT_NOPIPE 0     // instances drawing each tick's normals at use, not one step ahead (csr/pid_pump was -0.8 %
+                        // in 128-thread blocks; pipelined is -0.5 % in 256-thread blocks)
 #endif
 #ifndef GT_LATE
 #define GT_LATE 1       // controller after the tick's Euler update (only S1 / Z1 take its output)
