@@ -38,7 +38,8 @@ from .layout import N_CSTATE, PARAM_NAMES, PR, PSIGEGP, PSIGGUT, TRACE_COLUMNS
 from .protocol import ThreeMealProtocol, compile_protocol, compile_ticks, validate_protocol
 
 MODEL_ID = "hovorka_ext"
-PARITY_CHUNK = 256        # patients per parity launch (bounds injected-noise memory)
+PARITY_CHUNK_MAX = 4096   # patients per parity launch at most
+PARITY_NOISE_BYTES = 1 << 30   # injected-noise bytes per parity launch (host shared memory + device)
 
 
 class SteadyStateError(RuntimeError):
@@ -149,21 +150,26 @@ def _stats_from_parity(out: dict, i: int, config, sz) -> PatientStats:
     return st
 
 
-def _parity_run(items, config, hyper, device, record_trace=False, controller=0):
-    """items: list of (pid, p[30], x0[16], c0[11], basal, ProtocolArrays)."""
+def _parity_run(items, config, hyper, device, record_trace=False, controller=0, noise=None):
+    """items: list of (pid, p[30], x0[16], c0[11], basal, ProtocolArrays);
+    noise: (wiener [n,H,3], meas [n,H/ps], has_noise [n]) already drawn
+    (hostprep), else drawn here from the reference's streams."""
     sz = sizes(config)
     H, ps = sz["horizon_ticks"], sz["period_steps"]
     n = len(items)
-    wiener = np.zeros((n, H, 3))
-    meas = np.zeros((n, H // ps))
-    has_noise = np.zeros(n, dtype=np.uint8)
-    for i, (pid, p, *_rest) in enumerate(items):
-        proc, sens = _noise_flags(p)
-        w, m = rng.reference_noise(config.seed, pid, H, ps, proc, sens)
-        if w is not None:
-            wiener[i] = w
-        has_noise[i] = proc
-        meas[i] = m
+    if noise is not None:
+        wiener, meas, has_noise = noise
+    else:
+        wiener = np.zeros((n, H, 3))
+        meas = np.zeros((n, H // ps))
+        has_noise = np.zeros(n, dtype=np.uint8)
+        for i, (pid, p, *_rest) in enumerate(items):
+            proc, sens = _noise_flags(p)
+            w, m = rng.reference_noise(config.seed, pid, H, ps, proc, sens)
+            if w is not None:
+                wiener[i] = w
+            has_noise[i] = proc
+            meas[i] = m
     moff, meals, eoff, ex = _csr([it[5] for it in items])
     batch = engine.ParityBatch(
         params=np.stack([it[1] for it in items]), x0=np.stack([it[2] for it in items]),
@@ -213,8 +219,8 @@ def _empty_acc(config) -> TrialAccumulator:
 
 def _population_arrays(population, basal_scale):
     ids = np.array([int(pt.id) for pt, _ in population], dtype=np.int64)
-    params = np.stack([pack_params(ps.values) for _, ps in population])
-    basal = np.array([float(ps.u_basal_u_per_h) * basal_scale for _, ps in population])
+    params = pack_params_many([ps.values for _, ps in population])
+    basal = np.array([ps.u_basal_u_per_h for _, ps in population], dtype=np.float64) * basal_scale
     return ids, params, basal
 
 
@@ -261,8 +267,16 @@ def _known_ids():
     return _REGISTRY
 
 
+def _parity_chunk(sz) -> int:
+    """Patients per parity launch: the injected reference noise (~24 B per
+    patient-step) is bounded to PARITY_NOISE_BYTES per chunk."""
+    per = 8 * (3 * sz["horizon_ticks"] + sz["horizon_ticks"] // sz["period_steps"])
+    return int(max(32, min(PARITY_CHUNK_MAX, PARITY_NOISE_BYTES // per)))
+
+
 def _run_trial_parity(population, generator, controller_id, profile, model_id, config,
                       basal_scale, run_meta, trace_dir, progress, device) -> TrialResult:
+    from . import hostprep
     t0 = time.perf_counter()
     ids, params, basal = _population_arrays(population, basal_scale)
     hyper = hyper_vector(profile)
@@ -272,30 +286,75 @@ def _run_trial_parity(population, generator, controller_id, profile, model_id, c
     x0, ok = x0_d.cpu().numpy(), ok_d.cpu().numpy()
     acc = _empty_acc(config)
     record = config.store_trace == "always"
+    sz = sizes(config)
+    H, ps = sz["horizon_ticks"], sz["period_steps"]
+    flags = np.array([_noise_flags(params[i]) for i in range(len(population))], dtype=bool).reshape(-1, 2)
+    # the patients to simulate, in order; the others are aborted at staging
+    run = [i for i in range(len(population)) if ok[i] == GT_STATUS_OK]
+    chunk = _parity_chunk(sz)
+    spans = [run[lo:lo + chunk] for lo in range(0, len(run), chunk)]
+
+    # two page-locked noise blocks, alternated: the workers fill one while the
+    # device reads the other
+    nb = min(chunk, len(run))
+    use_pool = nb >= 64 and hostprep.pool() is not None
+    blocks = hostprep.blocks(nb, H, H // ps, use_pool, count=min(2, len(spans))) if spans else []
+
+    def start(c):
+        # host inputs of chunk c (protocols + the reference's noise streams),
+        # in the worker pool while the previous chunk runs on the device
+        idx = spans[c]
+        return hostprep.prepare(generator, config.seed, [population[i][0] for i in idx], ids[idx],
+                                flags[idx, 0], flags[idx, 1], config.horizon_s, H, H // ps,
+                                block=blocks[c % 2])
+
+    for i in range(len(population)):   # no steady state: aborted at staging (ids kept sorted)
+        if ok[i] != GT_STATUS_OK:
+            acc.add_aborted(int(ids[i]))
     done = 0
-    for lo in range(0, len(population), PARITY_CHUNK):
-        hi = min(lo + PARITY_CHUNK, len(population))
-        items, idx = [], []
-        for i in range(lo, hi):
-            if ok[i] != GT_STATUS_OK:
-                acc.add_aborted(int(ids[i]))
-                continue
-            pa = compile_protocol(generator.build(config.seed, population[i][0]), config.horizon_s)
-            items.append((int(ids[i]), params[i], x0[i], c0[i], basal[i], pa))
-            idx.append(i)
-        if items:
-            out, sz = _parity_run(items, config, hyper, device, record_trace=record, controller=code)
+    tm = ({"setup": time.perf_counter() - t0, "prep_wait": 0.0, "device": 0.0, "fold": 0.0}
+          if os.environ.get("GLUCOSIM_PARITY_TIMING") else None)
+    nxt = None
+    try:
+        nxt = start(0) if spans else None
+        for c, idx in enumerate(spans):
+            ta = time.perf_counter()
+            pas, block = nxt.result()
+            # the other block's chunk (c - 1) is done on the device: refill it now,
+            # while this chunk runs
+            nxt = start(c + 1) if c + 1 < len(spans) else None
+            tb = time.perf_counter()
+            m = len(idx)
+            items = [(int(ids[i]), params[i], x0[i], c0[i], basal[i], pa) for i, pa in zip(idx, pas)]
+            out, _sz = _parity_run(items, config, hyper, device, record_trace=record, controller=code,
+                                   noise=(block.wiener[:m], block.meas[:m], flags[idx, 0].astype(np.uint8)))
+            tc = time.perf_counter()
+            if tm is not None:
+                tm["prep_wait"] += tb - ta
+                tm["device"] += tc - tb
             for j, i in enumerate(idx):
                 if int(out["status"][j]) != GT_STATUS_OK:
                     acc.add_aborted(int(ids[i]))
                     continue
                 acc.add_patient(int(ids[i]), _stats_from_parity(out, j, config, sz))
                 if record and trace_dir is not None:
-                    save_trace(os.path.join(trace_dir, f"patient_{int(ids[i]):06d}.npz"),
-                               out["trace"][j])
-        done = hi
-        if progress:
-            progress(done, len(population))
+                    save_trace(os.path.join(trace_dir, f"patient_{int(ids[i]):06d}.npz"), out["trace"][j])
+            done = idx[-1] + 1
+            if tm is not None:
+                tm["fold"] += time.perf_counter() - tc
+            if progress:
+                progress(done, len(population))
+    finally:
+        if nxt is not None:
+            try:
+                nxt.result()   # let in-flight workers finish with the block before it goes
+            except Exception:
+                pass
+    if tm is not None:
+        print(f"parity run_trial: {len(spans)} chunks of <= {chunk}; " +
+              ", ".join(f"{k} {v:.3f} s" for k, v in tm.items()), flush=True)
+    if progress and done < len(population):
+        progress(len(population), len(population))
     wall_s = time.perf_counter() - t0
     if acc.n_patients == 0:
         raise SimulationError("all simulations diverged; nothing to report")

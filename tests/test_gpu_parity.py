@@ -408,3 +408,27 @@ def test_c3_arms_parity_subset(dev, oracle):
     for name in ("pid_x0.5", "pid_x1.5", "bolus_only"):
         d = tir[name][0] - base
         assert d.shape == (n,) and np.any(d != 0), name
+
+
+def test_parity_run_trial_pooled_host_inputs_equal_serial(dev, monkeypatch):
+    """run_trial(noise="reference") draws the reference's noise streams and
+    builds the protocols in a worker-process pool (hostprep) for chunks of
+    >= 64 patients; the report bytes equal the in-process path's, chunked
+    launches included (PARITY_NOISE_BYTES forced small: 3 chunks)."""
+    from paper_2202_13927_b200 import analytics, hostprep, simulation
+    from paper_2202_13927_b200.config import SimulationConfig
+    from paper_2202_13927_b200.controller import ControllerHyperparameters
+    from paper_2202_13927_b200.population import generate_population
+    from paper_2202_13927_b200.protocol import ThreeMealProtocol
+    cfg = SimulationConfig(horizon_s=2 * 86400.0, seed=11, dt_s=60.0)
+    pop = generate_population(11, 300, device=dev, on_exhausted="redraw_weight").entries()
+    per = 8 * (3 * 2880 + 576)
+    monkeypatch.setattr(simulation, "PARITY_NOISE_BYTES", 100 * per)
+    reports = []
+    for w in ("1", "4"):
+        monkeypatch.setenv("GLUCOSIM_HOST_WORKERS", w)
+        res = simulation.run_trial(pop, ThreeMealProtocol(), "dual_hormone", ControllerHyperparameters(),
+                                   "hovorka_ext", cfg, device=dev)
+        reports.append(analytics.report_bytes(res.report))
+    assert hostprep.workers() == 4
+    assert reports[0] == reports[1]
