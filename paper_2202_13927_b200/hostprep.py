@@ -150,6 +150,8 @@ def fill_noise(w: np.ndarray, m: np.ndarray, seed: int, pids, proc, sens) -> Non
 
 def _noise_task(args):
     name, shape_w, shape_m, lo, hi, seed, pids, proc, sens = args
+    # (spawned workers share the parent's resource tracker: attaching registers
+    # the name again, idempotently, and the parent's unlink releases it)
     shm = SharedMemory(name=name)
     try:
         w = np.ndarray(shape_w, dtype=np.float64, buffer=shm.buf)
