@@ -134,6 +134,16 @@ static_assert(!GT_SCS2 || kScS1, "GT_SCS2: S2 carried as dI*S2 needs S1 carried 
 #ifndef GT_F01Q
 #define GT_F01Q 0
 #endif
+// timing ablations (results wrong): 1 drops the piece
+#ifndef GT_ABL_TL
+#define GT_ABL_TL 0      // timeline points
+#endif
+#ifndef GT_ABL_NOISE
+#define GT_ABL_NOISE 0   // pipelined noise draws (the normals stay constant)
+#endif
+#ifndef GT_ABL_CTRL
+#define GT_ABL_CTRL 0    // the late controller call (the last decision is held)
+#endif
 #ifndef GT_FAST_MINB
 #define GT_FAST_MINB 2  // resident 256-thread blocks per SM (register budget 128: 16 warps per SM)
 #endif
@@ -1026,7 +1036,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       // traced launches: the reference's per-step BG check (_kernel.py:139-141),
       // so the abort tick is exact; other launches check bg_sum after the horizon
       if (TRACE && alive && !(fabs(bg) < INFINITY)) { alive = false; status = GT_STATUS_NONFINITE; death_tick = k; }
-      if (tick && ctl == next_grid_ctl) {  // timeline point (warp-uniform)
+      if (!GT_ABL_TL && tick && ctl == next_grid_ctl) {  // timeline point (warp-uniform)
         next_grid_ctl += u.grid_ctl;
         const long long v = __double2ll_rn(bg * kFpScale);
         // 0 <= v < 2^31 (bg < 128 mmol/L) for every live lane: four 32-bit
@@ -1057,7 +1067,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         tr[0] = (double)k * u.dt; tr[1] = bg; tr[2] = tr_y; tr[3] = gin_k != (R)0 ? tr_rate : 0.0;
         tr[4] = hrr; tr[5] = tr_basal; tr[6] = tr_bolus; tr[7] = tr_gluc;
       }
-      if (PIPE) draw_pipe(k + 1);
+      if (PIPE && !GT_ABL_NOISE) draw_pipe(k + 1);
       else if (!tick) draw_noise();
       // Euler–Maruyama step, re-associated (hovorka.py:76-150)
       // (in R: launch-uniform constants are rounded to R at their use)
@@ -1109,7 +1119,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       G = kScG ? FMR(G, (R)u.aS, bgR) : FMR(G, (R)u.aS, bgR * (R)u.hS);
       Q1 = nQ1; Q2 = nQ2; D1 = nD1; D2 = nD2;
       if (tick && kLateControl) {  // the controller, then the two states that take its output
-        control();
+        if (!GT_ABL_CTRL) control();
         S1 = FMR(S1, pc.aI, hu_ins);
         if (CTRL != GT_CTRL_PID_PUMP) Z1 = FMR(Z1, (R)u.aZ1, hu2);
       }
