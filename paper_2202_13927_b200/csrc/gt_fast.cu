@@ -144,6 +144,12 @@ static_assert(!GT_SCS2 || kScS1, "GT_SCS2: S2 carried as dI*S2 needs S1 carried 
 #ifndef GT_ABL_CTRL
 #define GT_ABL_CTRL 0    // the late controller call (the last decision is held)
 #endif
+#ifndef GT_PIDFLAT
+// instances (GT_PS5 bits) whose pid_pump controller runs its common path
+// without branches (see control()): -0.65 % three_meal/pid_pump, +0.65 %
+// csr/pid_pump (profiles/r02d_ab_fused.json)
+#define GT_PIDFLAT 1
+#endif
 #ifndef GT_FAST_MINB
 #define GT_FAST_MINB 2  // resident 256-thread blocks per SM (register budget 128: 16 warps per SM)
 #endif
@@ -897,13 +903,20 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         y = A_(kScG ? (double)G * u.hS : (double)G, M_(u.sqrtR, zm));
         if (TRACE) tr_y = y;
       }
+      constexpr bool kPidFlat = CTRL == GT_CTRL_PID_PUMP && (GT_PIDFLAT & kShapeBit) != 0;
       auto control = [&]() {
         // ---- controller_step_vec (controller.py:343-458); state in shared
         // memory.  Explicit IEEE operations in the reference's order: the
         // controller is bit-identical to the reference's for identical readings.
         int flags = sil[(SI_FLAGS) * kFastBS];
         double filt = sdl[(SC_FILT) * kFastBS], prev;
-        if (!(flags & 4)) { filt = y; prev = y; flags |= 4; }
+        if (kPidFlat) {   // the same values by selects (no branch: one basic block with the model)
+          const bool init = (flags & 4) != 0;
+          const double fn = A_(M_(u.hc[1], filt), M_(u.hyper[HFILTER], y));
+          prev = init ? filt : y;
+          filt = init ? fn : y;
+          flags |= 4;
+        } else if (!(flags & 4)) { filt = y; prev = y; flags |= 4; }
         else { prev = filt; filt = A_(M_(u.hc[1], filt), M_(u.hyper[HFILTER], y)); }
         sdl[(SC_FILT) * kFastBS] = filt;
         const double trend = S_(filt, prev);
@@ -927,7 +940,34 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           const double qf = M_(vol, u.hc[5]);
           double pulses = floor(qf);
           const double fr = S_(qf, pulses);
-          if (!(fr > 1e-9 && fr < 1.0 - 1e-9 && qf < 1e6)) pulses = floor(D_(vol, u.hyper[7]));
+          const bool exact = fr > 1e-9 && fr < 1.0 - 1e-9 && qf < 1e6;
+          if (kPidFlat) {
+            // the common path without branches (selects, the table lookup on a
+            // clamped index); the division cases and the meal bolus -- a few
+            // ticks per day -- in one rare branch that recomputes exactly what
+            // the branchy form below computes
+            pulses = pulses < 0.0 ? 0.0 : pulses;
+            double delivered = M_(pulses, u.hyper[7]);
+            double susp = S_(vol, delivered);
+            const bool tab = pulses < (double)kPulseTab;
+            b_basal = s_prate[tab ? (int)pulses : 0];
+            if (__builtin_expect(!exact || !tab || announced > 0.0, 0)) {
+              if (!exact) {
+                pulses = floor(D_(vol, u.hyper[7]));
+                if (pulses < 0.0) pulses = 0.0;
+                delivered = M_(pulses, u.hyper[7]);
+                susp = S_(vol, delivered);
+              }
+              b_basal = pulses < (double)kPulseTab ? s_prate[(int)pulses] : D_(delivered, ph);
+              if (announced > 0.0) {
+                double bb = D_(announced, sdl[(SC_ICR) * kFastBS]);
+                if (bb > u.hyper[9]) bb = u.hyper[9];
+                b_bolus = M_(floor(D_(bb, u.hyper[8])), u.hyper[8]);
+              }
+            }
+            sdl[(SC_SUSP) * kFastBS] = susp;
+          } else {
+          if (!exact) pulses = floor(D_(vol, u.hyper[7]));
           if (pulses < 0.0) pulses = 0.0;
           const double delivered = M_(pulses, u.hyper[7]);
           sdl[(SC_SUSP) * kFastBS] = S_(vol, delivered);
@@ -937,6 +977,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
             double bb = D_(announced, sdl[(SC_ICR) * kFastBS]);
             if (bb > u.hyper[9]) bb = u.hyper[9];
             b_bolus = M_(floor(D_(bb, u.hyper[8])), u.hyper[8]);
+          }
           }
         } else {
         const bool exercising = HAS_EX && phase >= 0.0;
