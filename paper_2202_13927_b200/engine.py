@@ -128,8 +128,11 @@ class ParityBatch:
 
 
 def run_parity(batch: ParityBatch, sz: dict, dt_s: float, period_s: float,
-               record_trace: bool = False, device=None) -> dict:
-    """Run the bitwise-parity integrator; returns numpy per-patient outputs."""
+               record_trace: bool = False, device=None, fetch: bool = True) -> dict:
+    """Run the bitwise-parity integrator; returns numpy per-patient outputs
+    (fetch=False: the device tensors, still being computed on the current
+    stream -- ``fetch_parity`` reads them; the inputs are stream-ordered, so
+    their memory is reused only after the launch)."""
     device = require_device(device)
     t = torch()
     n = batch.params.shape[0]
@@ -167,8 +170,11 @@ def run_parity(batch: ParityBatch, sz: dict, dt_s: float, period_s: float,
     for k, v in out.items():
         setattr(a, k, ptr(v))
     check(_lib.load().gt_simulate_parity(C.byref(a), stream_ptr(device)), "gt_simulate_parity")
-    res = {k: (v.cpu().numpy() if v is not None else None) for k, v in out.items()}
-    return res
+    return fetch_parity(out) if fetch else out
+
+
+def fetch_parity(out: dict) -> dict:
+    return {k: (v.cpu().numpy() if v is not None else None) for k, v in out.items()}
 
 
 # -------------------------------------------------------------- fast path

@@ -150,7 +150,7 @@ def _stats_from_parity(out: dict, i: int, config, sz) -> PatientStats:
     return st
 
 
-def _parity_run(items, config, hyper, device, record_trace=False, controller=0, noise=None):
+def _parity_run(items, config, hyper, device, record_trace=False, controller=0, noise=None, fetch=True):
     """items: list of (pid, p[30], x0[16], c0[11], basal, ProtocolArrays);
     noise: (wiener [n,H,3], meas [n,H/ps], has_noise [n]) already drawn
     (hostprep), else drawn here from the reference's streams."""
@@ -178,7 +178,7 @@ def _parity_run(items, config, hyper, device, record_trace=False, controller=0, 
         meal_off=moff, meals=meals, ex_off=eoff, ex=ex, wiener=wiener, has_noise=has_noise,
         meas=meas, controller=int(controller))
     return engine.run_parity(batch, sz, config.dt_s, config.controller_period_s,
-                             record_trace=record_trace, device=device), sz
+                             record_trace=record_trace, device=device, fetch=fetch), sz
 
 
 def simulate_closed_loop(patient, parameter_set, protocol, controller, model,
@@ -314,7 +314,20 @@ def _run_trial_parity(population, generator, controller_id, profile, model_id, c
     done = 0
     tm = ({"setup": time.perf_counter() - t0, "prep_wait": 0.0, "device": 0.0, "fold": 0.0}
           if os.environ.get("GLUCOSIM_PARITY_TIMING") else None)
-    nxt = None
+    def fold(idx, out_d):
+        out = engine.fetch_parity(out_d)
+        for j, i in enumerate(idx):
+            if int(out["status"][j]) != GT_STATUS_OK:
+                acc.add_aborted(int(ids[i]))
+                continue
+            acc.add_patient(int(ids[i]), _stats_from_parity(out, j, config, sz))
+            if record and trace_dir is not None:
+                save_trace(os.path.join(trace_dir, f"patient_{int(ids[i]):06d}.npz"), out["trace"][j])
+        if progress:
+            progress(idx[-1] + 1, len(population))
+        return idx[-1] + 1
+
+    nxt, pending = None, None
     try:
         nxt = start(0) if spans else None
         for c, idx in enumerate(spans):
@@ -326,24 +339,26 @@ def _run_trial_parity(population, generator, controller_id, profile, model_id, c
             tb = time.perf_counter()
             m = len(idx)
             items = [(int(ids[i]), params[i], x0[i], c0[i], basal[i], pa) for i, pa in zip(idx, pas)]
-            out, _sz = _parity_run(items, config, hyper, device, record_trace=record, controller=code,
-                                   noise=(block.wiener[:m], block.meas[:m], flags[idx, 0].astype(np.uint8)))
+            # launched without waiting (its inputs are copied before the call returns):
+            # the previous chunk is folded on the host while this one runs
+            out_d, _sz = _parity_run(items, config, hyper, device, record_trace=record, controller=code,
+                                     noise=(block.wiener[:m], block.meas[:m], flags[idx, 0].astype(np.uint8)),
+                                     fetch=False)
             tc = time.perf_counter()
             if tm is not None:
                 tm["prep_wait"] += tb - ta
                 tm["device"] += tc - tb
-            for j, i in enumerate(idx):
-                if int(out["status"][j]) != GT_STATUS_OK:
-                    acc.add_aborted(int(ids[i]))
-                    continue
-                acc.add_patient(int(ids[i]), _stats_from_parity(out, j, config, sz))
-                if record and trace_dir is not None:
-                    save_trace(os.path.join(trace_dir, f"patient_{int(ids[i]):06d}.npz"), out["trace"][j])
-            done = idx[-1] + 1
+            if pending is not None:
+                done = fold(*pending)
+            pending = (idx, out_d)
             if tm is not None:
                 tm["fold"] += time.perf_counter() - tc
-            if progress:
-                progress(done, len(population))
+        if pending is not None:
+            td = time.perf_counter()
+            done = fold(*pending)
+            pending = None
+            if tm is not None:
+                tm["fold"] += time.perf_counter() - td
     finally:
         if nxt is not None:
             try:
