@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import atexit
 import os
+import threading
 from concurrent.futures import ProcessPoolExecutor
 from multiprocessing import get_context
 from multiprocessing.shared_memory import SharedMemory
@@ -98,6 +99,9 @@ class NoiseBlock:
 
 
 _BLOCKS: dict = {}
+# one bitwise trial at a time uses the cached blocks (threads of one process
+# running trials concurrently take turns)
+LOCK = threading.Lock()
 
 
 def blocks(n: int, horizon_ticks: int, n_ctl: int, shared: bool, count: int = 2) -> list:

@@ -298,7 +298,7 @@ def _run_trial_parity(population, generator, controller_id, profile, model_id, c
     # device reads the other
     nb = min(chunk, len(run))
     use_pool = nb >= 64 and hostprep.pool() is not None
-    blocks = hostprep.blocks(nb, H, H // ps, use_pool, count=min(2, len(spans))) if spans else []
+    blocks = []
 
     def start(c):
         # host inputs of chunk c (protocols + the reference's noise streams),
@@ -328,7 +328,9 @@ def _run_trial_parity(population, generator, controller_id, profile, model_id, c
         return idx[-1] + 1
 
     nxt, pending = None, None
+    hostprep.LOCK.acquire()
     try:
+        blocks = hostprep.blocks(nb, H, H // ps, use_pool, count=min(2, len(spans))) if spans else []
         nxt = start(0) if spans else None
         for c, idx in enumerate(spans):
             ta = time.perf_counter()
@@ -365,6 +367,7 @@ def _run_trial_parity(population, generator, controller_id, profile, model_id, c
                 nxt.result()   # let in-flight workers finish with the block before it goes
             except Exception:
                 pass
+        hostprep.LOCK.release()
     if tm is not None:
         print(f"parity run_trial: {len(spans)} chunks of <= {chunk}; " +
               ", ".join(f"{k} {v:.3f} s" for k, v in tm.items()), flush=True)
