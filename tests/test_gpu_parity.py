@@ -144,8 +144,9 @@ def test_c1_parity_subset_1000_patients_4_weeks(dev, oracle, controller):
     print(f"C1 {controller}: {len(exc)} proven threshold ties of 1000 patients")
 
 
-@pytest.mark.parametrize("controller", ["dual_hormone", "pid_pump"])
-def test_c1_parity_subset_northern_year(dev, oracle, controller):
+@pytest.mark.parametrize("controller,dt_s,n,days", [("dual_hormone", 60.0, 1000, 28), ("pid_pump", 60.0, 1000, 28),
+                                                    ("dual_hormone", 30.0, 500, 14)])
+def test_c1_parity_subset_northern_year(dev, oracle, controller, dt_s, n, days):
     """The reference's own configuration at BASELINE configs[1] scale: the
     first 1 000 patients of the seed-1 device population x 4 weeks at dt 60 s
     on the NorthernYear protocol (weight-scaled meals, announced exercise;
@@ -153,7 +154,9 @@ def test_c1_parity_subset_northern_year(dev, oracle, controller):
     kernel (gt_northern.cu) and built on the host for the oracle, the
     reference's own noise streams injected.  The parity kernel equals the
     oracle bit for bit on every output; the fused kernel agrees to 1e-9 with
-    identical histograms and hypo events except proven threshold ties."""
+    identical histograms and hypo events except proven threshold ties.
+    The third case is the reference's own defaults end to end: its controller,
+    its protocol and its default 30 s step (simulation.py:75), 500 x 2 weeks."""
     import torch
     from paper_2202_13927_b200 import engine, rng
     from paper_2202_13927_b200.config import SimulationConfig
@@ -164,14 +167,14 @@ def test_c1_parity_subset_northern_year(dev, oracle, controller):
     from paper_2202_13927_b200.protocol import compile_protocol
     from paper_2202_13927_b200.simulation import _csr
     from paper_2202_13927_b200.trial import FastTrial
-    cfg = SimulationConfig(horizon_s=28 * 86400.0, seed=1, dt_s=60.0)
+    cfg = SimulationConfig(horizon_s=days * 86400.0, seed=1, dt_s=dt_s)
     prof = PIDProfile() if controller == "pid_pump" else ControllerHyperparameters()
     code = 1 if controller == "pid_pump" else 0
     gen = NorthernYearProtocol()
     assert gen.on_device()
-    pop = generate_population(1, 1000, device=dev, on_exhausted="redraw_weight")
+    pop = generate_population(1, n, device=dev, on_exhausted="redraw_weight")
     exc, n_ex_sessions, n_hypo = [], 0, 0
-    for lo in range(0, 1000, 250):
+    for lo in range(0, n, 250):
         hi = lo + 250
         ft = FastTrial(lo, pop.params_device[lo:hi].contiguous(), pop.basal_device[lo:hi].contiguous(), gen,
                        prof, cfg, controller_id=controller, device=dev)
@@ -212,9 +215,9 @@ def test_c1_parity_subset_northern_year(dev, oracle, controller):
         exc += ties.check_patients(oracle, dev, hi - lo, refd, fused,
                                    ties.inputs_from_arrays(params, x0, c0, ub, prof.to_vec(), moff, meals, eoff, ex,
                                                            W, hn, M, code, sz, cfg.dt_s, cfg.controller_period_s, lo),
-                                   label=f"C1 NorthernYear {controller} [{lo}, {hi})")
-    assert n_ex_sessions >= 1000 * 4     # announced exercise: 76 sessions a year, ~5.5 in 4 weeks
-    print(f"C1 NorthernYear {controller}: {len(exc)} proven threshold ties of 1000 patients; "
+                                   label=f"C1 NorthernYear {controller} dt {dt_s} [{lo}, {hi})")
+    assert n_ex_sessions >= n * days // 7   # announced exercise: 76 sessions a year, ~5.5 in 4 weeks
+    print(f"C1 NorthernYear {controller} dt {dt_s}: {len(exc)} proven threshold ties of {n} patients; "
           f"{n_ex_sessions} exercise sessions, {n_hypo} hypo events (<3.9) in the reference run")
 
 
