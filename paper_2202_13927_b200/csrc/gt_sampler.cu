@@ -339,19 +339,44 @@ __device__ __noinline__ void draw_attempt(const gt_sampler_args& a, uint32_t act
   }
 }
 
-// The parked patients, one block each: thread t evaluates attempt a0 + t of
-// the current body weight (cheap rules, then the steady-state solve of the
-// survivors), the lowest accepted attempt wins, and only the attempts before
-// it are counted -- exactly the sequential loop's result and rejection
-// counts, 128 attempts per round.
+// The parked patients, one block each.  A round takes the next kStragBS x
+// kStragC attempts of the current body weight: every thread applies the cheap
+// rules to kStragC consecutive attempts, the survivors are compacted in
+// attempt order (block scan) and solved in parallel, the lowest accepted
+// attempt wins, and only the attempts before it are counted -- exactly the
+// sequential loop's result and rejection counts.  A body weight that never
+// succeeds (its 10 000-attempt budget spent) takes 3 rounds, each about one
+// solve long, instead of 20.
+#ifndef GT_STRAG_C
+#define GT_STRAG_C 8
+#endif
+constexpr int kStragC = GT_STRAG_C;
+
+// cheap-rule code of one attempt: 1 a negative value, 2 outside one SD, 3 survivor
+__device__ __forceinline__ int cheap_code(const gt_sampler_args& a, const KeyRule* rules, uint32_t actr,
+                                          uint32_t pid, uint32_t k0, uint32_t k1) {
+  bool neg = false, outside = false;   // the normal draws' keys (as sampler_kernel's phase 1)
+  for (int q = 0; q < a.n_sampled; q += 2) {
+    const bool n0 = a.kind[q] == 0, n1 = q + 1 < a.n_sampled && a.kind[q + 1] == 0;
+    if (!(n0 || n1)) continue;
+    const U4 r = philox4x32_10(actr, pid, kRoleSamplerParams, (uint32_t)(q >> 1), k0, k1);
+    if (n0) key_verdict(a, rules[q], q, key52(r.x, r.y), neg, outside);
+    if (n1) key_verdict(a, rules[q + 1], q + 1, key52(r.z, r.w), neg, outside);
+  }
+  return neg ? 1 : (outside ? 2 : 3);
+}
+
 __global__ void __launch_bounds__(kStragBS) straggler_kernel(gt_sampler_args a, const KeyRule* rules,
                                                         const Straggler* park,
                                                         const unsigned int* n_park, int park_cap,
                                                         unsigned int* next) {
-  __shared__ int s_amin, s_last, s_j;
+  __shared__ int s_amin, s_last, s_j, s_nsurv;
+  __shared__ int s_wsum[kStragBS / 32];
+  __shared__ int s_list[kStragBS * kStragC];            // survivors' attempt numbers, in order
+  __shared__ unsigned char s_code[kStragBS * kStragC];  // their outcome: 3 no steady state, 4 basal, 5 accepted
   __shared__ KeyRule s_rules[kMaxSampled];
   for (int q = threadIdx.x; q < a.n_sampled; q += blockDim.x) s_rules[q] = rules[q];
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
   const int n_list = min((int)*n_park, park_cap);
   long long rej[4] = {0, 0, 0, 0};
@@ -381,43 +406,74 @@ __global__ void __launch_bounds__(kStragBS) straggler_kernel(gt_sampler_args a, 
         a0 = 0;
         continue;
       }
-      const int32_t att = a0 + t;
-      const bool valid = att < a.max_attempts;
-      const uint32_t actr = (uint32_t)(total + att);
-      int reason = 0;        // 1 negative, 2 outside 1 SD, 3 no steady state, 4 basal, 5 accepted
-      double ub = 0.0;
-      if (valid) {
-        bool neg = false, outside = false;   // the normal draws' keys (as sampler_kernel's phase 1)
-        for (int q = 0; q < a.n_sampled; q += 2) {
-          const bool n0 = a.kind[q] == 0, n1 = q + 1 < a.n_sampled && a.kind[q + 1] == 0;
-          if (!(n0 || n1)) continue;
-          const U4 r = philox4x32_10(actr, pid, kRoleSamplerParams, (uint32_t)(q >> 1), k0, k1);
-          if (n0) key_verdict(a, s_rules[q], q, key52(r.x, r.y), neg, outside);
-          if (n1) key_verdict(a, s_rules[q + 1], q + 1, key52(r.z, r.w), neg, outside);
-        }
-        if (neg) reason = 1;
-        else if (outside) reason = 2;
-        else {
-          draw_attempt(a, actr, pid, k0, k1, vals);
-          for (int q = 0; q < a.n_sampled; ++q) p[a.param_index[q]] = vals[q];
-          if (!steady_state_dev(p, a.target_bg, x, &ub)) reason = 3;
-          else reason = ub < a.min_basal_uh ? 4 : 5;
-        }
+      // ---- 1. cheap rules on kStragC consecutive attempts per thread
+      const int32_t base = a0 + t * kStragC;
+      unsigned codes = 0;   // 2 bits per attempt: 0 past the budget, else cheap_code
+      int n_s = 0;
+      for (int c = 0; c < kStragC; ++c) {
+        const int32_t att = base + c;
+        if (att >= a.max_attempts) break;
+        const int code = cheap_code(a, s_rules, (uint32_t)(total + att), pid, k0, k1);
+        codes |= (unsigned)code << (2 * c);
+        n_s += code == 3;
       }
+      // ---- 2. survivors compacted in attempt order (block exclusive scan)
+      int incl = n_s;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      if (lane == 31) s_wsum[wid] = incl;
       if (t == 0) { s_amin = INT_MAX; s_last = -1; }
       __syncthreads();
-      if (reason == 5) atomicMin(&s_amin, att);
+      if (t == 0) {
+        int run = 0;
+        for (int w2 = 0; w2 < kStragBS / 32; ++w2) { const int v = s_wsum[w2]; s_wsum[w2] = run; run += v; }
+        s_nsurv = run;
+      }
+      __syncthreads();
+      int pos = s_wsum[wid] + incl - n_s;
+      for (int c = 0; c < kStragC; ++c)
+        if (((codes >> (2 * c)) & 3u) == 3u) s_list[pos++] = base + c;
+      __syncthreads();
+      const int n_surv = s_nsurv;
+      // ---- 3. the survivors' values and steady-state solves, in parallel
+      for (int q = t; q < n_surv; q += kStragBS) {
+        const int32_t att = s_list[q];
+        double ub = 0.0;
+        draw_attempt(a, (uint32_t)(total + att), pid, k0, k1, vals);
+        for (int m = 0; m < a.n_sampled; ++m) p[a.param_index[m]] = vals[m];
+        const int code = !steady_state_dev(p, a.target_bg, x, &ub) ? 3 : (ub < a.min_basal_uh ? 4 : 5);
+        s_code[q] = (unsigned char)code;
+        if (code == 5) atomicMin(&s_amin, att);
+      }
       __syncthreads();
       const int amin = s_amin;
-      const bool counted = valid && att <= amin;   // attempts the sequential loop reaches
-      if (counted && reason >= 3) atomicMax(&s_last, (int)actr);
-      if (counted && reason >= 1 && reason <= 4) ++rej[reason - 1];
+      // ---- 4. count what the sequential loop reaches (attempts <= amin)
+      for (int c = 0; c < kStragC; ++c) {
+        const unsigned code = (codes >> (2 * c)) & 3u;
+        if ((code == 1u || code == 2u) && base + c < amin) ++rej[code - 1];
+      }
+      int mine = -1;   // the list entry of the accepted attempt, if this thread holds it
+      for (int q = t; q < n_surv; q += kStragBS) {
+        const int32_t att = s_list[q];
+        if (att > amin) continue;
+        const int code = s_code[q];
+        if (code == 3 || code == 4) ++rej[code - 1];
+        atomicMax(&s_last, (int)(total + att));   // the latest survivor reached (accepted included)
+        if (att == amin) mine = q;
+      }
       __syncthreads();
       if (s_last >= 0) last_surv = s_last;
       if (amin != INT_MAX) {
         total += amin + 1;
         status = 0;
-        if (att == amin) {   // the accepted attempt writes the patient
+        if (mine >= 0) {   // the accepted attempt writes the patient (its solve repeated: same values)
+          double ub = 0.0;
+          draw_attempt(a, (uint32_t)(total - 1), pid, k0, k1, vals);
+          for (int m = 0; m < a.n_sampled; ++m) p[a.param_index[m]] = vals[m];
+          steady_state_dev(p, a.target_bg, x, &ub);
           for (int k = 0; k < GT_N_PARAMS; ++k) a.params[i * GT_N_PARAMS + k] = p[k];
           for (int k = 0; k < GT_N_STATES; ++k) a.x0[i * GT_N_STATES + k] = x[k];
           a.u_basal_uh[i] = ub;
@@ -426,7 +482,7 @@ __global__ void __launch_bounds__(kStragBS) straggler_kernel(gt_sampler_args a, 
         }
         break;
       }
-      a0 += blockDim.x;
+      a0 += kStragBS * kStragC;
       __syncthreads();
     }
     if (status != 0 && t == 0) {   // exhausted: the sequential loop's last p (latest survivor's values)
