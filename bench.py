@@ -518,7 +518,7 @@ def run_ours(args):
     peak, peak_burst, peak_src = fp64_peak()
     achieved = flop_per_launch / sim_s / 1e12
     cpu_v, cpu_wall, cpu_kind, cpu_sample = None, None, None, None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and ws == 1:   # the CPU baseline: rank 0 at N = 1 only
         threads = os.cpu_count() or 1
         cpu_v, cpu_wall, cpu_kind, cpu_sample = cpu_reference_or_port(WEEKS, threads, args.controller)
     q = analytics.metric_quantiles(acc_all)
