@@ -120,3 +120,19 @@ def test_parity_rejects_a_short_day_buffer(lib):
 def test_fast_rejects_negative_slice_count(lib):
     rc, msg = _call_fast(lib, _fast_args(n_slices=-3))
     assert rc == -1 and "n_slices" in msg, (rc, msg)
+
+
+def test_fast_rejects_a_launch_too_large_for_its_offsets(lib):
+    """Maximum size: one fused launch holds fewer than 2^31 / 247 patients (the
+    histogram drain forms 32-bit element offsets); a larger one is refused
+    with GT_EINVAL before any CUDA call (no GPU needed), telling the caller to
+    shard."""
+    buf = C.create_string_buffer(64)
+    a = _fast_args(n=9_000_000)
+    for name, typ in a._fields_:
+        if typ is C.c_void_p:
+            setattr(a, name, C.addressof(buf))
+        elif isinstance(typ, type) and issubclass(typ, C._Pointer):
+            setattr(a, name, C.cast(C.addressof(buf), typ))
+    rc, msg = _call_fast(lib, a)
+    assert rc == -1 and "shard" in msg, (rc, msg)
