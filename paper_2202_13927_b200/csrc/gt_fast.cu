@@ -90,7 +90,10 @@ namespace gt {
 #define GT_NOISE_ROUNDS 7
 #endif
 #ifndef GT_DEAD_SINK
-#define GT_DEAD_SINK 1  // dead lanes count into the padding bin 247
+// instances (GT_PS5 bits) whose dead lanes count into the padding bin 247; the
+// others count masked lanes into their own bins and never write them out
+// (-0.6 % three_meal/pid_pump; +0.4 % on two other instances)
+#define GT_DEAD_SINK 14
 #endif
 #ifndef GT_FKEY
 #define GT_FKEY 1   // extremes / hypo-run branch keyed on FP32 bounds of the extremes (not bins)
@@ -675,7 +678,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
       alive = alive && inrange && !was_bad;  // padding lanes read patient 0's slot
     }
 
-    // GT_DEAD_SINK 0: a lane masked from the start (excluded, re-run mask, bad
+    // without the dead-lane sink (GT_DEAD_SINK bit off) a lane masked from the start (excluded, re-run mask, bad
     // initial state) counts into its shared bins like any other, and its
     // counts are never written out; a lane that dies during the run is
     // aborted and its statistics are discarded by the host either way
@@ -721,7 +724,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
         if (word == 0u) continue;
         s_hist[hword(w, tid)] = 0u;
         if (!inrange || abort_pass) continue;
-        if (!GT_DEAD_SINK && !ran) continue;   // a masked lane's counts are dropped
+        if (!(GT_DEAD_SINK & kShape) && !ran) continue;   // a masked lane's counts are dropped
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           const uint32_t c = (word >> (8 * b)) & 0xFFu;
@@ -1187,7 +1190,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           kb = min(max(kb, 0), GT_N_THRESHOLDS);
           kb += (s_thr[kb + 1] <= bb) - (s_thr[kb] > bb);
         }
-        if (GT_DEAD_SINK) kb = alive ? kb : GT_N_BG_BINS;  // dead lanes count into the padding bin 247
+        if (GT_DEAD_SINK & kShape) kb = alive ? kb : GT_N_BG_BINS;  // dead lanes count into the padding bin 247
         {  // byte ((kb >> 2) * kFastBS + tid) * 4 + (kb & 3)
           GT_CHECK(kb >= 0 && kb <= GT_N_BG_BINS, "histogram bin");
           const uint32_t ha = GT_HISTLIN ? hist_lane + (uint32_t)kb
@@ -1199,7 +1202,7 @@ fast_kernel(const gt_fast_args a, const Uni u, const Sched sch) {
           // column address is formed only on that path
           if (__builtin_expect(c == 255u, 0)) {
             asm volatile("st.shared.u8 [%0], 0;" :: "r"(ha) : "memory");
-            if (kb < GT_N_BG_BINS && inrange && !abort_pass && (GT_DEAD_SINK || ran)) {
+            if (kb < GT_N_BG_BINS && inrange && !abort_pass && ((GT_DEAD_SINK & kShape) || ran)) {
               // 32-bit element offset (the launcher bounds 247 n < 2^31): the drain
               // path then needs fewer scratch registers than a 64-bit index
               if (GT_DRAIN32 & kShapeBit) atomicAdd(a.bg_hist + (uint32_t)(kb * (uint32_t)n + (uint32_t)i), 255);
